@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark: OF-method iterations/s and HBM GB/s on B200 (BASELINE.json metric).
+
+A "step" is one iteration of Algorithm 2 on the whole graph: the
+fused chain C3 (update + direction) -> beta -> C4 (direction + Q, P Grams) ->
+[all-gather V] -> C2 (SpMM + T, R' Grams) -> Gram reduce -> [all-reduce] ->
+exact line search.  Workload: BASELINE config c4 (DCSBM N = 5M, 50M edges,
+k = 64, fp64), rows partitioned over N GPUs (strong scaling on the same graph).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value`  = K / (max over ranks of the CUDA-event time of the K iterations).
+`e2e`    = the same metric through ofsc_spectral_cluster (C ABI, Algorithm 1
+           end to end) from pinned HOST buffers: edge upload + graph build +
+           T_e2e iterations + row normalise + K-means + feature/label download.
+`roofline` = the dominant kernel's algorithmic bytes per launch / its average
+           CUDA-event duration (profiled pass on the same stream), vs the
+           measured HBM copy peak (MEASURED_PEAKS.json).
+`cpu_baseline` = the oracle (numpy/scipy, as it stands) on the host cores.
+The reference arm (--impl reference) times the oracle the same way.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, config_graph, x0_block, kmeans_init_rows  # noqa: E402
+
+METRIC = "OF-method iterations/sec and HBM GB/s (fraction of peak) at 1/2/4/8 B200"
+PHASES = ("update_direction", "beta", "direction_gram", "spmm_gram", "gram_reduce",
+          "line_search", "refresh", "comm")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--method", default="ofm_f2")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--refresh", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-methods", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy kernel)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_desc(cfg, dtype):
+    return (f"{cfg.name}: DCSBM N={cfg.n:,}, {cfg.blocks} blocks, E={cfg.edges:,} "
+            f"(avg deg {2 * cfg.edges / cfg.n:.0f}), within:between {cfg.ratio:g}:1, "
+            f"power-law degrees (exp -2.1, 10-100), k={cfg.k}, {dtype}")
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev_index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(cfg_n_local, nnz_local, n_global, k, es):
+    """Compulsory bytes per launch of each hot kernel."""
+    B = cfg_n_local * k * es
+    return {
+        # C2: V once (own rows; every gathered row is a row of V), X, write AV, CSR + s
+        "spmm_gram": 3 * B + 4 * nnz_local + 8 * (cfg_n_local + 1) + 8 * n_global,
+        # C3: read X, V, AX, AV, Gp; write X, AX, G
+        "update_direction": 8 * B,
+        # C4: read G, Vp, X; write V
+        "direction_gram": 4 * B,
+    }
+
+
+def iteration_bytes(n_local, nnz_local, n_global, k, es):
+    """Compulsory bytes of one whole iteration: 15 N x k block passes + CSR + s."""
+    B = n_local * k * es
+    return 15 * B + 4 * nnz_local + 8 * (n_local + 1) + 8 * n_global
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2305_10356_b200 as ofsc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = ofsc.Comm()
+    cfg = CONFIGS[args.config]
+    k = cfg.k
+    es = 8 if args.dtype == "f64" else 4
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    t0 = time.time()
+    src, dst, labels = config_graph(cfg)
+    gen_s = time.time() - t0
+    stream = torch.cuda.current_stream()
+
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a.record(stream)
+    g = ofsc.Graph(cfg.n, src, dst, comm=comm)
+    ev_b.record(stream)
+    torch.cuda.synchronize()
+    build_ms = ev_a.elapsed_time(ev_b)
+    info = g.info
+    rb, re_ = info["row_begin"], info["row_end"]
+    X0 = x0_block(cfg.n, k, cfg.seed_x0)[rb:re_]
+    X0d = torch.from_numpy(X0).to(tdt).cuda()
+    W, K = args.warmup, args.steps
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed_run(method, profile=False):
+        X = X0d.clone()
+        barrier()
+        r = ofsc.run(g, method, X, W + K, timing_skip=W, profile=profile, refresh=args.refresh)
+        barrier()
+        return r.report
+
+    # --- headline: K timed iterations after W warm-up iterations ---
+    clk = Clocks(local)
+    rep = timed_run(args.method)
+    clocks = clk.stop()
+    ms = max_over_ranks(rep["timed_ms"])
+    value = K / (ms / 1e3)
+
+    # --- per-kernel profile pass (CUDA events per launch, same stream) ---
+    prep = timed_run(args.method, profile=True)
+    kern = {PHASES[i]: {"ms_total": prep["kernel_ms"][i], "launches": prep["kernel_launches"][i]}
+            for i in range(8) if prep["kernel_launches"][i] or prep["kernel_ms"][i]}
+    dom = max(("spmm_gram", "update_direction", "direction_gram"),
+              key=lambda n: kern.get(n, {}).get("ms_total", 0.0))
+    nl = re_ - rb
+    algo = algorithmic_bytes(nl, info["nnz_local"], cfg.n, k, es)
+    avg_ms = kern[dom]["ms_total"] / max(kern[dom]["launches"], 1)
+    hbm_peak, peak_src = peaks()
+    achieved = algo[dom] / (avg_ms / 1e3) / 1e9
+    traffic = load_traffic()
+    tr_bytes = None
+    if traffic and traffic.get("config") == cfg.name and traffic.get("kernel") == dom:
+        tr_bytes = traffic.get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "traffic": tr_bytes, "algorithmic_bytes_per_launch": algo[dom],
+                "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src,
+                "share_of_step": round(kern[dom]["ms_total"] / max(sum(v["ms_total"] for v in kern.values()), 1e-9), 3)}
+    it_bytes = iteration_bytes(nl, info["nnz_local"], cfg.n, k, es)
+    iter_hbm = it_bytes * value / 1e9 / max(world, 1) if world == 1 else it_bytes * (K / (ms / 1e3)) / 1e9
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "it/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic seeded DCSBM graph (stands in for the Graph Challenge SBM graphs, P:583-584)",
+        "config": {"workload": workload_desc(cfg, args.dtype), "method": args.method, "k": k,
+                   "refresh": args.refresh, "global_batch": cfg.n, "parallelism": f"row-partition p={world}",
+                   "l2": "inputs larger than L2 (each N x k block 2.56 GB vs 126 MB L2)" if cfg.n * k * es > 2e8 else "working set partly L2-resident",
+                   "graph_gen_s": round(gen_s, 1), "graph_build_ms": round(build_ms, 2),
+                   "load_imbalance": info["load_imbalance"]},
+        "roofline": roofline,
+        "iteration_hbm": {"algorithmic_bytes_per_iter_per_gpu": it_bytes,
+                          "achieved_gbs_per_gpu": round(it_bytes * (K / (ms / 1e3)) / 1e9, 1),
+                          "frac": round(it_bytes * (K / (ms / 1e3)) / 1e9 / hbm_peak, 4)},
+        "kernels": kern,
+        "gpu_launches": rep["launches"],
+        "clocks": clocks,
+    }
+    del iter_hbm
+
+    # --- all four methods, same protocol ---
+    if not args.no_methods:
+        per = {}
+        for m in ofsc.METHODS:
+            r = timed_run(m)
+            per[m] = round(K / (max_over_ranks(r["timed_ms"]) / 1e3), 3)
+        out["per_method_it_s"] = per
+
+    # --- e2e through the C ABI with pinned host buffers ---
+    if not args.no_e2e:
+        out["e2e"] = run_e2e(args, cfg, comm, src, dst, X0, world, rank, barrier, max_over_ranks)
+
+    # --- CPU baseline: the oracle on the host cores (rank 0, N = 1 only) ---
+    if world == 1 and rank == 0 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(cfg, args.method, src, dst, X0)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    g.close()
+    if comm:
+        comm.close()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, cfg, comm, src, dst, X0, world, rank, barrier, max_over_ranks):
+    import ctypes as C
+    import torch
+    import paper_2305_10356_b200 as ofsc
+    L = ofsc.lib()
+    T = cfg.iters
+    k = cfg.k
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    h_src = torch.from_numpy(src).pin_memory()
+    h_dst = torch.from_numpy(dst).pin_memory()
+    h_X0 = torch.from_numpy(X0).to(tdt).pin_memory()
+    h_X = torch.empty_like(h_X0).pin_memory()
+    rows = torch.from_numpy(kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)).pin_memory()
+    h_lab = torch.empty(X0.shape[0], dtype=torch.int32).pin_memory()
+    o = ofsc.make_opts(k, T, refresh=args.refresh)
+    stream = torch.cuda.current_stream()
+    times = []
+    for step in range(1 + args.e2e_steps):
+        h_X.copy_(h_X0)                        # untimed host-side reset of the in/out buffer
+        rep = ofsc.Report()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record(stream)
+        st = L.ofsc_spectral_cluster(comm.handle if comm else None, cfg.n, src.size,
+                                     C.c_void_p(h_src.data_ptr()), C.c_void_p(h_dst.data_ptr()),
+                                     ofsc.METHODS[args.method], ofsc.DTYPES[args.dtype], C.byref(o),
+                                     C.c_void_p(h_X.data_ptr()), cfg.blocks,
+                                     C.c_void_p(rows.data_ptr()), 100,
+                                     C.c_void_p(h_lab.data_ptr()), C.byref(rep),
+                                     C.c_void_p(stream.cuda_stream))
+        b.record(stream)
+        barrier()
+        ofsc._check(st)
+        if step >= 1:
+            times.append(max_over_ranks(a.elapsed_time(b)))
+    ms = statistics.mean(times)
+    ari, nmi = (None, None)
+    if world == 1:
+        ari, nmi = ofsc.scores(h_lab.numpy(), config_graph(cfg)[2])
+    es = 8 if args.dtype == "f64" else 4
+    h2d = src.nbytes + dst.nbytes + X0.shape[0] * k * es + rows.numel() * 8
+    d2h = X0.shape[0] * k * es + X0.shape[0] * 4
+    return {"value": round(T / (ms / 1e3), 3), "unit": "it/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_call": round(ms, 2), "iters_per_call": T,
+            "calls_timed": len(times),
+            "what": "ofsc_spectral_cluster: edge H2D + GPU CSR build + T iterations + row "
+                    "normalise + K-means (K = planted blocks, <= 100 Lloyd steps) + D2H",
+            "ari_vs_planted": ari, "nmi_vs_planted": nmi}
+
+
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(th) if th else 1
+    except Exception:
+        return 1
+
+
+def cpu_baseline(cfg, method, src, dst, X0, iters=2):
+    """Oracle (numpy + scipy, as it stands) on the host: `iters` iterations of Algorithm 2."""
+    from oracle import build_operator, run_ofm
+    op = build_operator(cfg.n, src, dst)
+    marks = []
+    t0 = time.perf_counter()
+    run_ofm(op, method, X0, iters, refresh=0, callback=lambda t: marks.append(time.perf_counter()))
+    tot = marks[-1] - t0
+    per = (marks[-1] - marks[0]) / (iters - 1) if iters > 1 else tot
+    return {"value": round(1.0 / per, 5), "unit": "it/s", "cores": oracle_threads(),
+            "kind": "oracle", "host_cpus": os.cpu_count(),
+            "sample": f"{cfg.name} full graph, {method}, {iters} oracle iterations (refresh=0), "
+                      f"per-iteration time from iteration 2 (first includes setup); scipy SpMM "
+                      f"single-threaded, BLAS Grams with {oracle_threads()} threads"}
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """Reference arm: the oracle, as it stands, on this box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import build_operator, run_ofm
+    cfg = CONFIGS[args.config]
+    src, dst, _ = config_graph(cfg)
+    X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
+    op = build_operator(cfg.n, src, dst)
+    W, K = args.warmup, args.steps
+    marks = []
+    run_ofm(op, args.method, X0, W + K, refresh=0,
+            callback=lambda t: marks.append(time.perf_counter()))
+    # step t ends at marks[t]; the K timed steps are W .. W+K-1
+    start = marks[W - 1] if W >= 1 else None
+    if start is None:
+        raise SystemExit("--warmup must be >= 1 for the reference arm")
+    sec = marks[W + K - 1] - start
+    value = K / sec
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "it/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(1e3 * sec / K, 2),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic seeded DCSBM graph", "config": {"workload": workload_desc(cfg, "f64"),
+                                                         "method": args.method, "k": cfg.k},
+        "cpu_baseline": {"value": round(value, 5), "unit": "it/s", "cores": oracle_threads(),
+                         "kind": "oracle", "sample": f"{K} full oracle iterations of {cfg.name} "
+                                                     f"after {W} warm-up iterations"},
+        "e2e": {"value": round(value, 5), "unit": "it/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

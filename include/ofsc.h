@@ -1,0 +1,238 @@
+/*
+ * libofsc -- orthogonalization-free spectral clustering on B200 (sm_100a).
+ *
+ * C ABI of the data-parallel hot path of arXiv 2305.10356
+ * ("P:n" = /root/reference/PAPER.md line n).
+ *
+ *   Alg. 1 l.2   build A = L - 2I from an undirected edge list ....... ofsc_graph_build
+ *   Alg. 1 l.3   run OFM-f1 / TriOFM-f1 / OFM-f2 / TriOFM-f2 ......... ofsc_run
+ *                       (Algorithm 2)
+ *   Alg. 1 l.4   normalise each row of the features ................. ofsc_row_normalize
+ *   Alg. 1 l.5   Euclidean K-means (Lloyd) ........................... ofsc_kmeans
+ *   P:587               ARI / NMI of two labelings (host) .................. ofsc_scores
+ *   Alg. 1 end to end   host buffers in, labels out ........................ ofsc_spectral_cluster
+ *
+ * Conventions
+ *  - Pointers named d_* are CUDA device pointers, h_* are host pointers.  The
+ *    caller allocates and owns every array; the library owns the opaque handles
+ *    (graph, comm) and their device workspaces (freed by *_destroy).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Device work is stream-ordered.  Calls that fill host outputs (reports,
+ *    histories, info, *_out) synchronize `stream` before returning.
+ *  - Dense blocks (X, Y, features) are row-major with leading dimension ld >= k
+ *    (elements), fp64 (OFSC_F64) or fp32 (OFSC_F32).  fp32 means fp32 storage
+ *    of the N x k blocks and fp32 SpMM accumulation, with fp64 Grams, column
+ *    dots, k x k state and line search.
+ *  - Errors: every call returns an ofsc_status; no exception or exit() crosses
+ *    the ABI.  ofsc_last_error() gives a thread-local message for the last
+ *    failing call.  OFSC_ERR_ARG: null pointer, k < 1, k > n, k > OFSC_MAX_K,
+ *    ld < k, bad enum, rank/size mismatch.  OFSC_ERR_RANGE: edge endpoint
+ *    outside [0, n).  OFSC_ERR_CUDA / OFSC_ERR_NCCL: runtime failures.
+ *    OFSC_ERR_DIVERGED: a non-finite direction or step (X keeps the last
+ *    finite iterate).
+ *  - Multi-GPU: one process per GPU.  Rows are partitioned contiguously,
+ *    balanced by nnz; a rank's row range is ofsc_graph_info.row_begin/row_end
+ *    and every d_X / d_Y / d_labels argument is that rank's local row block.
+ *    comm == NULL means a single GPU.
+ *  - No CPU fallback: every numerical step runs in this library's sm_100a kernels.
+ */
+#ifndef OFSC_H
+#define OFSC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OFSC_MAX_K 64
+
+typedef enum {
+  OFSC_OK = 0,
+  OFSC_ERR_ARG = 1,
+  OFSC_ERR_RANGE = 2,
+  OFSC_ERR_NOMEM = 3,
+  OFSC_ERR_CUDA = 4,
+  OFSC_ERR_NCCL = 5,
+  OFSC_ERR_DIVERGED = 6,
+  OFSC_ERR_STATE = 7
+} ofsc_status;
+
+/* The paper's four methods: direction g and line-search cubic(s). */
+typedef enum {
+  OFSC_OFM_F1 = 0,    /* grad f1 = 4AX + 4XX^TX            eq:gradientf1 P:188-191 */
+  OFSC_TRIOFM_F1 = 1, /* g1 = AX + X triu(X^TX)            eq:gradientg1 P:209-212 */
+  OFSC_OFM_F2 = 2,    /* grad f2 = 4AX - 2XX^TAX - 2AXX^TX eq:gradientf2 P:232-235 */
+  OFSC_TRIOFM_F2 = 3  /* g2 = 2AX - AXtriu(X^TX) - Xtriu(X^TAX) eq:gradientg2 P:250-253 */
+} ofsc_method;
+
+typedef enum { OFSC_F64 = 0, OFSC_F32 = 1 } ofsc_dtype;
+
+/* Column-wise CG (Alg. 2 l.9): Polak-Ribiere, PR+ = max(beta, 0), or
+ * beta = 0 (steepest descent with exact line search). */
+typedef enum { OFSC_BETA_PR = 0, OFSC_BETA_PR_PLUS = 1, OFSC_BETA_ZERO = 2 } ofsc_beta_rule;
+
+typedef struct ofsc_comm_s* ofsc_comm;
+typedef struct ofsc_graph_s* ofsc_graph;
+typedef void* ofsc_stream;
+
+const char* ofsc_version(void);
+const char* ofsc_status_string(ofsc_status s);
+const char* ofsc_last_error(void);
+
+/* ---- communicator (NCCL over NVLink/NVSwitch) ---------------------------
+ * Rank 0 calls ofsc_get_unique_id and broadcasts the 128 bytes (e.g. with
+ * torch.distributed); every rank then calls ofsc_comm_create on its own GPU. */
+ofsc_status ofsc_get_unique_id(void* h_id128);
+ofsc_status ofsc_comm_create(const void* h_id128, int nranks, int rank, int cuda_device,
+                             ofsc_comm* out);
+ofsc_status ofsc_comm_destroy(ofsc_comm comm);
+
+/* ---- graph -> operator A = L - 2I (Alg. 1 l.2) ----------
+ * Canonical undirected edge set: self-loops dropped, duplicates collapsed
+ * (S_ij in {0,1}); d_i = |N(i)|, s_i = d_i^{-1/2} (0 if isolated);
+ * A_ii = -1, A_ij = -s_i s_j.  The CSR pattern (int64 row offsets, int32
+ * column ids sorted ascending per row) and s live on the device; values of A
+ * are implicit.  src/dst: m edges, host (edges_on_device = 0) or device
+ * pointers; every rank passes the full edge list.  Requires 1 <= n < 2^31. */
+typedef struct {
+  int64_t n;                    /* nodes */
+  int64_t n_edges_kept;         /* unique undirected non-loop edges */
+  int64_t nnz_global;           /* 2 * n_edges_kept (off-diagonal nnz of S) */
+  int64_t row_begin, row_end;   /* this rank's rows [row_begin, row_end) */
+  int64_t nnz_local;            /* off-diagonal nnz in this rank's rows */
+  int64_t n_isolated;           /* nodes with d_i = 0 */
+  int64_t n_self_loops_dropped;
+  int64_t n_duplicates_dropped;
+  int64_t max_degree;
+  double fro2_A;                /* ||A||_F^2 = n + sum_ij (s_i s_j)^2 */
+  double load_imbalance;        /* p * max_r nnz_r / nnz */
+} ofsc_graph_info;
+
+ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
+                             const int64_t* dst, int edges_on_device, ofsc_stream stream,
+                             ofsc_graph* out);
+ofsc_status ofsc_graph_info_get(ofsc_graph g, ofsc_graph_info* out);
+/* Copy this rank's CSR to host: h_row_ptr[n_local+1] (offsets from 0),
+ * h_col[nnz_local] (global ids), h_s[n] (full). Any pointer may be NULL. */
+ofsc_status ofsc_graph_copy_csr(ofsc_graph g, int64_t* h_row_ptr, int32_t* h_col, double* h_s);
+ofsc_status ofsc_graph_destroy(ofsc_graph g);
+
+/* Y = A Z for this rank's rows (the SpMM of eq:spmm P:440, values implicit).
+ * d_Z: all n rows (n x ldz) on every rank; d_Y: local rows (n_local x ldy). */
+ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_Z,
+                             int64_t ldz, void* d_Y, int64_t ldy, ofsc_stream stream);
+
+/* Kernel-level hook of the fused SpMM + Gram step: Y = A Z (local rows) and
+ * the k x k fp64 Grams d_grams[0..3] = Z^T Z, Z^T X, Z^T Y, X^T Y (row-major,
+ * 4 consecutive k x k blocks, summed over all ranks).  Z: n x ldz (all rows),
+ * X: local rows x ldx. */
+ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_Z,
+                                  int64_t ldz, const void* d_X, int64_t ldx, void* d_Y,
+                                  int64_t ldy, double* d_grams, ofsc_stream stream);
+
+/* ---- the orthogonalization-free iteration (Algorithm 2) ----- */
+typedef struct {
+  int32_t k;            /* features, 1 <= k <= min(n, OFSC_MAX_K) */
+  int32_t max_iters;    /* T: number of updates of X (tol = 0 runs exactly T) */
+  double tol;           /* 0 => fixed T (paper protocol); else stop when
+                           ||G||_F <= tol * c_m * ||X||_F, c_m = 4,1,2,1 */
+  int32_t beta_rule;    /* ofsc_beta_rule, default OFSC_BETA_PR_PLUS */
+  int32_t line_search;  /* 1 = exact line search; 0 = alpha_fixed */
+  double alpha_fixed;
+  int32_t refresh;      /* 1 = paper schedule: AX, X^TX, X^TAX recomputed every
+                           iteration (2 SpMMs); R > 1: recurrence
+                           AX += AV diag(alpha) + algebraic k x k update, recompute
+                           every R iterations; 0 = never recompute */
+  int32_t check_every;  /* with tol > 0: poll the device stop flag every n iterations */
+  int32_t timing_skip;  /* >= 0: CUDA-event time iterations [timing_skip, iters) on `stream`
+                           into ofsc_report.timed_ms; < 0: off */
+  int32_t profile;      /* 1: per-kernel CUDA-event timing into ofsc_report.kernel_ms
+                           (launches not captured in a CUDA graph); 0: off */
+} ofsc_opts;
+
+void ofsc_opts_default(ofsc_opts* o); /* k=0 (must be set), T=100, tol=0, PR+, exact LS,
+                                         refresh=0, check_every=8, timing_skip=-1, profile=0 */
+
+/* Kernel phases of one iteration, indices of ofsc_report.kernel_ms / kernel_launches. */
+enum {
+  OFSC_PH_UPDATE_DIRECTION = 0, /* C3: X += aV, AX += aAV, G = g_m(X), column dots */
+  OFSC_PH_BETA = 1,             /* k x k: beta, ||G||, objective, stop flags */
+  OFSC_PH_DIRECTION_GRAM = 2,   /* C4: V = -G + beta Vp, Q = V^T V, P = V^T X */
+  OFSC_PH_SPMM_GRAM = 3,        /* C2: AV = A V, T = V^T AV, R' = X^T AV */
+  OFSC_PH_GRAM_REDUCE = 4,      /* fixed-order reduction of per-CTA Gram partials */
+  OFSC_PH_LINE_SEARCH = 5,      /* k x k: cubics, roots, alpha, M/W update */
+  OFSC_PH_REFRESH = 6,          /* refresh iterations: X update, A X, X^T X, X^T A X */
+  OFSC_PH_COMM = 7,             /* NCCL collectives (p > 1) */
+  OFSC_NUM_PHASES = 8
+};
+
+typedef struct {
+  int32_t iters;              /* completed updates of X */
+  int32_t converged;          /* 1 if ||G|| hit the tolerance (or 0) */
+  int32_t diverged;           /* 1 if a direction or step was non-finite */
+  int32_t n_three_root_steps; /* line searches that selected among 3 real roots */
+  int32_t n_zero_steps;       /* degenerate (all-zero) cubics, alpha = 0 */
+  double grad_norm0, grad_norm, objective;
+  int32_t timed_iters;        /* iterations inside the timing window */
+  int32_t launches;           /* kernels this library launched inside the timing window */
+  double timed_ms;            /* CUDA-event time of the timing window (opts.timing_skip) */
+  double kernel_ms[8];        /* opts.profile: summed per-phase kernel time in the window */
+  int32_t kernel_launches[8]; /* opts.profile: launches per phase in the window */
+} ofsc_report;
+
+/* d_X (local rows x ldx, dtype dt): in = X0 or a warm start, out = features.
+ * h_history (optional, max_iters x 4): per iteration objective f(X_t), ||G_t||_F,
+ * min alpha_t, max alpha_t (NaN after a stop).  Synchronizes `stream`. */
+ofsc_status ofsc_run(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const ofsc_opts* opts,
+                     void* d_X, int64_t ldx, double* h_history, ofsc_report* rep,
+                     ofsc_stream stream);
+/* As ofsc_run, plus optional per-iteration step sizes and root-branch codes
+ * (host, max_iters x k each; codes as in DESIGN.md R9). */
+ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const ofsc_opts* opts,
+                        void* d_X, int64_t ldx, double* h_history, double* h_alphas,
+                        int32_t* h_codes, ofsc_report* rep, ofsc_stream stream);
+
+/* Kernel-level hook of the k x k exact line search (1 CTA on the device):
+ * given host Grams Q, P, T, R' = X^TAV, M = X^TX, W = X^TAX (k x k row-major
+ * each), return per-column alpha and branch codes (OFM methods broadcast
+ * one alpha) and the algebraically updated M, W (may be NULL). */
+ofsc_status ofsc_line_search(ofsc_method method, int32_t k, const double* h_Q, const double* h_P,
+                             const double* h_T, const double* h_Rp, const double* h_M,
+                             const double* h_W, double* h_alpha, int32_t* h_codes,
+                             double* h_M_out, double* h_W_out);
+
+/* ---- post-processing (Alg. 1 l.4-5) ------------------------------------- */
+/* y_i = x_i / ||x_i||_2, a zero row stays zero.  In-place allowed. */
+ofsc_status ofsc_row_normalize(ofsc_dtype dt, int64_t n_local, int32_t k, const void* d_X,
+                               int64_t ldx, void* d_Y, int64_t ldy, ofsc_stream stream);
+
+/* Lloyd K-means from given centroids d_centroids (K x dim fp64, in: init,
+ * out: final).  Assign: argmin_c sum_{d<dim} (y_d - C_cd)^2 (fp64, summed in
+ * d order, ties -> lowest c); update: cluster means (empty cluster keeps its
+ * centroid); stop when no label changes or after max_iters assignments.
+ * d_labels: int32 local rows.  iters_out / inertia_out optional host outputs. */
+ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t dim,
+                        const void* d_Y, int64_t ldy, int32_t n_clusters, double* d_centroids,
+                        int32_t max_iters, int32_t* d_labels, int32_t* iters_out,
+                        double* inertia_out, ofsc_stream stream);
+
+/* ARI and NMI (arithmetic-mean normalisation) of two host labelings. */
+ofsc_status ofsc_scores(int64_t n, const int32_t* h_a, const int32_t* h_b, double* ari,
+                        double* nmi);
+
+/* Algorithm 1 end to end from HOST buffers: edges (m, full list) -> build A ->
+ * run `method` from h_X (local rows x k, dense ld = k, dtype dt; in: X0, out:
+ * features before normalisation) -> row-normalise -> K-means with centroids
+ * initialised at the global rows h_init_rows[n_clusters] of the normalised
+ * features -> h_labels (local rows).  Copies host<->device inside the call. */
+ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t m, const int64_t* h_src,
+                                  const int64_t* h_dst, ofsc_method method, ofsc_dtype dt,
+                                  const ofsc_opts* opts, void* h_X, int32_t n_clusters,
+                                  const int64_t* h_init_rows, int32_t km_max_iters,
+                                  int32_t* h_labels, ofsc_report* rep, ofsc_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OFSC_H */

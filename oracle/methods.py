@@ -107,14 +107,16 @@ class OFMResult:
 
 
 def run_ofm(op: Operator, method: str, X0, T: int, *, tol=0.0, beta_rule="pr+",
-            line_search=True, alpha_fixed=0.0, refresh=1, precision="f64") -> OFMResult:
+            line_search=True, alpha_fixed=0.0, refresh=1, precision="f64",
+            callback=None) -> OFMResult:
     """Algorithm 2 for `T` iterations (T updates of X).
 
     refresh: 1 = the paper's schedule (A X, X^T X, X^T A X recomputed every
     iteration); R > 1 = recurrence AX += AV diag(alpha) and algebraic
     M, W updates with a recompute every R iterations; 0 = never recompute (R23).
     precision: "f64", or "f32" = fp32 storage of X, AX, G, V, AV with fp64
-    Grams / k x k arithmetic."""
+    Grams / k x k arithmetic.
+    callback: optional callable(t) invoked after iteration t (timing only)."""
     if method not in METHODS:
         raise ValueError(method)
     rnd = (lambda a: a) if precision == "f64" else \
@@ -185,6 +187,8 @@ def run_ofm(op: Operator, method: str, X0, T: int, *, tol=0.0, beta_rule="pr+",
         W = W + Rp * alpha[None, :] + alpha[:, None] * Rp.T + alpha[:, None] * Tm * alpha[None, :]
         Gp, Vp, gg_prev = G, V, gg
         res.iters = t + 1
+        if callback is not None:
+            callback(t)
     res.X = X
     res.state = {"AX": AX, "M": M, "W": W}
     return res

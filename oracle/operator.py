@@ -38,7 +38,9 @@ def build_operator(n, src, dst) -> Operator:
     loop = src == dst
     u = np.minimum(src[~loop], dst[~loop])
     v = np.maximum(src[~loop], dst[~loop])
-    keys = np.unique(u * np.int64(n) + v)           # S_ij in {0,1}: dedupe
+    keys = np.sort(u * np.int64(n) + v)             # S_ij in {0,1}: dedupe
+    if keys.size:
+        keys = keys[np.concatenate([[True], keys[1:] != keys[:-1]])]
     u, v = keys // n, keys % n
     rows = np.concatenate([u, v])                   # S symmetric (undirected graph)
     cols = np.concatenate([v, u])

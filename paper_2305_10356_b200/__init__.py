@@ -1,0 +1,405 @@
+"""paper_2305_10356_b200 -- orthogonalization-free spectral clustering on B200.
+
+Thin ctypes binding of libofsc.so (include/ofsc.h).  Argument marshalling
+only: every numerical step runs in the library's sm_100a kernels.  There is no
+CPU fallback; importing works without a GPU (so the ABI can be inspected), but
+every compute call needs the CUDA device and the in-tree libofsc.so, and fails
+loudly otherwise.
+
+Names follow the paper (arXiv 2305.10356): methods OFM-f1, TriOFM-f1, OFM-f2,
+TriOFM-f2, Algorithm 1, Algorithm 2.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libofsc.so")
+
+METHODS = {"ofm_f1": 0, "triofm_f1": 1, "ofm_f2": 2, "triofm_f2": 3}
+DTYPES = {"f64": 0, "f32": 1}
+BETA_RULES = {"pr": 0, "pr+": 1, "zero": 2}
+MAX_K = 64
+
+
+class OfscError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"ofsc status {status}: {msg}")
+        self.status = status
+
+
+class OfscDiverged(OfscError):
+    pass
+
+
+class Opts(C.Structure):
+    _fields_ = [("k", C.c_int32), ("max_iters", C.c_int32), ("tol", C.c_double),
+                ("beta_rule", C.c_int32), ("line_search", C.c_int32),
+                ("alpha_fixed", C.c_double), ("refresh", C.c_int32),
+                ("check_every", C.c_int32), ("timing_skip", C.c_int32), ("profile", C.c_int32)]
+
+
+class Report(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("diverged", C.c_int32),
+                ("n_three_root_steps", C.c_int32), ("n_zero_steps", C.c_int32),
+                ("grad_norm0", C.c_double), ("grad_norm", C.c_double),
+                ("objective", C.c_double), ("timed_iters", C.c_int32), ("launches", C.c_int32),
+                ("timed_ms", C.c_double), ("kernel_ms", C.c_double * 8),
+                ("kernel_launches", C.c_int32 * 8)]
+
+    def as_dict(self):
+        out = {}
+        for f, _ in self._fields_:
+            v = getattr(self, f)
+            out[f] = list(v) if f in ("kernel_ms", "kernel_launches") else v
+        return out
+
+
+class GraphInfo(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_edges_kept", C.c_int64), ("nnz_global", C.c_int64),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("nnz_local", C.c_int64),
+                ("n_isolated", C.c_int64), ("n_self_loops_dropped", C.c_int64),
+                ("n_duplicates_dropped", C.c_int64), ("max_degree", C.c_int64),
+                ("fro2_A", C.c_double), ("load_imbalance", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+# exported symbol -> (restype, argtypes); mirrors include/ofsc.h
+_P = C.c_void_p
+_I64 = C.c_int64
+_I32 = C.c_int32
+_ST = C.c_int
+SIGNATURES = {
+    "ofsc_version": (C.c_char_p, []),
+    "ofsc_status_string": (C.c_char_p, [_ST]),
+    "ofsc_last_error": (C.c_char_p, []),
+    "ofsc_get_unique_id": (_ST, [_P]),
+    "ofsc_comm_create": (_ST, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "ofsc_comm_destroy": (_ST, [_P]),
+    "ofsc_graph_build": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, _P, C.POINTER(_P)]),
+    "ofsc_graph_info_get": (_ST, [_P, C.POINTER(GraphInfo)]),
+    "ofsc_graph_copy_csr": (_ST, [_P, _P, _P, _P]),
+    "ofsc_graph_destroy": (_ST, [_P]),
+    "ofsc_graph_apply": (_ST, [_P, _ST, _I32, _P, _I64, _P, _I64, _P]),
+    "ofsc_graph_apply_gram": (_ST, [_P, _ST, _I32, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
+    "ofsc_opts_default": (None, [C.POINTER(Opts)]),
+    "ofsc_run": (_ST, [_P, _ST, _ST, C.POINTER(Opts), _P, _I64, _P, C.POINTER(Report), _P]),
+    "ofsc_run_ex": (_ST, [_P, _ST, _ST, C.POINTER(Opts), _P, _I64, _P, _P, _P,
+                          C.POINTER(Report), _P]),
+    "ofsc_line_search": (_ST, [_ST, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ofsc_row_normalize": (_ST, [_ST, _I64, _I32, _P, _I64, _P, _I64, _P]),
+    "ofsc_kmeans": (_ST, [_P, _ST, _I64, _I32, _P, _I64, _I32, _P, _I32, _P, _P, _P, _P]),
+    "ofsc_scores": (_ST, [_I64, _P, _P, _P, _P]),
+    "ofsc_spectral_cluster": (_ST, [_P, _I64, _I64, _P, _P, _ST, _ST, C.POINTER(Opts), _P,
+                                    _I32, _P, _I32, _P, C.POINTER(Report), _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libofsc.so (in-tree).  Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() "
+                              "(python -m paper_2305_10356_b200._build)")
+        try:
+            import torch  # noqa: F401  (load torch's libnccl/cudart first: one NCCL per process)
+        except Exception:
+            pass
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != 0:
+        msg = lib().ofsc_last_error().decode()
+        if st == 6:
+            raise OfscDiverged(st, msg)
+        raise OfscError(st, msg)
+
+
+def version():
+    return lib().ofsc_version().decode()
+
+
+# ---------------------------------------------------------------------------
+# torch marshalling helpers
+# ---------------------------------------------------------------------------
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(stream=None):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _dt_of(t):
+    torch = _torch()
+    if t.dtype == torch.float64:
+        return 0
+    if t.dtype == torch.float32:
+        return 1
+    raise TypeError("features must be float64 or float32")
+
+
+def _dev2d(t):
+    torch = _torch()
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dim() == 2 and t.stride(1) == 1):
+        raise TypeError("expected a 2-D CUDA tensor with unit column stride")
+    return t
+
+
+class Comm:
+    """NCCL communicator over torch.distributed ranks (one process per GPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = (C.c_ubyte * 128)()
+            _check(lib().ofsc_get_unique_id(C.cast(buf, C.c_void_p)))
+            uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            uid = uid.cuda()
+        dist.broadcast(uid, 0, group=group)
+        raw = bytes(uid.cpu().tolist())
+        buf = (C.c_ubyte * 128).from_buffer_copy(raw)
+        h = C.c_void_p()
+        _check(lib().ofsc_comm_create(C.cast(buf, C.c_void_p), self.size, self.rank,
+                                      torch.cuda.current_device(), C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _check(lib().ofsc_comm_destroy(self.handle))
+            self.handle = None
+
+
+class Graph:
+    """Shifted normalised Laplacian A = L - 2I of an undirected graph."""
+
+    def __init__(self, n, src, dst, comm: Comm | None = None, stream=None):
+        torch = _torch()
+        self.n = int(n)
+        self.comm = comm
+        h = C.c_void_p()
+        if isinstance(src, torch.Tensor) and src.is_cuda:
+            s = src.to(torch.int64).contiguous()
+            d = dst.to(torch.int64).contiguous()
+            _check(lib().ofsc_graph_build(comm.handle if comm else None, self.n, s.numel(),
+                                          C.c_void_p(s.data_ptr()), C.c_void_p(d.data_ptr()), 1,
+                                          _stream(stream), C.byref(h)))
+        else:
+            s = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
+            d = np.ascontiguousarray(np.asarray(dst, dtype=np.int64))
+            _check(lib().ofsc_graph_build(comm.handle if comm else None, self.n, s.size,
+                                          s.ctypes.data_as(C.c_void_p),
+                                          d.ctypes.data_as(C.c_void_p), 0, _stream(stream),
+                                          C.byref(h)))
+        self.handle = h
+        self.info = self.get_info()
+
+    def get_info(self):
+        gi = GraphInfo()
+        _check(lib().ofsc_graph_info_get(self.handle, C.byref(gi)))
+        return gi.as_dict()
+
+    @property
+    def n_local(self):
+        return self.info["row_end"] - self.info["row_begin"]
+
+    def copy_csr(self):
+        nl = self.n_local
+        rp = np.empty(nl + 1, np.int64)
+        col = np.empty(max(self.info["nnz_local"], 1), np.int32)
+        s = np.empty(self.n, np.float64)
+        _check(lib().ofsc_graph_copy_csr(self.handle, rp.ctypes.data_as(C.c_void_p),
+                                         col.ctypes.data_as(C.c_void_p),
+                                         s.ctypes.data_as(C.c_void_p)))
+        return rp, col[:self.info["nnz_local"]], s
+
+    def apply(self, Z, Y=None, stream=None):
+        """Y = A Z for the local rows (Z holds all n rows)."""
+        torch = _torch()
+        Z = _dev2d(Z)
+        k = Z.shape[1]
+        if Y is None:
+            Y = torch.empty((self.n_local, k), dtype=Z.dtype, device=Z.device)
+        _check(lib().ofsc_graph_apply(self.handle, _dt_of(Z), k, C.c_void_p(Z.data_ptr()),
+                                      Z.stride(0), C.c_void_p(Y.data_ptr()), Y.stride(0),
+                                      _stream(stream)))
+        return Y
+
+    def apply_gram(self, Z, X, stream=None):
+        """Fused SpMM + Gram hook: Y = A Z and (Z^T Z, Z^T X, Z^T Y, X^T Y)."""
+        torch = _torch()
+        Z, X = _dev2d(Z), _dev2d(X)
+        k = Z.shape[1]
+        Y = torch.empty((self.n_local, k), dtype=Z.dtype, device=Z.device)
+        G = torch.empty((4, k, k), dtype=torch.float64, device=Z.device)
+        _check(lib().ofsc_graph_apply_gram(self.handle, _dt_of(Z), k, C.c_void_p(Z.data_ptr()),
+                                           Z.stride(0), C.c_void_p(X.data_ptr()), X.stride(0),
+                                           C.c_void_p(Y.data_ptr()), Y.stride(0),
+                                           C.c_void_p(G.data_ptr()), _stream(stream)))
+        return Y, G
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().ofsc_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+PHASES = ("update_direction", "beta", "direction_gram", "spmm_gram", "gram_reduce",
+          "line_search", "refresh", "comm")
+
+
+def make_opts(k, max_iters, tol=0.0, beta_rule="pr+", line_search=True, alpha_fixed=0.0,
+              refresh=0, check_every=8, timing_skip=-1, profile=False):
+    o = Opts()
+    lib().ofsc_opts_default(C.byref(o))
+    o.k, o.max_iters, o.tol = int(k), int(max_iters), float(tol)
+    o.beta_rule = BETA_RULES[beta_rule]
+    o.line_search = 1 if line_search else 0
+    o.alpha_fixed = float(alpha_fixed)
+    o.refresh = int(refresh)
+    o.check_every = int(check_every)
+    o.timing_skip = int(timing_skip)
+    o.profile = 1 if profile else 0
+    return o
+
+
+@dataclass
+class RunResult:
+    report: dict
+    history: np.ndarray
+    alphas: np.ndarray | None = None
+    codes: np.ndarray | None = None
+
+
+def run(graph: Graph, method: str, X, max_iters, *, tol=0.0, beta_rule="pr+",
+        line_search=True, alpha_fixed=0.0, refresh=0, check_every=8, debug=False,
+        timing_skip=-1, profile=False, raise_on_diverge=True, stream=None) -> RunResult:
+    """Algorithm 2 on the device; X (local rows x k CUDA tensor) is updated in place."""
+    X = _dev2d(X)
+    k = X.shape[1]
+    o = make_opts(k, max_iters, tol, beta_rule, line_search, alpha_fixed, refresh, check_every,
+                  timing_skip, profile)
+    T = int(max_iters)
+    hist = np.full((max(T, 1), 4), np.nan)
+    rep = Report()
+    al = np.empty((max(T, 1), k)) if debug else None
+    cd = np.empty((max(T, 1), k), np.int32) if debug else None
+    st = lib().ofsc_run_ex(graph.handle, METHODS[method], _dt_of(X), C.byref(o),
+                           C.c_void_p(X.data_ptr()), X.stride(0), hist.ctypes.data_as(C.c_void_p),
+                           al.ctypes.data_as(C.c_void_p) if debug else None,
+                           cd.ctypes.data_as(C.c_void_p) if debug else None,
+                           C.byref(rep), _stream(stream))
+    if st == 6 and not raise_on_diverge:
+        pass
+    else:
+        _check(st)
+    return RunResult(rep.as_dict(), hist[:T], al[:T] if debug else None,
+                     cd[:T] if debug else None)
+
+
+def line_search(method, Q, P, T, Rp, M, W):
+    """k x k exact line search on the device from host Grams (kernel-level hook)."""
+    k = Q.shape[0]
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (Q, P, T, Rp, M, W)]
+    alpha = np.empty(k)
+    codes = np.empty(k, np.int32)
+    Mo = np.empty((k, k))
+    Wo = np.empty((k, k))
+    _check(lib().ofsc_line_search(METHODS[method], k,
+                                  *[a.ctypes.data_as(C.c_void_p) for a in arrs],
+                                  alpha.ctypes.data_as(C.c_void_p), codes.ctypes.data_as(C.c_void_p),
+                                  Mo.ctypes.data_as(C.c_void_p), Wo.ctypes.data_as(C.c_void_p)))
+    return alpha, codes, Mo, Wo
+
+
+def row_normalize(X, Y=None, stream=None):
+    torch = _torch()
+    X = _dev2d(X)
+    if Y is None:
+        Y = torch.empty_like(X)
+    _check(lib().ofsc_row_normalize(_dt_of(X), X.shape[0], X.shape[1], C.c_void_p(X.data_ptr()),
+                                    X.stride(0), C.c_void_p(Y.data_ptr()), Y.stride(0),
+                                    _stream(stream)))
+    return Y
+
+
+def kmeans(Y, centroids, max_iters=100, comm: Comm | None = None, stream=None):
+    """Lloyd K-means from the given centroids (K x dim float64 CUDA tensor, updated in place)."""
+    torch = _torch()
+    Y = _dev2d(Y)
+    assert centroids.dtype == torch.float64 and centroids.is_cuda and centroids.is_contiguous()
+    labels = torch.empty(Y.shape[0], dtype=torch.int32, device=Y.device)
+    it = C.c_int32()
+    inertia = C.c_double()
+    _check(lib().ofsc_kmeans(comm.handle if comm else None, _dt_of(Y), Y.shape[0], Y.shape[1],
+                             C.c_void_p(Y.data_ptr()), Y.stride(0), centroids.shape[0],
+                             C.c_void_p(centroids.data_ptr()), int(max_iters),
+                             C.c_void_p(labels.data_ptr()), C.byref(it), C.byref(inertia),
+                             _stream(stream)))
+    return labels, it.value, inertia.value
+
+
+def scores(a, b):
+    """(ARI, NMI) of two labelings (host)."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.int32))
+    ari, nmi = C.c_double(), C.c_double()
+    _check(lib().ofsc_scores(a.size, a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                             C.byref(ari), C.byref(nmi)))
+    return ari.value, nmi.value
+
+
+def spectral_cluster(n, src, dst, method, X0, n_clusters, init_rows, *, max_iters,
+                     dtype="f64", km_max_iters=100, comm: Comm | None = None, stream=None,
+                     **run_opts):
+    """Algorithm 1 end to end from host buffers (ofsc_spectral_cluster).
+
+    X0: host (local rows x k) array (copied; features returned); returns
+    (labels int32[n_local], features, report)."""
+    npdt = np.float64 if dtype == "f64" else np.float32
+    X = np.ascontiguousarray(np.array(X0, dtype=npdt))
+    src = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
+    dst = np.ascontiguousarray(np.asarray(dst, dtype=np.int64))
+    rows = np.ascontiguousarray(np.asarray(init_rows, dtype=np.int64))
+    labels = np.empty(X.shape[0], np.int32)
+    o = make_opts(X.shape[1], max_iters, **run_opts)
+    rep = Report()
+    _check(lib().ofsc_spectral_cluster(comm.handle if comm else None, int(n), src.size,
+                                       src.ctypes.data_as(C.c_void_p),
+                                       dst.ctypes.data_as(C.c_void_p), METHODS[method],
+                                       DTYPES[dtype], C.byref(o), X.ctypes.data_as(C.c_void_p),
+                                       int(n_clusters), rows.ctypes.data_as(C.c_void_p),
+                                       int(km_max_iters), labels.ctypes.data_as(C.c_void_p),
+                                       C.byref(rep), _stream(stream) if stream is not None else None))
+    return labels, X, rep.as_dict()

@@ -1,0 +1,1053 @@
+// libofsc C ABI and host runtime: graph handles, workspaces, the iteration
+// schedule (captured once as a CUDA graph per iteration kind), NCCL
+// collectives for the row-partitioned multi-GPU path, K-means driver, scores.
+// See include/ofsc.h for the contract of every entry point.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace ofsc {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+template <typename F>
+static ofsc_status guard(F&& f) {
+  try {
+    f();
+    return OFSC_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return OFSC_ERR_NOMEM;
+  } catch (...) {
+    set_last_error("unknown internal error");
+    return OFSC_ERR_STATE;
+  }
+}
+
+static size_t esize(ofsc_dtype dt) { return dt == OFSC_F64 ? 8 : 4; }
+
+// RAII device buffer (stream-ordered allocation)
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t bytes, cudaStream_t st) : s(st) {
+    if (bytes) OFSC_CUDA(cudaMallocAsync(&p, bytes, st));
+  }
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  template <typename T>
+  T* as() const { return (T*)p; }
+};
+
+static void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+static ncclDataType_t nccl_type(ofsc_dtype dt) { return dt == OFSC_F64 ? ncclFloat64 : ncclFloat32; }
+
+// Per-graph run workspace (allocated on first run, reused while (dtype, KP) match).
+struct Workspace {
+  bool have = false;
+  ofsc_dtype dt = OFSC_F64;
+  int KP = 0;
+  void *X = nullptr, *AX = nullptr, *G = nullptr, *AV = nullptr, *Vg = nullptr, *Xg = nullptr;
+  double *part_cols = nullptr, *part_g4 = nullptr, *part_g2 = nullptr, *grams = nullptr;
+  double* state = nullptr;  // M, W [KP*KP each], alpha, beta, gg_prev [KP], colred [2KP]
+  DevCtl* ctl = nullptr;
+  int nb3 = 0, nb4 = 0, nb2 = 0;
+  cudaGraph_t g_iter = nullptr, g_refresh = nullptr;
+  cudaGraphExec_t e_iter = nullptr, e_refresh = nullptr;
+  cudaStream_t cap = nullptr;  // private stream used only for graph capture
+  void release() {
+    if (cap) cudaStreamDestroy(cap);
+    cap = nullptr;
+    if (e_iter) cudaGraphExecDestroy(e_iter);
+    if (e_refresh) cudaGraphExecDestroy(e_refresh);
+    if (g_iter) cudaGraphDestroy(g_iter);
+    if (g_refresh) cudaGraphDestroy(g_refresh);
+    e_iter = e_refresh = nullptr;
+    g_iter = g_refresh = nullptr;
+    for (void* q : {X, AX, G, AV, Vg, Xg, (void*)part_cols, (void*)part_g4, (void*)part_g2,
+                    (void*)grams, (void*)state, (void*)ctl})
+      dfree(q);
+    X = AX = G = AV = Vg = Xg = nullptr;
+    part_cols = part_g4 = part_g2 = grams = state = nullptr;
+    ctl = nullptr;
+    have = false;
+  }
+};
+
+}  // namespace ofsc
+
+using namespace ofsc;
+
+struct ofsc_graph_s {
+  ofsc_comm comm = nullptr;
+  int p = 1, rank = 0;
+  int64_t n = 0, row_begin = 0, row_end = 0, n_local = 0, slot_rows = 0, own_off = 0;
+  int64_t nnz_local = 0;
+  std::vector<int64_t> begins;     // p + 1
+  int64_t* d_begins = nullptr;
+  int64_t* row_ptr = nullptr;      // n_local + 1, from 0
+  int32_t* col = nullptr;          // slot ids (== global ids when p == 1)
+  double* s_slot = nullptr;        // [p * slot_rows]
+  float* s32_slot = nullptr;
+  ofsc_graph_info info{};
+  Workspace ws;
+};
+
+extern "C" {
+
+const char* ofsc_version(void) { return "ofsc 0.1.0 (sm_100a)"; }
+
+const char* ofsc_status_string(ofsc_status s) {
+  switch (s) {
+    case OFSC_OK: return "ok";
+    case OFSC_ERR_ARG: return "invalid argument";
+    case OFSC_ERR_RANGE: return "edge endpoint out of range";
+    case OFSC_ERR_NOMEM: return "out of memory";
+    case OFSC_ERR_CUDA: return "CUDA error";
+    case OFSC_ERR_NCCL: return "NCCL error";
+    case OFSC_ERR_DIVERGED: return "iteration diverged (non-finite direction or step)";
+    case OFSC_ERR_STATE: return "invalid state";
+  }
+  return "unknown status";
+}
+
+const char* ofsc_last_error(void) { return g_last_error.c_str(); }
+
+void ofsc_opts_default(ofsc_opts* o) {
+  if (!o) return;
+  o->k = 0;
+  o->max_iters = 100;
+  o->tol = 0.0;
+  o->beta_rule = OFSC_BETA_PR_PLUS;
+  o->line_search = 1;
+  o->alpha_fixed = 0.0;
+  o->refresh = 0;
+  o->check_every = 8;
+  o->timing_skip = -1;
+  o->profile = 0;
+}
+
+ofsc_status ofsc_get_unique_id(void* h_id128) {
+  return guard([&] {
+    OFSC_REQUIRE(h_id128, OFSC_ERR_ARG, "null id");
+    static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+    ncclUniqueId id;
+    OFSC_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(h_id128, &id, 128);
+  });
+}
+
+ofsc_status ofsc_comm_create(const void* h_id128, int nranks, int rank, int cuda_device,
+                             ofsc_comm* out) {
+  return guard([&] {
+    OFSC_REQUIRE(h_id128 && out && nranks >= 1 && rank >= 0 && rank < nranks, OFSC_ERR_ARG,
+                 "bad communicator arguments");
+    OFSC_CUDA(cudaSetDevice(cuda_device));
+    auto* c = new ofsc_comm_s();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = cuda_device;
+    ncclUniqueId id;
+    std::memcpy(&id, h_id128, 128);
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      throw Error{OFSC_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)};
+    }
+    *out = c;
+  });
+}
+
+ofsc_status ofsc_comm_destroy(ofsc_comm comm) {
+  return guard([&] {
+    if (!comm) return;
+    if (comm->nccl) ncclCommDestroy(comm->nccl);
+    delete comm;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// graph build
+// ---------------------------------------------------------------------------
+static void graph_free(ofsc_graph g) {
+  g->ws.release();
+  dfree(g->d_begins);
+  dfree(g->row_ptr);
+  dfree(g->col);
+  dfree(g->s_slot);
+  dfree(g->s32_slot);
+}
+
+ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
+                             const int64_t* dst, int edges_on_device, ofsc_stream stream,
+                             ofsc_graph* out) {
+  ofsc_graph g = nullptr;
+  ofsc_status st = guard([&] {
+    OFSC_REQUIRE(out && n >= 1 && m >= 0 && (m == 0 || (src && dst)), OFSC_ERR_ARG,
+                 "bad graph arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    g = new ofsc_graph_s();
+    g->comm = comm;
+    g->p = comm ? comm->nranks : 1;
+    g->rank = comm ? comm->rank : 0;
+    g->n = n;
+    CsrDevice csr;
+    {
+      const size_t eb = (!edges_on_device && m > 0) ? m * sizeof(int64_t) : 0;
+      DBuf ds(eb, s), dd(eb, s);
+      const int64_t* psrc = src;
+      const int64_t* pdst = dst;
+      if (eb) {
+        OFSC_CUDA(cudaMemcpyAsync(ds.p, src, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        OFSC_CUDA(cudaMemcpyAsync(dd.p, dst, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        psrc = ds.as<int64_t>();
+        pdst = dd.as<int64_t>();
+      }
+      try {
+        build_csr(n, m, psrc, pdst, csr, s);
+      } catch (...) {
+        dfree(csr.row_ptr);
+        dfree(csr.col);
+        dfree(csr.s);
+        throw;
+      }
+    }
+    const int p = g->p;
+    // nnz-balanced contiguous row split (each row weighted deg + 1: nnz(A) incl. diagonal)
+    std::vector<int64_t> rp(n + 1);
+    OFSC_CUDA(cudaMemcpyAsync(rp.data(), csr.row_ptr, (n + 1) * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    g->begins.assign(p + 1, 0);
+    g->begins[p] = n;
+    const double total = (double)(csr.nnz + n);
+    int64_t i = 0;
+    for (int r = 1; r < p; ++r) {
+      const double target = total * r / p;
+      while (i < n && (double)(rp[i] + i) < target) ++i;
+      g->begins[r] = std::max(i, g->begins[r - 1]);
+    }
+    g->row_begin = g->begins[g->rank];
+    g->row_end = g->begins[g->rank + 1];
+    g->n_local = g->row_end - g->row_begin;
+    int64_t slot = 0, max_nnz = 0;
+    for (int r = 0; r < p; ++r) {
+      slot = std::max(slot, g->begins[r + 1] - g->begins[r]);
+      const int64_t nz = rp[g->begins[r + 1]] - rp[g->begins[r]] + (g->begins[r + 1] - g->begins[r]);
+      max_nnz = std::max(max_nnz, nz);
+    }
+    g->slot_rows = p == 1 ? n : std::max<int64_t>(slot, 1);
+    g->own_off = (int64_t)g->rank * g->slot_rows;
+    const int64_t e0 = rp[g->row_begin], e1 = rp[g->row_end];
+    g->nnz_local = e1 - e0;
+    if (p == 1) {
+      g->row_ptr = csr.row_ptr;
+      g->col = csr.col;
+      g->s_slot = csr.s;
+      OFSC_CUDA(cudaMalloc(&g->s32_slot, n * sizeof(float)));
+      OFSC_CUDA(cudaMalloc(&g->d_begins, 2 * sizeof(int64_t)));
+      OFSC_CUDA(cudaMemcpyAsync(g->d_begins, g->begins.data(), 2 * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+      scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, 1, n, s);
+    } else {
+      OFSC_CUDA(cudaMalloc(&g->d_begins, (p + 1) * sizeof(int64_t)));
+      OFSC_CUDA(cudaMemcpyAsync(g->d_begins, g->begins.data(), (p + 1) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+      OFSC_CUDA(cudaMalloc(&g->row_ptr, (g->n_local + 1) * sizeof(int64_t)));
+      OFSC_CUDA(cudaMalloc(&g->col, std::max<int64_t>(g->nnz_local, 1) * sizeof(int32_t)));
+      OFSC_CUDA(cudaMalloc(&g->s_slot, (size_t)p * g->slot_rows * sizeof(double)));
+      OFSC_CUDA(cudaMalloc(&g->s32_slot, (size_t)p * g->slot_rows * sizeof(float)));
+      OFSC_CUDA(cudaMemsetAsync(g->s_slot, 0, (size_t)p * g->slot_rows * sizeof(double), s));
+      OFSC_CUDA(cudaMemsetAsync(g->s32_slot, 0, (size_t)p * g->slot_rows * sizeof(float), s));
+      rebase_row_ptr(csr.row_ptr + g->row_begin, g->n_local, e0, g->row_ptr, s);
+      remap_columns(csr.col + e0, g->nnz_local, g->col, g->d_begins, p, g->slot_rows, s);
+      scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, p, g->slot_rows, s);
+      OFSC_CUDA(cudaStreamSynchronize(s));
+      dfree(csr.row_ptr);
+      dfree(csr.col);
+      dfree(csr.s);
+    }
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    ofsc_graph_info& in = g->info;
+    in.n = n;
+    in.n_edges_kept = csr.m_kept;
+    in.nnz_global = csr.nnz;
+    in.row_begin = g->row_begin;
+    in.row_end = g->row_end;
+    in.nnz_local = g->nnz_local;
+    in.n_isolated = csr.n_isolated;
+    in.n_self_loops_dropped = csr.n_loops;
+    in.n_duplicates_dropped = csr.n_dups;
+    in.max_degree = csr.max_deg;
+    in.fro2_A = csr.fro2;
+    in.load_imbalance = (double)p * (double)max_nnz / total;
+    *out = g;
+  });
+  if (st != OFSC_OK && g) {
+    graph_free(g);
+    delete g;
+  }
+  return st;
+}
+
+ofsc_status ofsc_graph_info_get(ofsc_graph g, ofsc_graph_info* out) {
+  return guard([&] {
+    OFSC_REQUIRE(g && out, OFSC_ERR_ARG, "null argument");
+    *out = g->info;
+  });
+}
+
+ofsc_status ofsc_graph_copy_csr(ofsc_graph g, int64_t* h_row_ptr, int32_t* h_col, double* h_s) {
+  return guard([&] {
+    OFSC_REQUIRE(g, OFSC_ERR_ARG, "null graph");
+    if (h_row_ptr)
+      OFSC_CUDA(cudaMemcpy(h_row_ptr, g->row_ptr, (g->n_local + 1) * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost));
+    if (h_col && g->nnz_local > 0) {
+      OFSC_CUDA(cudaMemcpy(h_col, g->col, g->nnz_local * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      if (g->p > 1) {  // slot ids -> global ids
+        for (int64_t e = 0; e < g->nnz_local; ++e) {
+          const int64_t sid = h_col[e];
+          const int r = (int)(sid / g->slot_rows);
+          h_col[e] = (int32_t)(g->begins[r] + (sid - (int64_t)r * g->slot_rows));
+        }
+      }
+    }
+    if (h_s) {
+      std::vector<double> slot((size_t)g->p * g->slot_rows);
+      OFSC_CUDA(cudaMemcpy(slot.data(), g->s_slot, slot.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost));
+      for (int r = 0; r < g->p; ++r)
+        for (int64_t q = g->begins[r]; q < g->begins[r + 1]; ++q)
+          h_s[q] = slot[(size_t)r * g->slot_rows + (q - g->begins[r])];
+    }
+  });
+}
+
+ofsc_status ofsc_graph_destroy(ofsc_graph g) {
+  return guard([&] {
+    if (!g) return;
+    cudaDeviceSynchronize();
+    graph_free(g);
+    delete g;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// helpers for the hooks: user layout (global rows, ld) -> slot layout (KP)
+// ---------------------------------------------------------------------------
+namespace ofsc {
+
+__global__ void k_to_slots(int k, int KP, int64_t n, const void* src, int64_t lds, void* dst,
+                           const int64_t* begins, int p, int64_t slot_rows, int f64) {
+  const int64_t total = n * KP;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = e / KP;
+    const int c = (int)(e % KP);
+    int r = 0;
+    while (r + 1 < p && begins[r + 1] <= g) ++r;
+    const int64_t id = r * slot_rows + (g - begins[r]);
+    if (f64) ((double*)dst)[id * KP + c] = c < k ? ((const double*)src)[g * lds + c] : 0.0;
+    else ((float*)dst)[id * KP + c] = c < k ? ((const float*)src)[g * lds + c] : 0.0f;
+  }
+}
+
+static void to_slots(ofsc_graph g, ofsc_dtype dt, int k, int KP, const void* src, int64_t lds,
+                     void* dst, cudaStream_t s) {
+  OFSC_CUDA(cudaMemsetAsync(dst, 0, (size_t)g->p * g->slot_rows * KP * esize(dt), s));
+  k_to_slots<<<num_sms() * 8, 256, 0, s>>>(k, KP, g->n, src, lds, dst, g->d_begins, g->p,
+                                          g->slot_rows, dt == OFSC_F64);
+  OFSC_LAUNCH_CHECK();
+}
+
+static void allreduce_d(ofsc_graph g, double* buf, size_t count, cudaStream_t s) {
+  if (g->p > 1) OFSC_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, g->comm->nccl, s));
+}
+
+__global__ void k_extract_kk(const double* in, int KP, int k, double* out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * k) out[e] = in[(e / k) * KP + (e % k)];
+}
+__global__ void k_embed_kk(const double* in, int KP, int k, double* out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < KP * KP) {
+    const int i = e / KP, j = e % KP;
+    out[e] = (i < k && j < k) ? in[i * k + j] : 0.0;
+  }
+}
+
+}  // namespace ofsc
+
+extern "C" {
+
+ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_Z, int64_t ldz,
+                             void* d_Y, int64_t ldy, ofsc_stream stream) {
+  return guard([&] {
+    OFSC_REQUIRE(g && d_Z && d_Y && k >= 1 && ldz >= k && ldy >= k, OFSC_ERR_ARG, "bad apply args");
+    OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (g->p == 1) {
+      launch_spmm_plain(dt, k, g->n_local, 0, g->row_ptr, g->col, g->s_slot, g->s32_slot, d_Z, ldz,
+                        d_Y, ldy, s);
+    } else {
+      DBuf zs((size_t)g->p * g->slot_rows * k * esize(dt), s);
+      to_slots(g, dt, k, k, d_Z, ldz, zs.p, s);
+      launch_spmm_plain(dt, k, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
+                        zs.p, k, d_Y, ldy, s);
+    }
+  });
+}
+
+ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_Z,
+                                  int64_t ldz, const void* d_X, int64_t ldx, void* d_Y,
+                                  int64_t ldy, double* d_grams, ofsc_stream stream) {
+  return guard([&] {
+    OFSC_REQUIRE(g && d_Z && d_X && d_Y && d_grams && k >= 1 && k <= OFSC_MAX_K && ldz >= k &&
+                     ldx >= k && ldy >= k,
+                 OFSC_ERR_ARG, "bad apply_gram args");
+    OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int KP = padded_k(k);
+    const size_t es = esize(dt);
+    const int64_t nl = g->n_local;
+    DBuf zs((size_t)g->p * g->slot_rows * KP * es, s), xs(std::max<int64_t>(nl, 1) * KP * es, s),
+        ys(std::max<int64_t>(nl, 1) * KP * es, s);
+    to_slots(g, dt, k, KP, d_Z, ldz, zs.p, s);
+    launch_copy_in(dt, k, KP, nl, d_X, ldx, xs.p, s);
+    const int nb = grid_rows(std::max<int64_t>(nl, 1), 2);
+    DBuf p4((size_t)nb * 2 * KP * KP * 8, s), p2((size_t)nb * 2 * KP * KP * 8, s),
+        gr((size_t)4 * KP * KP * 8, s);
+    const char* zown = (const char*)zs.p + (size_t)g->own_off * KP * es;
+    launch_gram_pair(dt, KP, nl, zown, zown, xs.p, p4.as<double>(), nb, s);
+    launch_spmm_gram(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p,
+                     xs.p, ys.p, p2.as<double>(), 0, nullptr, nb, s);
+    launch_reduce_partials(p4.as<double>(), nb, 2 * KP * KP, gr.as<double>(), s);
+    launch_reduce_partials(p2.as<double>(), nb, 2 * KP * KP, gr.as<double>() + 2 * KP * KP, s);
+    allreduce_d(g, gr.as<double>(), 4 * KP * KP, s);
+    launch_copy_out(dt, k, KP, nl, ys.p, d_Y, ldy, s);
+    for (int q = 0; q < 4; ++q)
+      k_extract_kk<<<(k * k + 255) / 256, 256, 0, s>>>(gr.as<double>() + q * KP * KP, KP, k,
+                                                       d_grams + q * k * k);
+    OFSC_LAUNCH_CHECK();
+    OFSC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// the iteration
+// ---------------------------------------------------------------------------
+namespace ofsc {
+
+static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s) {
+  Workspace& w = g->ws;
+  if (w.have && w.dt == dt && w.KP == KP) return;
+  w.release();
+  const size_t es = esize(dt);
+  const int64_t nl = std::max<int64_t>(g->n_local, 1);
+  const size_t blk = (size_t)nl * KP * es;
+  OFSC_CUDA(cudaMalloc(&w.X, blk));
+  OFSC_CUDA(cudaMalloc(&w.AX, blk));
+  OFSC_CUDA(cudaMalloc(&w.G, blk));
+  OFSC_CUDA(cudaMalloc(&w.AV, blk));
+  const size_t vg = g->p == 1 ? blk : (size_t)g->p * g->slot_rows * KP * es;
+  OFSC_CUDA(cudaMalloc(&w.Vg, vg));
+  w.nb3 = grid_rows(nl, 2);
+  w.nb4 = grid_rows(nl, 2);
+  w.nb2 = grid_rows(nl, 2);
+  OFSC_CUDA(cudaMalloc(&w.part_cols, (size_t)w.nb3 * 2 * KP * 8));
+  OFSC_CUDA(cudaMalloc(&w.part_g4, (size_t)w.nb4 * 2 * KP * KP * 8));
+  OFSC_CUDA(cudaMalloc(&w.part_g2, (size_t)w.nb2 * 2 * KP * KP * 8));
+  OFSC_CUDA(cudaMalloc(&w.grams, (size_t)4 * KP * KP * 8));
+  OFSC_CUDA(cudaMalloc(&w.state, (size_t)(2 * KP * KP + 5 * KP) * 8));
+  OFSC_CUDA(cudaMalloc(&w.ctl, sizeof(DevCtl)));
+  w.dt = dt;
+  w.KP = KP;
+  w.have = true;
+}
+
+static IterParams make_params(ofsc_graph g, int method, const ofsc_opts& o, int KP) {
+  Workspace& w = g->ws;
+  const size_t es = esize(w.dt);
+  IterParams p{};
+  p.n_local = g->n_local;
+  p.own_off = g->own_off;
+  p.k = o.k;
+  p.KP = KP;
+  p.method = method;
+  p.beta_rule = o.beta_rule;
+  p.line_search = o.line_search;
+  p.T = o.max_iters;
+  p.alpha_fixed = o.alpha_fixed;
+  p.tol = o.tol;
+  static const double cm[4] = {4.0, 1.0, 2.0, 1.0};
+  p.cm = cm[method];
+  p.fro2 = g->info.fro2_A;
+  p.X = w.X;
+  p.AX = w.AX;
+  p.G = w.G;
+  p.AV = w.AV;
+  p.Vg = w.Vg;
+  p.V = g->p == 1 ? w.Vg : (void*)((char*)w.Vg + (size_t)g->own_off * KP * es);
+  p.row_ptr = g->row_ptr;
+  p.col = g->col;
+  p.s = g->s_slot;
+  p.s32 = g->s32_slot;
+  p.M = w.state;
+  p.W = w.state + KP * KP;
+  p.alpha = w.state + 2 * KP * KP;
+  p.beta = p.alpha + KP;
+  p.gg_prev = p.beta + KP;
+  p.colred = p.gg_prev + KP;
+  p.grams = w.grams;
+  p.part_cols = w.part_cols;
+  p.part_g4 = w.part_g4;
+  p.part_g2 = w.part_g2;
+  p.ctl = w.ctl;
+  return p;
+}
+
+// Per-phase launch accounting and optional CUDA-event timing (opts.profile).
+struct Prof {
+  bool timing = false;
+  cudaStream_t s = nullptr;
+  int launches[OFSC_NUM_PHASES] = {};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  template <typename F>
+  void ph(int id, int nlaunch, F&& f) {
+    launches[id] += nlaunch;
+    if (!timing) {
+      f();
+      return;
+    }
+    cudaEvent_t a, b;
+    OFSC_CUDA(cudaEventCreate(&a));
+    OFSC_CUDA(cudaEventCreate(&b));
+    OFSC_CUDA(cudaEventRecord(a, s));
+    f();
+    OFSC_CUDA(cudaEventRecord(b, s));
+    ev.push_back({id, {a, b}});
+  }
+  int total() const {
+    int t = 0;
+    for (int i = 0; i < OFSC_NUM_PHASES; ++i) t += i == OFSC_PH_COMM ? 0 : launches[i];
+    return t;
+  }
+  void resolve(double* ms) {
+    for (auto& e : ev) {
+      float x = 0.f;
+      OFSC_CUDA(cudaEventElapsedTime(&x, e.second.first, e.second.second));
+      ms[e.first] += x;
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+    ev.clear();
+  }
+  ~Prof() {
+    for (auto& e : ev) {
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+  }
+};
+
+// AX = A X, M = X^T X, W = X^T A X (init and refresh).  X must be current.
+static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaStream_t s,
+                        Prof& pr) {
+  Workspace& w = g->ws;
+  const size_t es = esize(dt);
+  const void* Zg = w.X;
+  if (g->p > 1) {
+    if (!w.Xg) OFSC_CUDA(cudaMalloc(&w.Xg, (size_t)g->p * g->slot_rows * p.KP * es));
+    char* slot = (char*)w.Xg + (size_t)g->own_off * p.KP * es;
+    pr.ph(OFSC_PH_COMM, 0, [&] {
+      OFSC_CUDA(cudaMemcpyAsync(slot, w.X, (size_t)g->n_local * p.KP * es,
+                                cudaMemcpyDeviceToDevice, s));
+      OFSC_NCCL(ncclAllGather(slot, w.Xg, (size_t)g->slot_rows * p.KP, nccl_type(dt),
+                              g->comm->nccl, s));
+    });
+    Zg = w.Xg;
+  }
+  pr.ph(OFSC_PH_REFRESH, 2, [&] {
+    launch_spmm_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
+                     g->s32_slot, Zg, nullptr, w.AX, w.part_g2, 1, &p.ctl->stop, w.nb2, s);
+    launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, p.M, s);  // M, W contiguous
+  });
+  pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, p.M, 2 * (size_t)p.KP * p.KP, s); });
+}
+
+// One iteration of Algorithm 2 (l.8-12), the R-mode schedule of DESIGN.md:
+// C3 -> beta -> C4 -> [all-gather V] -> C2 -> Gram reduce -> [all-reduce] -> line search.
+static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool refresh,
+                          cudaStream_t s, Prof& pr) {
+  Workspace& w = g->ws;
+  if (refresh) {
+    pr.ph(OFSC_PH_REFRESH, 1, [&] { launch_update_x(dt, p, s); });
+    refresh_ops(g, dt, p, s, pr);
+    pr.ph(OFSC_PH_UPDATE_DIRECTION, 1, [&] { launch_update_direction(dt, p, 0, w.nb3, s); });
+  } else {
+    pr.ph(OFSC_PH_UPDATE_DIRECTION, 1, [&] { launch_update_direction(dt, p, 1, w.nb3, s); });
+  }
+  if (g->p == 1) {
+    pr.ph(OFSC_PH_BETA, 1, [&] { launch_beta(p, w.nb3, 0, s); });
+  } else {
+    pr.ph(OFSC_PH_BETA, 1, [&] { launch_reduce_cols(p, w.nb3, s); });
+    pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, p.colred, 2 * (size_t)p.KP, s); });
+    pr.ph(OFSC_PH_BETA, 1, [&] { launch_beta(p, w.nb3, 1, s); });
+  }
+  pr.ph(OFSC_PH_DIRECTION_GRAM, 1, [&] { launch_direction_gram(dt, p, w.nb4, s); });
+  if (g->p > 1)
+    pr.ph(OFSC_PH_COMM, 0, [&] {
+      OFSC_NCCL(ncclAllGather(p.V, w.Vg, (size_t)g->slot_rows * p.KP, nccl_type(dt),
+                              g->comm->nccl, s));
+    });
+  pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
+    launch_spmm_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
+                     g->s32_slot, w.Vg, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
+  });
+  pr.ph(OFSC_PH_GRAM_REDUCE, 2, [&] {
+    launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, s);
+    launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, w.grams + 2 * p.KP * p.KP, s);
+  });
+  pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, w.grams, 4 * (size_t)p.KP * p.KP, s); });
+  pr.ph(OFSC_PH_LINE_SEARCH, 1, [&] { launch_linesearch(p, s); });
+}
+
+static bool use_graphs(ofsc_graph g) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("OFSC_NO_GRAPH");
+    env = (e && e[0] == '1') ? 0 : 1;
+  }
+  return env == 1 && g->p == 1;
+}
+
+static void capture(cudaGraph_t* gr, cudaGraphExec_t* ex, cudaStream_t s,
+                    const std::function<void()>& body) {
+  OFSC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(s, &junk);
+    if (junk) cudaGraphDestroy(junk);
+    throw;
+  }
+  OFSC_CUDA(cudaStreamEndCapture(s, gr));
+  OFSC_CUDA(cudaGraphInstantiate(ex, *gr, 0));
+}
+
+}  // namespace ofsc
+
+extern "C" {
+
+ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const ofsc_opts* opts,
+                        void* d_X, int64_t ldx, double* h_history, double* h_alphas,
+                        int32_t* h_codes, ofsc_report* rep, ofsc_stream stream) {
+  bool diverged = false;
+  ofsc_status st = guard([&] {
+    OFSC_REQUIRE(g && opts && d_X, OFSC_ERR_ARG, "null argument");
+    const ofsc_opts o = *opts;
+    OFSC_REQUIRE(method >= 0 && method <= 3, OFSC_ERR_ARG, "bad method");
+    OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
+    OFSC_REQUIRE(o.k >= 1 && o.k <= OFSC_MAX_K && o.k <= g->n, OFSC_ERR_ARG, "need 1 <= k <= min(n, 64)");
+    OFSC_REQUIRE(ldx >= o.k && o.max_iters >= 0, OFSC_ERR_ARG, "bad ldx / max_iters");
+    OFSC_REQUIRE(o.beta_rule >= 0 && o.beta_rule <= 2 && o.refresh >= 0 && o.tol >= 0.0,
+                 OFSC_ERR_ARG, "bad options");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int KP = padded_k(o.k);
+    ensure_workspace(g, dt, KP, s);
+    Workspace& w = g->ws;
+    const int T = o.max_iters;
+    const size_t es = esize(dt);
+    IterParams p = make_params(g, method, o, KP);
+    DBuf hist((size_t)std::max(T, 1) * 4 * 8, s);
+    DBuf halpha(h_alphas ? (size_t)std::max(T, 1) * KP * 8 : 0, s);
+    DBuf hcode(h_codes ? (size_t)std::max(T, 1) * KP * 4 : 0, s);
+    p.hist = hist.as<double>();
+    p.hist_alpha = halpha.as<double>();
+    p.hist_code = hcode.as<int>();
+    OFSC_CUDA(cudaMemsetAsync(p.hist, 0xff, (size_t)std::max(T, 1) * 4 * 8, s));  // NaN
+    const size_t blk = (size_t)std::max<int64_t>(g->n_local, 1) * KP * es;
+    const size_t vg = g->p == 1 ? blk : (size_t)g->p * g->slot_rows * KP * es;
+    launch_copy_in(dt, o.k, KP, g->n_local, d_X, ldx, w.X, s);
+    OFSC_CUDA(cudaMemsetAsync(w.G, 0, blk, s));
+    OFSC_CUDA(cudaMemsetAsync(w.AV, 0, blk, s));
+    OFSC_CUDA(cudaMemsetAsync(w.Vg, 0, vg, s));
+    OFSC_CUDA(cudaMemsetAsync(w.state, 0, (size_t)(2 * KP * KP + 5 * KP) * 8, s));
+    OFSC_CUDA(cudaMemsetAsync(w.ctl, 0, sizeof(DevCtl), s));
+    // init: AX = A X0, M = X0^T X0, W = X0^T A X0
+    {
+      Prof init;
+      refresh_ops(g, dt, p, s, init);
+    }
+    // The iteration is captured once per call as CUDA graphs (plain and refresh
+    // iteration); they bake in this call's history buffers.  Profiling runs
+    // eager launches bracketed by events instead.
+    const bool graphs = use_graphs(g) && !o.profile;
+    int n_launch_iter = 0, n_launch_refresh = 0;
+    if (graphs) {
+      if (w.e_iter) cudaGraphExecDestroy(w.e_iter);
+      if (w.e_refresh) cudaGraphExecDestroy(w.e_refresh);
+      if (w.g_iter) cudaGraphDestroy(w.g_iter);
+      if (w.g_refresh) cudaGraphDestroy(w.g_refresh);
+      w.e_iter = w.e_refresh = nullptr;
+      w.g_iter = w.g_refresh = nullptr;
+      // capture on a private stream (the caller's may be the legacy default stream,
+      // which cannot be captured); the graphs are then launched on the caller's stream.
+      if (!w.cap) OFSC_CUDA(cudaStreamCreateWithFlags(&w.cap, cudaStreamNonBlocking));
+      Prof c1, c2;
+      capture(&w.g_iter, &w.e_iter, w.cap, [&] { iteration_ops(g, dt, p, false, w.cap, c1); });
+      n_launch_iter = c1.total();
+      if (o.refresh >= 1) {
+        capture(&w.g_refresh, &w.e_refresh, w.cap,
+                [&] { iteration_ops(g, dt, p, true, w.cap, c2); });
+        n_launch_refresh = c2.total();
+      }
+    }
+    int* h_stop = nullptr;
+    OFSC_CUDA(cudaMallocHost(&h_stop, sizeof(int)));
+    struct HostFree {
+      int* q;
+      ~HostFree() { cudaFreeHost(q); }
+    } hf{h_stop};
+    const int check = o.tol > 0.0 ? std::max(1, o.check_every) : 0;
+    const int t0 = o.timing_skip >= 0 ? o.timing_skip : (o.profile ? 0 : T + 1);
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    struct EvFree {
+      cudaEvent_t* a;
+      cudaEvent_t* b;
+      ~EvFree() {
+        if (*a) cudaEventDestroy(*a);
+        if (*b) cudaEventDestroy(*b);
+      }
+    } evf{&ev0, &ev1};
+    Prof prof, quiet;
+    prof.timing = o.profile != 0;
+    prof.s = s;
+    int launches = 0, t_last = 0, timed_iters = 0;
+    for (int t = 0; t < T; ++t) {
+      const bool in_window = t >= t0;
+      if (t == t0) {
+        OFSC_CUDA(cudaEventCreate(&ev0));
+        OFSC_CUDA(cudaEventRecord(ev0, s));
+      }
+      const bool refresh = t > 0 && o.refresh >= 1 && t % o.refresh == 0;
+      if (graphs) {
+        OFSC_CUDA(cudaGraphLaunch(refresh ? w.e_refresh : w.e_iter, s));
+        if (in_window) launches += refresh ? n_launch_refresh : n_launch_iter;
+      } else {
+        Prof& pr = in_window ? prof : quiet;
+        const int before = pr.total();
+        iteration_ops(g, dt, p, refresh, s, pr);
+        if (in_window) launches += pr.total() - before;
+      }
+      if (in_window) ++timed_iters;
+      t_last = t + 1;
+      if (check && (t + 1) % check == 0) {
+        OFSC_CUDA(cudaMemcpyAsync(h_stop, &w.ctl->stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+        OFSC_CUDA(cudaStreamSynchronize(s));
+        if (*h_stop) break;
+      }
+    }
+    if (ev0) {
+      OFSC_CUDA(cudaEventCreate(&ev1));
+      OFSC_CUDA(cudaEventRecord(ev1, s));
+    }
+    (void)t_last;
+    launch_update_x(dt, p, s);  // pending step of the last iteration (no-op after a stop)
+    launch_copy_out(dt, o.k, KP, g->n_local, w.X, d_X, ldx, s);
+    DevCtl c;
+    OFSC_CUDA(cudaMemcpyAsync(&c, w.ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, s));
+    std::vector<double> hh((size_t)std::max(T, 1) * 4);
+    OFSC_CUDA(cudaMemcpyAsync(hh.data(), p.hist, hh.size() * 8, cudaMemcpyDeviceToHost, s));
+    std::vector<double> ha;
+    std::vector<int> hc;
+    if (h_alphas) {
+      ha.resize((size_t)std::max(T, 1) * KP);
+      OFSC_CUDA(cudaMemcpyAsync(ha.data(), p.hist_alpha, ha.size() * 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (h_codes) {
+      hc.resize((size_t)std::max(T, 1) * KP);
+      OFSC_CUDA(cudaMemcpyAsync(hc.data(), p.hist_code, hc.size() * 4, cudaMemcpyDeviceToHost, s));
+    }
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    if (h_history) std::memcpy(h_history, hh.data(), (size_t)T * 4 * 8);
+    for (int t = 0; t < T; ++t)
+      for (int j = 0; j < o.k; ++j) {
+        const bool done = t < c.iter || (c.stop == 2 && t == c.iter);
+        if (h_alphas) h_alphas[(size_t)t * o.k + j] = done ? ha[(size_t)t * KP + j] : NAN;
+        if (h_codes) h_codes[(size_t)t * o.k + j] = done ? hc[(size_t)t * KP + j] : -1;
+      }
+    if (rep) {
+      rep->iters = c.iter;
+      rep->converged = c.stop == 1;
+      rep->diverged = c.stop == 2;
+      rep->n_three_root_steps = c.n_three;
+      rep->n_zero_steps = c.n_zero;
+      rep->grad_norm0 = c.gnorm0;
+      rep->grad_norm = c.gnorm;
+      rep->objective = c.obj;
+      rep->timed_iters = timed_iters;
+      rep->launches = launches;
+      rep->timed_ms = 0.0;
+      if (ev0 && ev1) {
+        float ms = 0.f;
+        OFSC_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+        rep->timed_ms = ms;
+      }
+      for (int q = 0; q < OFSC_NUM_PHASES; ++q) {
+        rep->kernel_ms[q] = 0.0;
+        rep->kernel_launches[q] = o.profile ? prof.launches[q] : 0;
+      }
+      if (o.profile) prof.resolve(rep->kernel_ms);
+    }
+    diverged = c.stop == 2;
+  });
+  if (st == OFSC_OK && diverged) {
+    set_last_error("non-finite direction or step; X holds the last finite iterate");
+    return OFSC_ERR_DIVERGED;
+  }
+  return st;
+}
+
+ofsc_status ofsc_run(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const ofsc_opts* opts,
+                     void* d_X, int64_t ldx, double* h_history, ofsc_report* rep,
+                     ofsc_stream stream) {
+  return ofsc_run_ex(g, method, dt, opts, d_X, ldx, h_history, nullptr, nullptr, rep, stream);
+}
+
+ofsc_status ofsc_line_search(ofsc_method method, int32_t k, const double* h_Q, const double* h_P,
+                             const double* h_T, const double* h_Rp, const double* h_M,
+                             const double* h_W, double* h_alpha, int32_t* h_codes,
+                             double* h_M_out, double* h_W_out) {
+  return guard([&] {
+    OFSC_REQUIRE(h_Q && h_P && h_T && h_Rp && h_M && h_W && h_alpha && k >= 1 && k <= OFSC_MAX_K,
+                 OFSC_ERR_ARG, "bad line-search args");
+    OFSC_REQUIRE(method >= 0 && method <= 3, OFSC_ERR_ARG, "bad method");
+    const int KP = padded_k(k);
+    cudaStream_t s = nullptr;
+    DBuf in((size_t)6 * k * k * 8, s), gr((size_t)6 * KP * KP * 8, s), al((size_t)KP * 8, s),
+        cd((size_t)KP * 4, s);
+    const double* src[6] = {h_Q, h_P, h_T, h_Rp, h_M, h_W};
+    for (int q = 0; q < 6; ++q)
+      OFSC_CUDA(cudaMemcpyAsync(in.as<double>() + q * k * k, src[q], (size_t)k * k * 8,
+                                cudaMemcpyHostToDevice, s));
+    for (int q = 0; q < 6; ++q)
+      k_embed_kk<<<(KP * KP + 255) / 256, 256, 0, s>>>(in.as<double>() + q * k * k, KP, k,
+                                                       gr.as<double>() + q * KP * KP);
+    OFSC_LAUNCH_CHECK();
+    double* M = gr.as<double>() + 4 * KP * KP;
+    double* W = gr.as<double>() + 5 * KP * KP;
+    launch_linesearch_hook(method, k, KP, gr.as<double>(), M, W, al.as<double>(), cd.as<int>(), s);
+    std::vector<double> a(KP), mw(2 * KP * KP);
+    std::vector<int> c(KP);
+    OFSC_CUDA(cudaMemcpyAsync(a.data(), al.p, KP * 8, cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaMemcpyAsync(c.data(), cd.p, KP * 4, cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaMemcpyAsync(mw.data(), M, 2 * KP * KP * 8, cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < k; ++i) {
+      h_alpha[i] = a[i];
+      if (h_codes) h_codes[i] = c[i];
+      for (int j = 0; j < k; ++j) {
+        if (h_M_out) h_M_out[i * k + j] = mw[i * KP + j];
+        if (h_W_out) h_W_out[i * k + j] = mw[KP * KP + i * KP + j];
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// post-processing
+// ---------------------------------------------------------------------------
+ofsc_status ofsc_row_normalize(ofsc_dtype dt, int64_t n_local, int32_t k, const void* d_X,
+                               int64_t ldx, void* d_Y, int64_t ldy, ofsc_stream stream) {
+  return guard([&] {
+    OFSC_REQUIRE(d_X && d_Y && n_local >= 0 && k >= 1 && k <= OFSC_MAX_K && ldx >= k && ldy >= k,
+                 OFSC_ERR_ARG, "bad normalize args");
+    OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
+    if (n_local == 0) return;
+    launch_row_normalize(dt, n_local, k, d_X, ldx, d_Y, ldy, (cudaStream_t)stream);
+  });
+}
+
+ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t dim,
+                        const void* d_Y, int64_t ldy, int32_t n_clusters, double* d_centroids,
+                        int32_t max_iters, int32_t* d_labels, int32_t* iters_out,
+                        double* inertia_out, ofsc_stream stream) {
+  return guard([&] {
+    OFSC_REQUIRE(d_Y && d_centroids && d_labels && n_local >= 0 && dim >= 1 && ldy >= dim &&
+                     n_clusters >= 1 && max_iters >= 1,
+                 OFSC_ERR_ARG, "bad kmeans args");
+    OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int K = n_clusters;
+    const int nb = kmeans_blocks(std::max<int64_t>(n_local, 1));
+    const int W = dim + 1;
+    DBuf chg(8, s), pin((size_t)nb * 8, s), part((size_t)nb * K * W * 8, s),
+        red((size_t)K * W * 8, s), tot(8, s);
+    OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
+    unsigned long long* h_chg = nullptr;
+    OFSC_CUDA(cudaMallocHost(&h_chg, 8));
+    struct HostFree {
+      void* q;
+      ~HostFree() { cudaFreeHost(q); }
+    } hf{h_chg};
+    int it = 0;
+    double inertia = 0.0;
+    for (it = 1; it <= max_iters; ++it) {
+      OFSC_CUDA(cudaMemsetAsync(chg.p, 0, 8, s));
+      OFSC_CUDA(cudaMemsetAsync(pin.p, 0, (size_t)nb * 8, s));
+      if (n_local > 0)
+        launch_kmeans_assign(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
+                             chg.as<unsigned long long>(), pin.as<double>(), nb, s);
+      launch_reduce_partials(pin.as<double>(), nb, 1, tot.as<double>(), s);
+      if (comm && comm->nranks > 1) {
+        OFSC_NCCL(ncclAllReduce(chg.p, chg.p, 1, ncclUint64, ncclSum, comm->nccl, s));
+        OFSC_NCCL(ncclAllReduce(tot.p, tot.p, 1, ncclFloat64, ncclSum, comm->nccl, s));
+      }
+      OFSC_CUDA(cudaMemcpyAsync(h_chg, chg.p, 8, cudaMemcpyDeviceToHost, s));
+      OFSC_CUDA(cudaMemcpyAsync(&inertia, tot.p, 8, cudaMemcpyDeviceToHost, s));
+      OFSC_CUDA(cudaStreamSynchronize(s));
+      if (it > 1 && *h_chg == 0) break;
+      if (n_local > 0)
+        launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nb, s);
+      else
+        OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nb * K * W * 8, s));
+      launch_reduce_partials(part.as<double>(), nb, K * W, red.as<double>(), s);
+      if (comm && comm->nranks > 1)
+        OFSC_NCCL(ncclAllReduce(red.p, red.p, (size_t)K * W, ncclFloat64, ncclSum, comm->nccl, s));
+      launch_kmeans_finish(K, dim, red.as<double>(), d_centroids, s);
+    }
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    if (iters_out) *iters_out = std::min(it, max_iters);
+    if (inertia_out) *inertia_out = inertia;
+  });
+}
+
+ofsc_status ofsc_scores(int64_t n, const int32_t* a, const int32_t* b, double* ari, double* nmi) {
+  return guard([&] {
+    OFSC_REQUIRE(a && b && n >= 1, OFSC_ERR_ARG, "bad scores args");
+    std::map<int32_t, int> ia, ib;
+    for (int64_t i = 0; i < n; ++i) {
+      ia.emplace(a[i], (int)ia.size());
+      ib.emplace(b[i], (int)ib.size());
+    }
+    const size_t ra = ia.size(), rb = ib.size();
+    std::vector<int64_t> C(ra * rb, 0), sa(ra, 0), sb(rb, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int x = ia[a[i]], y = ib[b[i]];
+      ++C[(size_t)x * rb + y];
+      ++sa[x];
+      ++sb[y];
+    }
+    auto c2 = [](double x) { return x * (x - 1.0) / 2.0; };
+    double sij = 0, sA = 0, sB = 0;
+    for (int64_t v : C) sij += c2((double)v);
+    for (int64_t v : sa) sA += c2((double)v);
+    for (int64_t v : sb) sB += c2((double)v);
+    const double e = n > 1 ? sA * sB / c2((double)n) : 0.0;
+    const double den = 0.5 * (sA + sB) - e;
+    if (ari) *ari = den == 0.0 ? 1.0 : (sij - e) / den;
+    if (nmi) {
+      double ha = 0, hb = 0, mi = 0;
+      const double N = (double)n;
+      for (int64_t v : sa)
+        if (v) ha -= (v / N) * std::log(v / N);
+      for (int64_t v : sb)
+        if (v) hb -= (v / N) * std::log(v / N);
+      for (size_t x = 0; x < ra; ++x)
+        for (size_t y = 0; y < rb; ++y) {
+          const int64_t v = C[x * rb + y];
+          if (v) mi += (v / N) * std::log((v / N) / ((sa[x] / N) * (sb[y] / N)));
+        }
+      *nmi = (ha + hb == 0.0) ? 1.0 : 2.0 * mi / (ha + hb);
+    }
+  });
+}
+
+}  // extern "C"
+
+namespace ofsc {
+// C[c] = Y[init_rows[c] - row_begin] for rows owned by this rank, 0 otherwise
+__global__ void k_gather_rows(int K, int dim, const int64_t* rows, int64_t row_begin, int64_t n_local,
+                              const void* Y, int64_t ldy, int f64, double* C) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K * dim) return;
+  const int c = e / dim, d = e % dim;
+  const int64_t r = rows[c] - row_begin;
+  double v = 0.0;
+  if (r >= 0 && r < n_local)
+    v = f64 ? ((const double*)Y)[r * ldy + d] : (double)((const float*)Y)[r * ldy + d];
+  C[e] = v;
+}
+}  // namespace ofsc
+
+extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t m,
+                                             const int64_t* h_src, const int64_t* h_dst,
+                                             ofsc_method method, ofsc_dtype dt,
+                                             const ofsc_opts* opts, void* h_X, int32_t n_clusters,
+                                             const int64_t* h_init_rows, int32_t km_max_iters,
+                                             int32_t* h_labels, ofsc_report* rep,
+                                             ofsc_stream stream) {
+  ofsc_graph g = nullptr;
+  ofsc_status run_st = OFSC_OK;
+  ofsc_status st = guard([&] {
+    OFSC_REQUIRE(opts && h_X && h_init_rows && h_labels && n_clusters >= 1, OFSC_ERR_ARG,
+                 "bad spectral_cluster args");
+    cudaStream_t s = (cudaStream_t)stream;
+    ofsc_status b = ofsc_graph_build(comm, n, m, h_src, h_dst, 0, stream, &g);
+    if (b != OFSC_OK) throw Error{b, g_last_error};
+    const int k = opts->k;
+    const int64_t nl = g->n_local;
+    const size_t es = esize(dt);
+    DBuf dX(std::max<int64_t>(nl, 1) * k * es, s), dY(std::max<int64_t>(nl, 1) * k * es, s),
+        dC((size_t)n_clusters * k * 8, s), dL(std::max<int64_t>(nl, 1) * 4, s),
+        dR((size_t)n_clusters * 8, s);
+    OFSC_CUDA(cudaMemcpyAsync(dX.p, h_X, nl * k * es, cudaMemcpyHostToDevice, s));
+    run_st = ofsc_run(g, method, dt, opts, dX.p, k, nullptr, rep, stream);
+    if (run_st != OFSC_OK && run_st != OFSC_ERR_DIVERGED) throw Error{run_st, g_last_error};
+    OFSC_CUDA(cudaMemcpyAsync(h_X, dX.p, nl * k * es, cudaMemcpyDeviceToHost, s));
+    ofsc_status r = ofsc_row_normalize(dt, nl, k, dX.p, k, dY.p, k, stream);
+    if (r != OFSC_OK) throw Error{r, g_last_error};
+    OFSC_CUDA(cudaMemcpyAsync(dR.p, h_init_rows, (size_t)n_clusters * 8, cudaMemcpyHostToDevice, s));
+    k_gather_rows<<<(n_clusters * k + 255) / 256, 256, 0, s>>>(
+        n_clusters, k, dR.as<int64_t>(), g->row_begin, nl, dY.p, k, dt == OFSC_F64, dC.as<double>());
+    OFSC_LAUNCH_CHECK();
+    if (comm && comm->nranks > 1)
+      OFSC_NCCL(ncclAllReduce(dC.p, dC.p, (size_t)n_clusters * k, ncclFloat64, ncclSum, comm->nccl, s));
+    r = ofsc_kmeans(comm, dt, nl, k, dY.p, k, n_clusters, dC.as<double>(), km_max_iters,
+                    dL.as<int32_t>(), nullptr, nullptr, stream);
+    if (r != OFSC_OK) throw Error{r, g_last_error};
+    OFSC_CUDA(cudaMemcpyAsync(h_labels, dL.p, nl * 4, cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaStreamSynchronize(s));
+  });
+  if (g) ofsc_graph_destroy(g);
+  if (st == OFSC_OK && run_st == OFSC_ERR_DIVERGED) return OFSC_ERR_DIVERGED;
+  return st;
+}

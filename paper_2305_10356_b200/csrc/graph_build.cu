@@ -1,0 +1,277 @@
+// C1: undirected edge list -> CSR pattern of S and s = D^{-1/2} (Alg. 1 l.2).
+//   1. key = (min(u,v) << 32) | max(u,v); self-loops -> sentinel (dropped, P:31 S is 0/1)
+//   2. radix sort + unique: the canonical undirected edge set (duplicates collapsed)
+//   3. symmetrise: (u,v) and (v,u) as (row << 32) | col, radix sort -> CSR order,
+//      columns ascending within each row
+//   4. degree histogram (integer atomics), exclusive scan -> row_ptr
+//   5. s_i = 1 / sqrt(d_i) (0 for an isolated node), ||A||_F^2 = n + sum (s_i s_j)^2
+// cub (CUDA toolkit) supplies the radix sort / unique / scan building blocks.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace ofsc {
+
+namespace {
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  explicit DevBuf(size_t count, cudaStream_t st) : n(count), s(st) {
+    if (count) OFSC_CUDA(cudaMallocAsync(&p, count * sizeof(T), st));
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+constexpr unsigned long long kSentinel = ~0ull;
+
+__global__ void k_make_keys(int64_t m, int64_t n, const int64_t* src, const int64_t* dst,
+                            unsigned long long* keys, unsigned long long* n_loops, int* bad) {
+  unsigned long long loops = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = src[e], v = dst[e];
+    if (u < 0 || v < 0 || u >= n || v >= n) {
+      *bad = 1;
+      keys[e] = kSentinel;
+      continue;
+    }
+    if (u == v) {
+      ++loops;
+      keys[e] = kSentinel;
+      continue;
+    }
+    const unsigned long long a = (unsigned long long)(u < v ? u : v);
+    const unsigned long long b = (unsigned long long)(u < v ? v : u);
+    keys[e] = (a << 32) | b;
+  }
+  if (loops) atomicAdd(n_loops, loops);
+}
+
+__global__ void k_symmetrise(int64_t E, const unsigned long long* ukeys, unsigned long long* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ukeys[e];
+    const unsigned long long u = k >> 32, v = k & 0xffffffffull;
+    out[2 * e] = k;
+    out[2 * e + 1] = (v << 32) | u;
+  }
+}
+
+__global__ void k_split_keys(int64_t nnz, const unsigned long long* keys, int32_t* col,
+                             int* deg) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[e];
+    col[e] = (int32_t)(k & 0xffffffffull);
+    atomicAdd(deg + (k >> 32), 1);
+  }
+}
+
+__global__ void k_scale(int64_t n, const int* deg, double* s, int64_t* row_ptr_last,
+                        unsigned long long* n_iso, int* max_deg, int64_t nnz) {
+  unsigned long long iso = 0;
+  int md = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int d = deg[i];
+    s[i] = d > 0 ? 1.0 / sqrt((double)d) : 0.0;   // D^{-1/2}; isolated -> 0 (R12)
+    iso += d == 0;
+    md = d > md ? d : md;
+  }
+  if (iso) atomicAdd(n_iso, iso);
+  atomicMax(max_deg, md);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *row_ptr_last = nnz;
+}
+
+__global__ void k_deg_to_i64(int64_t n, const int* deg, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = deg[i];
+}
+
+// per-CTA partial of sum_i sum_{j in N(i)} (s_i s_j)^2 over a contiguous row range
+__global__ void k_fro2(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* s,
+                       double* part) {
+  __shared__ double red[256];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = imin64(n, r0 + per);
+  double a = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double si2 = s[i] * s[i];
+    for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; ++q) {
+      const double sj = s[col[q]];
+      a += si2 * (sj * sj);
+    }
+  }
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+int blocks_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst, CsrDevice& out,
+               cudaStream_t st) {
+  OFSC_REQUIRE(n >= 1 && n < (int64_t(1) << 31), OFSC_ERR_ARG, "need 1 <= n < 2^31");
+  out.n = n;
+  DevBuf<unsigned long long> counters(2, st);   // [0] loops, [1] isolated
+  DevBuf<int> flags(2, st);                     // [0] bad endpoint, [1] max degree
+  OFSC_CUDA(cudaMemsetAsync(counters.p, 0, 2 * sizeof(unsigned long long), st));
+  OFSC_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), st));
+  int64_t E = 0;
+  DevBuf<unsigned long long> ukeys(m > 0 ? m : 1, st);
+  if (m > 0) {
+    DevBuf<unsigned long long> keys(m, st);
+    k_make_keys<<<blocks_for(m), 256, 0, st>>>(m, n, d_src, d_dst, keys.p, counters.p, flags.p);
+    OFSC_LAUNCH_CHECK();
+    DevBuf<unsigned long long> sorted(m, st);
+    size_t tmp_bytes = 0;
+    OFSC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, sorted.p, m, 0, 64, st));
+    {
+      DevBuf<char> tmp(tmp_bytes, st);
+      OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, m, 0, 64, st));
+    }
+    DevBuf<int64_t> nsel(1, st);
+    tmp_bytes = 0;
+    OFSC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp_bytes, sorted.p, ukeys.p, nsel.p, m, st));
+    {
+      DevBuf<char> tmp(tmp_bytes, st);
+      OFSC_CUDA(cub::DeviceSelect::Unique(tmp.p, tmp_bytes, sorted.p, ukeys.p, nsel.p, m, st));
+    }
+    int64_t h_nsel = 0;
+    unsigned long long h_cnt[2];
+    int h_flags[2];
+    OFSC_CUDA(cudaMemcpyAsync(&h_nsel, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaMemcpyAsync(h_cnt, counters.p, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaMemcpyAsync(h_flags, flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaStreamSynchronize(st));
+    OFSC_REQUIRE(!h_flags[0], OFSC_ERR_RANGE, "edge endpoint outside [0, n)");
+    out.n_loops = (int64_t)h_cnt[0];
+    unsigned long long last = 0;
+    if (h_nsel > 0)
+      OFSC_CUDA(cudaMemcpy(&last, ukeys.p + h_nsel - 1, sizeof(last), cudaMemcpyDeviceToHost));
+    E = h_nsel - ((h_nsel > 0 && last == kSentinel) ? 1 : 0);
+  }
+  out.m_kept = E;
+  out.n_dups = m - out.n_loops - E;
+  out.nnz = 2 * E;
+  OFSC_REQUIRE(out.nnz < (int64_t(1) << 40), OFSC_ERR_ARG, "graph too large");
+  OFSC_CUDA(cudaMallocAsync(&out.row_ptr, (n + 1) * sizeof(int64_t), st));
+  OFSC_CUDA(cudaMallocAsync(&out.col, (out.nnz > 0 ? out.nnz : 1) * sizeof(int32_t), st));
+  OFSC_CUDA(cudaMallocAsync(&out.s, n * sizeof(double), st));
+  DevBuf<int> deg(n, st);
+  OFSC_CUDA(cudaMemsetAsync(deg.p, 0, n * sizeof(int), st));
+  if (E > 0) {
+    DevBuf<unsigned long long> sym(out.nnz, st), sym_sorted(out.nnz, st);
+    k_symmetrise<<<blocks_for(E), 256, 0, st>>>(E, ukeys.p, sym.p);
+    OFSC_LAUNCH_CHECK();
+    int hi = 1;
+    while ((int64_t(1) << hi) < n) ++hi;
+    size_t tmp_bytes = 0;
+    OFSC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, sym.p, sym_sorted.p, out.nnz, 0,
+                                             32 + hi, st));
+    {
+      DevBuf<char> tmp(tmp_bytes, st);
+      OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, sym.p, sym_sorted.p, out.nnz, 0,
+                                               32 + hi, st));
+    }
+    k_split_keys<<<blocks_for(out.nnz), 256, 0, st>>>(out.nnz, sym_sorted.p, out.col, deg.p);
+    OFSC_LAUNCH_CHECK();
+  }
+  {
+    DevBuf<int64_t> deg64(n, st);
+    k_deg_to_i64<<<blocks_for(n), 256, 0, st>>>(n, deg.p, deg64.p);
+    OFSC_LAUNCH_CHECK();
+    size_t tmp_bytes = 0;
+    OFSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg64.p, out.row_ptr, n, st));
+    DevBuf<char> tmp(tmp_bytes, st);
+    OFSC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, deg64.p, out.row_ptr, n, st));
+  }
+  k_scale<<<blocks_for(n), 256, 0, st>>>(n, deg.p, out.s, out.row_ptr + n, counters.p + 1,
+                                         flags.p + 1, out.nnz);
+  OFSC_LAUNCH_CHECK();
+  const int nb = blocks_for(n) < 1024 ? blocks_for(n) : 1024;
+  DevBuf<double> part(nb, st);
+  k_fro2<<<nb, 256, 0, st>>>(n, out.row_ptr, out.col, out.s, part.p);
+  OFSC_LAUNCH_CHECK();
+  std::vector<double> hp(nb);
+  unsigned long long iso = 0;
+  int md = 0;
+  OFSC_CUDA(cudaMemcpyAsync(hp.data(), part.p, nb * sizeof(double), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaMemcpyAsync(&iso, counters.p + 1, sizeof(iso), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaMemcpyAsync(&md, flags.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaStreamSynchronize(st));
+  double f = 0.0;
+  for (int b = 0; b < nb; ++b) f += hp[b];
+  out.fro2 = (double)n + f;
+  out.n_isolated = (int64_t)iso;
+  out.max_deg = md;
+}
+
+// ---- multi-GPU layout helpers ----------------------------------------------
+// global id g (owned by rank r, rows [b_r, b_{r+1})) -> slot id r*slot_rows + (g - b_r)
+__global__ void k_remap(const int32_t* in, int64_t nnz, int32_t* out, const int64_t* begins, int p,
+                        int64_t slot_rows) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = in[e];
+    int r = 0;
+    while (r + 1 < p && begins[r + 1] <= g) ++r;
+    out[e] = (int32_t)(r * slot_rows + (g - begins[r]));
+  }
+}
+
+void remap_columns(const int32_t* col_in, int64_t nnz, int32_t* col_out, const int64_t* d_begins,
+                   int p, int64_t slot_rows, cudaStream_t st) {
+  if (nnz <= 0) return;
+  k_remap<<<blocks_for(nnz), 256, 0, st>>>(col_in, nnz, col_out, d_begins, p, slot_rows);
+  OFSC_LAUNCH_CHECK();
+}
+
+__global__ void k_scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
+                                const int64_t* begins, int p, int64_t slot_rows) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int r = 0;
+    while (r + 1 < p && begins[r + 1] <= g) ++r;
+    const int64_t id = r * slot_rows + (g - begins[r]);
+    s_slot[id] = s[g];
+    s32_slot[id] = (float)s[g];
+  }
+}
+
+void scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
+                   const int64_t* d_begins, int p, int64_t slot_rows, cudaStream_t st) {
+  k_scatter_slots<<<blocks_for(n), 256, 0, st>>>(s, n, s_slot, s32_slot, d_begins, p, slot_rows);
+  OFSC_LAUNCH_CHECK();
+}
+
+__global__ void k_rebase(const int64_t* in, int64_t rows, int64_t base, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= rows;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] - base;
+}
+
+void rebase_row_ptr(const int64_t* in, int64_t rows, int64_t base, int64_t* out, cudaStream_t st) {
+  k_rebase<<<blocks_for(rows + 1), 256, 0, st>>>(in, rows, base, out);
+  OFSC_LAUNCH_CHECK();
+}
+
+}  // namespace ofsc

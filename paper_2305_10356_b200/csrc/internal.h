@@ -1,0 +1,163 @@
+// Internal declarations shared by the libofsc translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ofsc.h"
+
+namespace ofsc {
+
+// ---- error plumbing: internal code throws, every ABI entry point catches ----
+struct Error {
+  ofsc_status st;
+  std::string msg;
+};
+void set_last_error(const std::string& m);
+
+#define OFSC_CUDA(x)                                                                    \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::ofsc::Error{OFSC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+#define OFSC_NCCL(x)                                                                    \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess)                                                              \
+      throw ::ofsc::Error{OFSC_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+#define OFSC_REQUIRE(cond, code, m)                       \
+  do {                                                    \
+    if (!(cond)) throw ::ofsc::Error{code, std::string(m)}; \
+  } while (0)
+#define OFSC_LAUNCH_CHECK() OFSC_CUDA(cudaGetLastError())
+
+constexpr int kTR = 32;        // rows per tile of the row-wise kernels
+constexpr int kThreads = 256;  // threads per CTA of the tiled kernels
+
+// Padded feature width used on the device (columns k..KP-1 are kept at zero).
+inline int padded_k(int k) { return k <= 16 ? 16 : k <= 32 ? 32 : k <= 48 ? 48 : 64; }
+
+// Device control block of one run (stream-ordered, no host round trip).
+struct DevCtl {
+  int iter;      // completed updates of X
+  int stop;      // 0 running, 1 converged, 2 diverged
+  int n_three;   // line searches that chose among three real roots
+  int n_zero;    // degenerate cubics
+  double gnorm0, gnorm, obj;
+};
+
+// Everything the per-iteration kernels need, passed by value.
+struct IterParams {
+  int64_t n_local;      // rows owned by this rank
+  int64_t own_off;      // slot id of local row 0 inside the gathered layout
+  int k, KP, method, beta_rule, line_search, T;
+  double alpha_fixed, tol, cm, fro2;
+  // N x KP blocks (type set by the dtype of the run)
+  void* X;
+  void* AX;
+  void* G;
+  void* V;              // local rows of V (a view into Vg when p > 1)
+  void* AV;
+  const void* Vg;       // V for the gathers (all slots)
+  // CSR
+  const int64_t* row_ptr;
+  const int32_t* col;   // slot ids
+  const double* s;      // per slot id
+  const float* s32;
+  // k x k state (KP x KP, row-major, fp64)
+  double* M;
+  double* W;
+  double* alpha;        // [KP]
+  double* beta;         // [KP]
+  double* gg_prev;      // [KP]
+  double* colred;       // [2 KP] reduced (gg, dg) when p > 1
+  double* grams;        // [4 KP KP]: Q, P, T, R'
+  double* part_cols;    // [nblk][2][KP]
+  double* part_g4;      // [nblk][2][KP][KP] (Q, P)
+  double* part_g2;      // [nblk][2][KP][KP] (T, R')
+  DevCtl* ctl;
+  double* hist;         // [T][4]
+  double* hist_alpha;   // [T][KP]
+  int* hist_code;       // [T][KP]
+};
+
+// ---- launchers (kernels_*.cu) ----
+int grid_rows(int64_t n_rows, int blocks_per_sm);
+int num_sms();
+
+// C3: X += alpha V, AX += alpha AV (if apply_update), G = g_m(X, AX, M, W), column partials.
+void launch_update_direction(ofsc_dtype dt, const IterParams& p, int apply_update, int nblk,
+                             cudaStream_t s);
+// X += alpha V only (refresh iterations, final update); also used to write X out.
+void launch_update_x(ofsc_dtype dt, const IterParams& p, cudaStream_t s);
+// C4: V = -G + beta Vp, partial Grams Q = V^T V, P = V^T X.
+void launch_direction_gram(ofsc_dtype dt, const IterParams& p, int nblk, cudaStream_t s);
+// C2: Y = A Z (Z gathered), partial Grams. mode 0: (Zown^T Y, Xown^T Y); mode 1: (Zown^T Zown, Zown^T Y)
+void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
+                      const int64_t* row_ptr, const int32_t* col, const double* s,
+                      const float* s32, const void* Zg, const void* Xown, void* Y,
+                      double* part, int mode, const int* stop, int nblk, cudaStream_t st);
+// plain SpMM (no Grams) into an arbitrary ld
+void launch_spmm_plain(ofsc_dtype dt, int k, int64_t n_local, int64_t own_off,
+                       const int64_t* row_ptr, const int32_t* col, const double* s,
+                       const float* s32, const void* Zg, int64_t ldz, void* Y, int64_t ldy,
+                       cudaStream_t st);
+// generic tile Gram pair: part = (A^T B, A^T C) over local rows (KP-padded blocks)
+void launch_gram_pair(ofsc_dtype dt, int KP, int64_t n_local, const void* A, const void* B,
+                      const void* C, double* part, int nblk, cudaStream_t st);
+// sum partial Grams over blocks in fixed order: out[g] = sum_b part[b][g], g < ngram
+void launch_reduce_partials(const double* part, int nblk, int per_blk, double* out,
+                            cudaStream_t st);
+// column partial reduction (gg, dg) -> colred (used when p > 1)
+void launch_reduce_cols(const IterParams& p, int nblk, cudaStream_t st);
+// beta / convergence / history (1 CTA).  reduced: read colred instead of part_cols
+void launch_beta(const IterParams& p, int nblk, int reduced, cudaStream_t st);
+// exact line search + algebraic M, W update (1 CTA)
+void launch_linesearch(const IterParams& p, cudaStream_t st);
+// line-search hook: coefficients from given Grams (device), no ctl
+void launch_linesearch_hook(int method, int k, int KP, const double* grams, double* M, double* W,
+                            double* alpha, int* codes, cudaStream_t st);
+// layout helpers
+void launch_copy_in(ofsc_dtype dt, int k, int KP, int64_t n, const void* src, int64_t lds,
+                    void* dst, cudaStream_t st);
+void launch_copy_out(ofsc_dtype dt, int k, int KP, int64_t n, const void* src, void* dst,
+                     int64_t ldd, cudaStream_t st);
+void launch_row_normalize(ofsc_dtype dt, int64_t n, int k, const void* X, int64_t ldx, void* Y,
+                          int64_t ldy, cudaStream_t st);
+// K-means
+void launch_kmeans_assign(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                          const double* C, int* labels, unsigned long long* changes,
+                          double* part_inertia, int nblk, cudaStream_t st);
+void launch_kmeans_partial(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                           const int* labels, double* part, int nblk, cudaStream_t st);
+void launch_kmeans_finish(int K, int dim, const double* red, double* C, cudaStream_t st);
+int kmeans_blocks(int64_t n);
+
+// graph build (graph_build.cu)
+struct CsrDevice {
+  int64_t n = 0, m_kept = 0, nnz = 0, n_loops = 0, n_dups = 0, n_isolated = 0, max_deg = 0;
+  double fro2 = 0.0;
+  int64_t* row_ptr = nullptr;  // [n+1]
+  int32_t* col = nullptr;      // [nnz] global ids
+  double* s = nullptr;         // [n]
+};
+void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst, CsrDevice& out,
+               cudaStream_t st);
+void remap_columns(const int32_t* col_in, int64_t nnz, int32_t* col_out, const int64_t* d_begins,
+                   int p, int64_t slot_rows, cudaStream_t st);
+void scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
+                   const int64_t* d_begins, int p, int64_t slot_rows, cudaStream_t st);
+void rebase_row_ptr(const int64_t* in, int64_t rows, int64_t base, int64_t* out, cudaStream_t st);
+
+}  // namespace ofsc
+
+struct ofsc_comm_s {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};

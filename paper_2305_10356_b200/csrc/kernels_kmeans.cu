@@ -1,0 +1,153 @@
+// Lloyd K-means on the normalised features (Alg. 1 l.5).
+//   assign: label_r = argmin_c sum_{d=0}^{dim-1} (y_rd - C_cd)^2, summed in d
+//           order in fp64, ties -> lowest c (R20).  Compiled with
+//           -fmad=false so the distance rounds exactly as written, identical to
+//           the oracle's, and every argmin decision is taken in the same precision.
+//   update: per-CTA partial sums over a contiguous row range in row order (one
+//           thread per feature column, no atomics), fixed-order reduction,
+//           mean; an empty cluster keeps its centroid.
+#include "common.cuh"
+
+namespace ofsc {
+
+constexpr int kKmThreads = 256;
+
+// One warp per row; lane l evaluates centroids l, l+32, ...; centroids are held
+// transposed in smem (Ct[d][c]) so a warp's reads are conflict-free.
+template <typename T>
+__global__ void __launch_bounds__(kKmThreads)
+k_kmeans_assign(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
+                const double* __restrict__ C, int* __restrict__ labels,
+                unsigned long long* changes, double* part_inertia) {
+  extern __shared__ double sm[];
+  double* Ct = sm;                         // [dim][K]
+  double* rows = Ct + (size_t)dim * K;     // [8 warps][dim]
+  __shared__ double s_in[kKmThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < dim * K; e += kKmThreads) {
+    const int c = e / dim, d = e % dim;
+    Ct[d * K + c] = C[e];
+  }
+  __syncthreads();
+  double* yr = rows + warp * dim;
+  double inertia = 0.0;
+  unsigned long long nchg = 0;
+  const int64_t nw = (int64_t)gridDim.x * (kKmThreads / 32);
+  for (int64_t r = (int64_t)blockIdx.x * (kKmThreads / 32) + warp; r < n; r += nw) {
+    for (int d = lane; d < dim; d += 32) yr[d] = ld1(Y + r * ldy + d);
+    __syncwarp();
+    double best = 0.0;
+    int bc = 0x7fffffff;
+    for (int c = lane; c < K; c += 32) {
+      double acc = 0.0;
+      for (int d = 0; d < dim; ++d) {
+        const double diff = yr[d] - Ct[d * K + c];
+        acc = acc + diff * diff;
+      }
+      if (bc == 0x7fffffff || acc < best) {   // c increases: strict < keeps the lowest index
+        best = acc;
+        bc = c;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (oc != 0x7fffffff && (bc == 0x7fffffff || ob < best || (ob == best && oc < bc))) {
+        best = ob;
+        bc = oc;
+      }
+    }
+    if (lane == 0) {
+      if (labels[r] != bc) ++nchg;
+      labels[r] = bc;
+      inertia += best;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    s_in[warp] = inertia;
+    if (nchg) atomicAdd(changes, nchg);      // integer: order-independent
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0;
+    for (int w = 0; w < kKmThreads / 32; ++w) a += s_in[w];
+    part_inertia[blockIdx.x] = a;
+  }
+}
+
+int kmeans_blocks(int64_t n) {
+  int64_t b = (n + 63) / 64;
+  const int64_t cap = (int64_t)num_sms() * 4;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+void launch_kmeans_assign(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                          const double* C, int* labels, unsigned long long* changes,
+                          double* part_inertia, int nblk, cudaStream_t st) {
+  const size_t smem = ((size_t)dim * K + (size_t)(kKmThreads / 32) * dim) * sizeof(double);
+  OFSC_REQUIRE(smem <= 200 * 1024, OFSC_ERR_ARG, "n_clusters * dim too large for K-means smem");
+  if (dt == OFSC_F64) {
+    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_kmeans_assign<double><<<nblk, kKmThreads, smem, st>>>(n, dim, (const double*)Y, ldy, K, C,
+                                                            labels, changes, part_inertia);
+  } else {
+    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_assign<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_kmeans_assign<float><<<nblk, kKmThreads, smem, st>>>(n, dim, (const float*)Y, ldy, K, C,
+                                                           labels, changes, part_inertia);
+  }
+  OFSC_LAUNCH_CHECK();
+}
+
+// Partial cluster sums of a contiguous row range: part[b][c][0..dim-1] = sums,
+// part[b][c][dim] = count.  Thread d < dim owns column d; rows in order.
+template <typename T>
+__global__ void k_kmeans_partial(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
+                                 const int* __restrict__ labels, double* part) {
+  extern __shared__ double acc[];          // [K][dim+1]
+  const int tid = threadIdx.x;
+  const int W = dim + 1;
+  for (int e = tid; e < K * W; e += blockDim.x) acc[e] = 0.0;
+  __syncthreads();
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per;
+  const int64_t r1 = imin64(n, r0 + per);
+  if (tid < W) {
+    for (int64_t r = r0; r < r1; ++r) {
+      const int c = labels[r];
+      acc[c * W + tid] += tid < dim ? ld1(Y + r * ldy + tid) : 1.0;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < K * W; e += blockDim.x) part[(int64_t)blockIdx.x * K * W + e] = acc[e];
+}
+
+void launch_kmeans_partial(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                           const int* labels, double* part, int nblk, cudaStream_t st) {
+  const size_t smem = (size_t)K * (dim + 1) * sizeof(double);
+  const int th = ((dim + 1 + 31) / 32) * 32;
+  if (dt == OFSC_F64) {
+    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_partial<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_kmeans_partial<double><<<nblk, th, smem, st>>>(n, dim, (const double*)Y, ldy, K, labels, part);
+  } else {
+    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_partial<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_kmeans_partial<float><<<nblk, th, smem, st>>>(n, dim, (const float*)Y, ldy, K, labels, part);
+  }
+  OFSC_LAUNCH_CHECK();
+}
+
+// red[c][0..dim-1] = sums, red[c][dim] = count -> C[c] = mean (empty keeps C[c]).
+__global__ void k_kmeans_finish(int K, int dim, const double* red, double* C) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= K * dim) return;
+  const int c = e / dim, d = e % dim;
+  const double cnt = red[c * (dim + 1) + dim];
+  if (cnt > 0.0) C[e] = red[c * (dim + 1) + d] / cnt;
+}
+
+void launch_kmeans_finish(int K, int dim, const double* red, double* C, cudaStream_t st) {
+  k_kmeans_finish<<<(K * dim + 255) / 256, 256, 0, st>>>(K, dim, red, C);
+  OFSC_LAUNCH_CHECK();
+}
+
+}  // namespace ofsc

@@ -1,0 +1,98 @@
+"""Post-processing parity (P4): row normalisation, K-means on identical features,
+scores, and Algorithm 1 end to end through ofsc_spectral_cluster."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2305_10356_b200 as ofsc  # noqa: E402
+from oracle import (build_operator, run_ofm, row_normalize, kmeans_lloyd, ari, nmi)  # noqa: E402
+from synth import CONFIGS, config_graph, x0_block, kmeans_init_rows  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ofsc.lib()
+
+
+@pytest.fixture(scope="module")
+def c1_features():
+    cfg = CONFIGS["c1"]
+    s, d, lab = config_graph(cfg)
+    op = build_operator(cfg.n, s, d)
+    o = run_ofm(op, "ofm_f2", x0_block(cfg.n, cfg.k, cfg.seed_x0), cfg.iters)
+    return cfg, s, d, lab, o.X
+
+
+def test_row_normalize_parity(c1_features):
+    cfg, s, d, lab, X = c1_features
+    X = X.copy()
+    X[5] = 0.0
+    Y = ofsc.row_normalize(torch.from_numpy(X).cuda()).cpu().numpy()
+    Yo = row_normalize(X)
+    assert np.max(np.abs(Y - Yo)) <= 4e-16
+    assert np.all(Y[5] == 0.0)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_kmeans_identical_features_identical_labels(name):
+    cfg = CONFIGS[name]
+    s, d, lab = config_graph(cfg)
+    op = build_operator(cfg.n, s, d)
+    X = run_ofm(op, "ofm_f1", x0_block(cfg.n, cfg.k, cfg.seed_x0), 60, refresh=0).X
+    Y = row_normalize(X)                                # identical features on both sides
+    rows = kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)
+    lo, Co, ito, ino = kmeans_lloyd(Y, Y[rows], max_iters=100)
+    C = torch.from_numpy(Y[rows].copy()).cuda()
+    lg, itg, ing = ofsc.kmeans(torch.from_numpy(Y).cuda(), C, max_iters=100)
+    lg = lg.cpu().numpy()
+    mism = np.nonzero(lg != lo)[0]
+    # mismatches are allowed only at near-ties of the two closest centroids
+    for r in mism:
+        dd = np.sort(np.sum((Y[r] - Co) ** 2, axis=1))
+        assert dd[1] - dd[0] <= 1e-12 * dd[1]
+    assert len(mism) <= max(1, cfg.n // 10000)
+    assert itg == ito
+    assert abs(ing - ino) <= 1e-10 * ino
+    assert np.allclose(C.cpu().numpy(), Co, atol=1e-13)
+
+
+def test_kmeans_first_assignment_bit_exact():
+    """One Lloyd assignment from identical centroids: every argmin decision is
+    taken in the same precision and order, so labels are identical."""
+    rng = np.random.default_rng(3)
+    Y = row_normalize(rng.standard_normal((5000, 17)))
+    C0 = Y[:9].copy()
+    lo, _, _, ino = kmeans_lloyd(Y, C0, max_iters=1)
+    lg, _, ing = ofsc.kmeans(torch.from_numpy(Y).cuda(), torch.from_numpy(C0).cuda(), max_iters=1)
+    assert np.array_equal(lg.cpu().numpy(), lo)
+    assert abs(ing - ino) <= 1e-12 * ino
+
+
+def test_scores_match_oracle():
+    rng = np.random.default_rng(0)
+    for _ in range(10):
+        a, b = rng.integers(0, 5, 300), rng.integers(0, 7, 300)
+        ga, gn = ofsc.scores(a, b)
+        assert abs(ga - ari(a, b)) <= 1e-12 and abs(gn - nmi(a, b)) <= 1e-12
+    assert ofsc.scores([0, 0, 1, 1], [0, 1, 0, 1])[0] == pytest.approx(-0.5)
+
+
+@pytest.mark.parametrize("method", ["ofm_f1", "ofm_f2", "triofm_f1", "triofm_f2"])
+def test_algorithm1_end_to_end_c1(method):
+    cfg = CONFIGS["c1"]
+    s, d, lab = config_graph(cfg)
+    X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
+    rows = kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)
+    labels, feats, rep = ofsc.spectral_cluster(cfg.n, s, d, method, X0, cfg.blocks, rows,
+                                               max_iters=cfg.iters)
+    op = build_operator(cfg.n, s, d)
+    o = run_ofm(op, method, X0, cfg.iters, refresh=0)
+    Y = row_normalize(o.X)
+    lo, _, _, _ = kmeans_lloyd(Y, Y[rows], 100)
+    a_gpu, a_or = ari(labels, lab), ari(lo, lab)
+    assert rep["iters"] == cfg.iters
+    assert a_gpu >= 0.8 and abs(a_gpu - a_or) <= 0.02

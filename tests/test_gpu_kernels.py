@@ -1,0 +1,145 @@
+"""Kernel-level parity (P0): CSR build, SpMM, fused SpMM + Gram, line search.
+
+CUDA path (through the C ABI) vs the oracle on identical seeded inputs."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2305_10356_b200 as ofsc  # noqa: E402
+from oracle import (build_operator, apply_A, grams, cubic_coefficients, select_step,  # noqa: E402
+                    fro2_A, METHODS)
+from synth import CONFIGS, config_graph, dcsbm_graph, x0_block  # noqa: E402
+from tests import graphs as G  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ofsc.lib()
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+GRAPHS = {
+    "c1": lambda: config_graph(CONFIGS["c1"])[:2] + (CONFIGS["c1"].n,),
+    "c2": lambda: config_graph(CONFIGS["c2"])[:2] + (CONFIGS["c2"].n,),
+    "messy": lambda: (np.array([0, 1, 1, 2, 3, 3, 5, 9, 9, 7]), np.array([1, 0, 1, 3, 2, 2, 5, 8, 7, 9]), 12),
+    "ragged": lambda: dcsbm_graph(1037, 5, 6000, 2.0, 9)[:2] + (1037,),
+}
+
+
+@pytest.mark.parametrize("name", list(GRAPHS))
+def test_csr_bit_exact(name):
+    s, d, n = GRAPHS[name]()
+    op = build_operator(n, s, d)
+    g = ofsc.Graph(n, s, d)
+    rp, col, sv = g.copy_csr()
+    assert np.array_equal(rp, op.row_ptr)
+    assert np.array_equal(col.astype(np.int64), op.col)
+    assert np.array_equal(sv, op.s)            # 1/sqrt(d): correctly rounded on both sides
+    info = g.info
+    assert info["n_edges_kept"] == op.n_edges
+    assert info["n_self_loops_dropped"] == op.n_self_loops
+    assert info["n_duplicates_dropped"] == op.n_duplicates
+    assert info["n_isolated"] == int(np.sum(op.deg == 0))
+    assert info["max_degree"] == int(op.deg.max())
+    assert abs(info["fro2_A"] - fro2_A(op)) <= 1e-13 * fro2_A(op)
+
+
+def test_build_from_device_edges_and_errors():
+    s, d, n = GRAPHS["c1"]()
+    g1 = ofsc.Graph(n, s, d)
+    g2 = ofsc.Graph(n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
+    a, b = g1.copy_csr(), g2.copy_csr()
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    with pytest.raises(ofsc.OfscError) as e:
+        ofsc.Graph(5, np.array([0, 1]), np.array([1, 5]))
+    assert e.value.status == 2
+    g0 = ofsc.Graph(4, np.array([], np.int64), np.array([], np.int64))   # no edges: A = -I
+    Z = torch.randn(4, 3, dtype=torch.float64, device="cuda")
+    assert torch.equal(g0.apply(Z), -Z)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "ragged"])
+@pytest.mark.parametrize("k", [1, 11, 32, 48, 64])
+def test_spmm_f64(name, k):
+    s, d, n = GRAPHS[name]()
+    op = build_operator(n, s, d)
+    g = ofsc.Graph(n, s, d)
+    Z = np.random.default_rng(k).standard_normal((n, k))
+    Y = g.apply(torch.from_numpy(Z).cuda()).cpu().numpy()
+    Yo = apply_A(op, Z)
+    assert np.max(np.abs(Y - Yo)) <= 1e-14 * np.max(np.abs(Yo)) * 4
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "ragged"])
+@pytest.mark.parametrize("k", [3, 11, 16, 32, 48, 64])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_fused_spmm_gram(name, k, dtype):
+    s, d, n = GRAPHS[name]()
+    op = build_operator(n, s, d)
+    g = ofsc.Graph(n, s, d)
+    rng = np.random.default_rng(100 + k)
+    Z = rng.standard_normal((n, k)) / np.sqrt(n)
+    X = rng.standard_normal((n, k)) / np.sqrt(n)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    if dtype == "f32":
+        Z = Z.astype(np.float32).astype(np.float64)
+        X = X.astype(np.float32).astype(np.float64)
+    Y, Gm = g.apply_gram(torch.from_numpy(Z).to(tdt).cuda(), torch.from_numpy(X).to(tdt).cuda())
+    Y = Y.double().cpu().numpy()
+    Gm = Gm.cpu().numpy()
+    prec = "f64" if dtype == "f64" else "f32"
+    Yo = apply_A(op, Z, prec)
+    Q, P, T, Rp = grams(Z, X, Yo)
+    if dtype == "f64":
+        assert np.max(np.abs(Y - Yo)) <= 4e-14 * np.max(np.abs(Yo))
+        tol = 1e-13
+    else:
+        assert np.max(np.abs(Y - Yo)) <= 1e-6 * np.max(np.abs(Yo))
+        tol = 1e-6
+    for got, want in zip(Gm, (Q, P, T, Rp)):
+        assert rel(got, want) <= tol
+
+
+@pytest.mark.parametrize("method", METHODS)
+@pytest.mark.parametrize("seed", range(6))
+def test_line_search_kernel_matches_oracle(method, seed):
+    """The k x k kernel on oracle Grams: same alpha (to rounding) and same branch codes."""
+    s, d, n = GRAPHS["c1"]()
+    op = build_operator(n, s, d)
+    rng = np.random.default_rng(seed)
+    k = 11
+    X = rng.standard_normal((n, k)) / np.sqrt(n) * (1 + seed)
+    V = rng.standard_normal((n, k)) / np.sqrt(n) * 10.0 ** (-seed)
+    AX, AV = apply_A(op, X), apply_A(op, V)
+    Q, P, T, Rp = grams(V, X, AV)
+    M, W = X.T @ X, X.T @ AX
+    alpha, codes, Mo, Wo = ofsc.line_search(method, Q, P, T, Rp, M, W)
+    c3, c2, c1, c0 = cubic_coefficients(method, Q, P, T, Rp, M, W)
+    if method.startswith("tri"):
+        want = [select_step(c3[i], c2[i], c1[i], c0[i]) for i in range(k)]
+    else:
+        want = [select_step(c3, c2, c1, c0)] * k
+    wa = np.array([w[0] for w in want])
+    assert list(codes) == [w[1] for w in want]
+    assert np.max(np.abs(alpha - wa)) <= 1e-11 * max(1.0, np.max(np.abs(wa)))
+    D = np.diag(alpha)
+    assert rel(Mo, M + P.T @ D + D @ P + D @ Q @ D) <= 1e-13
+    assert rel(Wo, W + Rp @ D + D @ Rp.T + D @ T @ D) <= 1e-13
+
+
+def test_line_search_textbook_cubics_on_device():
+    """Grams built so the OFM-f1 cubic is a^3 - a: k = 1, Q = 1, P = 0, T = -1, R' = 0, M = 0."""
+    one = np.ones((1, 1))
+    zero = np.zeros((1, 1))
+    alpha, codes, _, _ = ofsc.line_search("ofm_f1", one, zero, -one, zero, zero, zero)
+    assert alpha[0] == -1.0 and codes[0] in (8, 9, 10)
+    alpha, codes, _, _ = ofsc.line_search("ofm_f1", zero, zero, zero, zero, zero, zero)
+    assert alpha[0] == 0.0 and codes[0] == 0
