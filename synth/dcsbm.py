@@ -11,6 +11,7 @@ oracle and the CUDA path receive bit-identical inputs.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -180,9 +181,33 @@ _CACHE = {}
 
 
 def config_graph(cfg: Config):
-    """Graph of a named config (memoised in-process only)."""
+    """Graph of a named config, memoised in-process and (for large configs) in an
+    on-disk cache (OFSC_SYNTH_CACHE, default /tmp/ofsc_synth) keyed by all
+    generator parameters.  The cache only saves generation time; the arrays are
+    a pure function of the config."""
     key = cfg.name
-    if key not in _CACHE:
-        _CACHE[key] = dcsbm_graph(cfg.n, cfg.blocks, cfg.edges, cfg.ratio,
-                                  cfg.seed_graph, cfg.dirichlet)
-    return _CACHE[key]
+    if key in _CACHE:
+        return _CACHE[key]
+    path = None
+    if cfg.edges >= 1_000_000:
+        d = os.environ.get("OFSC_SYNTH_CACHE", "/tmp/ofsc_synth")
+        tag = f"{cfg.name}_{cfg.n}_{cfg.blocks}_{cfg.edges}_{cfg.ratio}_{cfg.dirichlet}_{cfg.seed_graph}_v1"
+        path = os.path.join(d, tag + ".npz")
+        if os.path.exists(path):
+            try:
+                z = np.load(path)
+                _CACHE[key] = (z["src"], z["dst"], z["labels"])
+                return _CACHE[key]
+            except Exception:
+                pass
+    out = dcsbm_graph(cfg.n, cfg.blocks, cfg.edges, cfg.ratio, cfg.seed_graph, cfg.dirichlet)
+    if path is not None:
+        try:
+            os.makedirs(os.path.dirname(path), exist_ok=True)
+            tmp = path + f".{os.getpid()}.tmp.npz"
+            np.savez(tmp, src=out[0], dst=out[1], labels=out[2])
+            os.replace(tmp, path)
+        except Exception:
+            pass
+    _CACHE[key] = out
+    return out
