@@ -477,11 +477,10 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   OFSC_CUDA(cudaMalloc(&w.AV, blk));
   const size_t vg = g->p == 1 ? blk : (size_t)g->p * g->slot_rows * KP * es;
   OFSC_CUDA(cudaMalloc(&w.Vg, vg));
-  w.nb3 = grid_rows(nl, 2);
-  w.nb4 = grid_rows(nl, 2);
+  const int nbmax = num_sms() * 4;   // grids of the streaming kernels are chosen per run
   w.nb2 = grid_rows(nl, 2);
-  OFSC_CUDA(cudaMalloc(&w.part_cols, (size_t)w.nb3 * 2 * KP * 8));
-  OFSC_CUDA(cudaMalloc(&w.part_g4, (size_t)w.nb4 * 2 * KP * KP * 8));
+  OFSC_CUDA(cudaMalloc(&w.part_cols, (size_t)nbmax * 2 * KP * 8));
+  OFSC_CUDA(cudaMalloc(&w.part_g4, (size_t)nbmax * 2 * KP * KP * 8));
   OFSC_CUDA(cudaMalloc(&w.part_g2, (size_t)w.nb2 * 2 * KP * KP * 8));
   OFSC_CUDA(cudaMalloc(&w.grams, (size_t)4 * KP * KP * 8));
   OFSC_CUDA(cudaMalloc(&w.state, (size_t)(2 * KP * KP + 5 * KP) * 8));
@@ -493,6 +492,8 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
 
 static IterParams make_params(ofsc_graph g, int method, const ofsc_opts& o, int KP) {
   Workspace& w = g->ws;
+  w.nb3 = c3_grid(w.dt, KP, method, std::max<int64_t>(g->n_local, 1));
+  w.nb4 = c4_grid(w.dt, KP, std::max<int64_t>(g->n_local, 1));
   const size_t es = esize(w.dt);
   IterParams p{};
   p.n_local = g->n_local;

@@ -38,58 +38,6 @@ __device__ __forceinline__ double ld1(const float* p) { return (double)*p; }
 __device__ __forceinline__ void st1(double* p, double v) { *p = v; }
 __device__ __forceinline__ void st1(float* p, double v) { *p = (float)v; }
 
-// Per-thread register block of two k x k Gram products over smem tiles.
-// Thread (ti, tj) = (tid >> 4, tid & 15) owns rows i = ii*16 + ti and columns
-// j = jj*16 + tj (stride-16 interleave: conflict-free smem reads).
-template <int KP>
-struct GramPair {
-  static constexpr int B = KP / 16;
-  double a[B][B];
-  double b[B][B];
-  __device__ __forceinline__ void zero() {
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-#pragma unroll
-      for (int j = 0; j < B; ++j) a[i][j] = b[i][j] = 0.0;
-  }
-  // a += L1^T R1, b += L2^T R2 over `rows` rows of KP-wide smem tiles.
-  template <bool LEFT_SHARED, bool RIGHT_SHARED>
-  __device__ __forceinline__ void accumulate(const double* L1, const double* R1, const double* L2,
-                                             const double* R2, int rows, int ti, int tj) {
-    for (int r = 0; r < rows; ++r) {
-      double l1[B], l2[B], r1[B], r2[B];
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-        l1[i] = L1[r * KP + i * 16 + ti];
-        l2[i] = LEFT_SHARED ? l1[i] : L2[r * KP + i * 16 + ti];
-      }
-#pragma unroll
-      for (int j = 0; j < B; ++j) {
-        r1[j] = R1[r * KP + j * 16 + tj];
-        r2[j] = RIGHT_SHARED ? r1[j] : R2[r * KP + j * 16 + tj];
-      }
-#pragma unroll
-      for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          a[i][j] = fma(l1[i], r1[j], a[i][j]);
-          b[i][j] = fma(l2[i], r2[j], b[i][j]);
-        }
-    }
-  }
-  // part[0][i][j] = a, part[1][i][j] = b
-  __device__ __forceinline__ void store(double* part, int ti, int tj) const {
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-#pragma unroll
-      for (int j = 0; j < B; ++j) {
-        const int ii = i * 16 + ti, jj = j * 16 + tj;
-        part[ii * KP + jj] = a[i][j];
-        part[KP * KP + ii * KP + jj] = b[i][j];
-      }
-  }
-};
-
 // Dispatch on the padded width.
 #define OFSC_DISPATCH_KP(KP, ...)                       \
   switch (KP) {                                         \

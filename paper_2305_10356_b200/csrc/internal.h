@@ -91,6 +91,9 @@ struct IterParams {
 int grid_rows(int64_t n_rows, int blocks_per_sm);
 int num_sms();
 
+// grid sizes of the TMA-pipelined streaming kernels (<= 4 * #SMs)
+int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n);
+int c4_grid(ofsc_dtype dt, int KP, int64_t n);
 // C3: X += alpha V, AX += alpha AV (if apply_update), G = g_m(X, AX, M, W), column partials.
 void launch_update_direction(ofsc_dtype dt, const IterParams& p, int apply_update, int nblk,
                              cudaStream_t s);

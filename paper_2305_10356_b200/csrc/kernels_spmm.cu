@@ -5,12 +5,13 @@
 // One warp (or a KP/2-lane group) per row gathers the neighbour rows of Z with
 // 16-byte vector loads (coalesced 2*KP*sizeof(T) bytes per neighbour), summing
 // in CSR (ascending column) order.  Row tiles of 32 rows are staged in shared
-// memory and the epilogue accumulates per-CTA partial Grams with the GramPair
-// register blocks; a fixed-order reduction (kernels_rows.cu) finishes them, so
+// memory and the epilogue accumulates per-CTA partial Grams on the fp64 tensor
+// path (DmmaGram, mma.sync m8n8k4); a fixed-order reduction (kernels_rows.cu) finishes them, so
 // runs are bitwise reproducible.
 //   mode 0 (iteration):  T = Z^T Y, R' = X^T Y    (Z = V)
 //   mode 1 (refresh):    M = Z^T Z, W = Z^T Y     (Z = X)
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace ofsc {
 
@@ -26,16 +27,17 @@ k_spmm_gram(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_pt
             const float* __restrict__ s32, const T* __restrict__ Zg, const T* __restrict__ Xown,
             T* __restrict__ Y, double* __restrict__ part, const int* stop) {
   if (stop && *stop) return;
-  __shared__ __align__(16) double Zs[kTR * KP];
-  __shared__ __align__(16) double Ys[kTR * KP];
-  __shared__ __align__(16) double Xs[MODE == 0 ? kTR * KP : 1];
+  constexpr int LD = KP + 4;                      // padded: conflict-free DMMA fragments
+  extern __shared__ __align__(16) double sp_sm[];
+  double* Zs = sp_sm;
+  double* Ys = Zs + kTR * LD;
+  double* Xs = Ys + kTR * LD;                    // mode 0 only
   constexpr int LPR = KP / 2;                    // lanes per row (2 columns per lane)
   constexpr int RPW = (32 % LPR == 0) ? 32 / LPR : 1;  // rows per warp pass
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int sub = lane / LPR, l = lane % LPR;
   const bool active = sub < RPW;
-  const int ti = tid >> 4, tj = tid & 15;
-  GramPair<KP> acc;
+  DmmaGram<KP> acc;
   acc.zero();
   const int64_t ntiles = (n_local + kTR - 1) / kTR;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -91,23 +93,40 @@ k_spmm_gram(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_pt
         own = make_double2((double)zo.x, (double)zo.y);
         if (MODE == 0) xo = ld2(Xown + i * KP + 2 * l);
       }
-      Ys[r * KP + 2 * l] = y.x;
-      Ys[r * KP + 2 * l + 1] = y.y;
-      Zs[r * KP + 2 * l] = own.x;
-      Zs[r * KP + 2 * l + 1] = own.y;
+      Ys[r * LD + 2 * l] = y.x;
+      Ys[r * LD + 2 * l + 1] = y.y;
+      Zs[r * LD + 2 * l] = own.x;
+      Zs[r * LD + 2 * l + 1] = own.y;
       if (MODE == 0) {
-        Xs[r * KP + 2 * l] = xo.x;
-        Xs[r * KP + 2 * l + 1] = xo.y;
+        Xs[r * LD + 2 * l] = xo.x;
+        Xs[r * LD + 2 * l + 1] = xo.y;
       }
     }
     __syncthreads();
     if (part) {
-      if (MODE == 0) acc.template accumulate<false, true>(Zs, Ys, Xs, Ys, rows, ti, tj);
-      else acc.template accumulate<true, false>(Zs, Zs, Zs, Ys, rows, ti, tj);
+      const int r4 = (rows + 3) & ~3;
+      if (MODE == 0) acc.accumulate(Zs, Ys, Xs, Ys, r4, warp, lane);   // T = Z^T Y, R' = X^T Y
+      else acc.accumulate(Zs, Zs, Zs, Ys, r4, warp, lane);             // M = Z^T Z, W = Z^T Y
     }
     __syncthreads();
   }
-  if (part) acc.store(part + (int64_t)blockIdx.x * 2 * KP * KP, ti, tj);
+  if (part) acc.store(part + (int64_t)blockIdx.x * 2 * KP * KP, warp, lane);
+}
+
+template <typename T, int KP, int MODE>
+static void launch_sg(int64_t n_local, int64_t own_off, const int64_t* row_ptr, const int32_t* col,
+                      const double* s, const float* s32, const void* Zg, const void* Xown, void* Y,
+                      double* part, const int* stop, int nblk, cudaStream_t st) {
+  const size_t smem = (size_t)(MODE == 0 ? 3 : 2) * kTR * (KP + 4) * 8;
+  auto kern = k_spmm_gram<T, KP, MODE>;
+  static bool set = false;
+  if (!set) {
+    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = true;
+  }
+  kern<<<nblk, kThreads, smem, st>>>(n_local, own_off, row_ptr, col, s, s32, (const T*)Zg,
+                                     (const T*)Xown, (T*)Y, part, stop);
+  OFSC_LAUNCH_CHECK();
 }
 
 void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
@@ -116,26 +135,13 @@ void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       int mode, const int* stop, int nblk, cudaStream_t st) {
   OFSC_DISPATCH_KP(KP, {
     if (dt == OFSC_F64) {
-      if (mode == 0)
-        k_spmm_gram<double, KPC, 0><<<nblk, kThreads, 0, st>>>(
-            n_local, own_off, row_ptr, col, s, s32, (const double*)Zg, (const double*)Xown,
-            (double*)Y, part, stop);
-      else
-        k_spmm_gram<double, KPC, 1><<<nblk, kThreads, 0, st>>>(
-            n_local, own_off, row_ptr, col, s, s32, (const double*)Zg, (const double*)Xown,
-            (double*)Y, part, stop);
+      if (mode == 0) launch_sg<double, KPC, 0>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
+      else launch_sg<double, KPC, 1>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
     } else {
-      if (mode == 0)
-        k_spmm_gram<float, KPC, 0><<<nblk, kThreads, 0, st>>>(
-            n_local, own_off, row_ptr, col, s, s32, (const float*)Zg, (const float*)Xown,
-            (float*)Y, part, stop);
-      else
-        k_spmm_gram<float, KPC, 1><<<nblk, kThreads, 0, st>>>(
-            n_local, own_off, row_ptr, col, s, s32, (const float*)Zg, (const float*)Xown,
-            (float*)Y, part, stop);
+      if (mode == 0) launch_sg<float, KPC, 0>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
+      else launch_sg<float, KPC, 1>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
     }
   });
-  OFSC_LAUNCH_CHECK();
 }
 
 // Plain SpMM with arbitrary leading dimensions (ABI hook ofsc_graph_apply):

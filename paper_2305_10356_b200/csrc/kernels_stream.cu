@@ -1,0 +1,403 @@
+// Streaming row kernels of the iteration, TMA-pipelined (sm_100a):
+//   C3  k_update_direction: X += alpha V, AX += alpha AV (Alg. 2 l.12, applied
+//       lazily), G = g_m(X) (eq:gradientf1/g1/f2/g2) and the column
+//       dots of Alg. 2 l.9;
+//   C4  k_direction_gram: V = -G + beta Vp (Alg. 2 l.10) fused with the Grams
+//       Q = V^T V, P = V^T X of the line-search cubics.
+// Row tiles (TR rows x KP columns) are contiguous in HBM, so each operand tile
+// is one 1-D TMA bulk copy (cp.async.bulk) into an S-stage shared-memory ring
+// completed on an mbarrier; results leave through TMA bulk stores from the same
+// stage buffers.  The N x k . k x k products and the Grams run on the fp64
+// tensor path (mma.sync m8n8k4 f64 = DMMA.8x8x4) from padded smem copies.
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace ofsc {
+
+template <typename T>
+__device__ __forceinline__ double rndT(double v) { return (double)(T)v; }
+
+constexpr int kSTR = 16;   // rows per streamed tile
+constexpr int kSST = 3;    // pipeline stages
+
+template <typename T, int KP>
+struct StreamTile {
+  static constexpr int LD = KP + 4;                                // padded double stride
+  static constexpr uint32_t ARR = kSTR * KP * sizeof(T);           // bytes of one full tile array
+};
+
+// ---------------------------------------------------------------------------
+// C3
+// ---------------------------------------------------------------------------
+template <typename T, int KP, int METHOD>
+struct C3Smem {
+  static constexpr bool USE_W = (METHOD == OFSC_OFM_F2 || METHOD == OFSC_TRIOFM_F2);
+  static constexpr int LD = KP + 4;
+  static constexpr size_t ms = (size_t)KP * LD * 8;
+  static constexpr size_t ws = USE_W ? ms : 0;
+  static constexpr size_t xp = (size_t)kSTR * LD * 8;
+  static constexpr size_t arr = (size_t)kSTR * KP * sizeof(T);
+  static constexpr size_t stage = 5 * arr;                          // X, AX, V, AV, G
+  static constexpr size_t bytes = ms + ws + 2 * xp + kSST * stage + KP * 8 + kSST * 8;
+};
+
+template <typename T, int KP, int METHOD>
+__global__ void __launch_bounds__(kThreads, 1)
+k_update_direction(IterParams p, int apply_update) {
+  using S = C3Smem<T, KP, METHOD>;
+  constexpr int LD = S::LD;
+  constexpr bool TRI = (METHOD == OFSC_TRIOFM_F1 || METHOD == OFSC_TRIOFM_F2);
+  constexpr bool F1 = (METHOD == OFSC_OFM_F1 || METHOD == OFSC_TRIOFM_F1);
+  constexpr int NB = KP / 8;
+  if (p.ctl->stop) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* Ms = (double*)smraw;
+  double* Ws = (double*)(smraw + S::ms);
+  double* Xp = (double*)(smraw + S::ms + S::ws);
+  double* AXp = Xp + kSTR * LD;
+  unsigned char* stg = smraw + S::ms + S::ws + 2 * S::xp;
+  double* s_alpha = (double*)(stg + kSST * S::stage);
+  uint64_t* bar = (uint64_t*)(s_alpha + KP);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int64_t ntiles = (p.n_local + kSTR - 1) / kSTR;
+  T* gX = (T*)p.X;
+  T* gAX = (T*)p.AX;
+  T* gG = (T*)p.G;
+  const T* gV = (const T*)p.V;
+  const T* gAV = (const T*)p.AV;
+  auto arr = [&](int st, int a) { return (T*)(stg + st * S::stage + a * S::arr); };  // 0 X,1 AX,2 V,3 AV,4 G
+  auto issue = [&](int st, int64_t tile) {
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, p.n_local - row0);
+    const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+    mbar_arrive_expect_tx(&bar[st], (apply_update ? 5u : 3u) * b);
+    const int64_t off = row0 * KP;
+    bulk_g2s(arr(st, 0), gX + off, b, &bar[st]);
+    bulk_g2s(arr(st, 1), gAX + off, b, &bar[st]);
+    if (apply_update) {
+      bulk_g2s(arr(st, 2), gV + off, b, &bar[st]);
+      bulk_g2s(arr(st, 3), gAV + off, b, &bar[st]);
+    }
+    bulk_g2s(arr(st, 4), gG + off, b, &bar[st]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kSST; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  for (int e = tid; e < KP * KP; e += kThreads) {
+    const int j = e / KP, c = e % KP;
+    const bool keep = !TRI || j <= c;              // triu keeps the diagonal (R15)
+    Ms[j * LD + c] = keep ? p.M[e] : 0.0;
+    if (S::USE_W) Ws[j * LD + c] = keep ? p.W[e] : 0.0;
+  }
+  if (tid < KP) s_alpha[tid] = apply_update ? p.alpha[tid] : 0.0;
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < kSST; ++s) {
+      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+      if (tile < ntiles) issue(s, tile);
+    }
+  // per-lane column dots: columns cb*8 + 2 tig (+1) for the lane's cb slots
+  const int rb = warp >> 2, wp = warp & 3;
+  double gg[2][2] = {{0, 0}, {0, 0}}, dg[2][2] = {{0, 0}, {0, 0}};
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kSST;
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, p.n_local - row0);
+    mbar_wait(&bar[st], (uint32_t)((it / kSST) & 1));
+    T* sX = arr(st, 0);
+    T* sAX = arr(st, 1);
+    const T* sV = arr(st, 2);
+    const T* sAV = arr(st, 3);
+    T* sG = arr(st, 4);
+    // phase A: X' = X + alpha V, AX' = AX + alpha AV (rounded to storage), padded copies
+    for (int e = tid; e < kSTR * KP; e += kThreads) {
+      const int r = e / KP, c = e % KP;
+      double x = 0.0, ax = 0.0;
+      if (r < rows) {
+        x = (double)sX[e];
+        ax = (double)sAX[e];
+        if (apply_update) {
+          x = rndT<T>(x + s_alpha[c] * (double)sV[e]);
+          ax = rndT<T>(ax + s_alpha[c] * (double)sAV[e]);
+          sX[e] = (T)x;
+          sAX[e] = (T)ax;
+        }
+      }
+      Xp[r * LD + c] = x;
+      AXp[r * LD + c] = ax;
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0 && apply_update) {
+      const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+      bulk_s2g(gX + row0 * KP, sX, b);
+      bulk_s2g(gAX + row0 * KP, sAX, b);
+      bulk_commit();
+    }
+    // phase B: G tile = f(X' M, X' W, AX' M) on DMMA.  Warp: row block rb, column
+    // blocks wp and wp + 4.
+    double a1[2][2] = {{0, 0}, {0, 0}}, a2[2][2] = {{0, 0}, {0, 0}};
+    const double* xrow = Xp + (rb * 8 + gid) * LD + tig;
+    const double* arow = AXp + (rb * 8 + gid) * LD + tig;
+#pragma unroll 4
+    for (int j0 = 0; j0 < KP; j0 += 4) {
+      const double xa = xrow[j0];
+      const double aa = F1 ? 0.0 : arow[j0];
+      const int mrow = (j0 + tig) * LD + gid;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int cb = wp + 4 * u;
+        if (cb < NB) {
+          const double m = Ms[mrow + cb * 8];
+          if (F1) {
+            dmma(a1[u][0], a1[u][1], xa, m);                 // X M (or X triu M)
+          } else {
+            const double w = Ws[mrow + cb * 8];
+            dmma(a1[u][0], a1[u][1], xa, w);                 // X W (or X triu W)
+            dmma(a2[u][0], a2[u][1], aa, m);                 // AX M (or AX triu M)
+          }
+        }
+      }
+    }
+    // phase C: G, column dots, in-place store into the stage's G tile
+    const int r = rb * 8 + gid;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int cb = wp + 4 * u;
+      if (cb < NB && r < rows) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = cb * 8 + 2 * tig + h;
+          const double ax = AXp[r * LD + c];
+          double g;
+          if (METHOD == OFSC_OFM_F1) g = 4.0 * ax + 4.0 * a1[u][h];
+          else if (METHOD == OFSC_TRIOFM_F1) g = ax + a1[u][h];
+          else if (METHOD == OFSC_OFM_F2) g = 4.0 * ax - 2.0 * a1[u][h] - 2.0 * a2[u][h];
+          else g = 2.0 * ax - a2[u][h] - a1[u][h];
+          g = rndT<T>(g);
+          const double gp = (double)sG[r * KP + c];
+          sG[r * KP + c] = (T)g;
+          gg[u][h] = fma(g, g, gg[u][h]);
+          dg[u][h] = fma(g - gp, g, dg[u][h]);
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(gG + row0 * KP, sG, (uint32_t)rows * KP * sizeof(T));
+      bulk_commit();
+      const int64_t nxt = tile + (int64_t)kSST * gridDim.x;
+      if (nxt < ntiles) {
+        bulk_wait_read_all();                     // stage st no longer read by the stores
+        issue(st, nxt);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+  // column partials: reduce over gid (lanes), then over the two row-block warps
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        gg[u][h] += __shfl_xor_sync(0xffffffffu, gg[u][h], o);
+        dg[u][h] += __shfl_xor_sync(0xffffffffu, dg[u][h], o);
+      }
+  __syncthreads();
+  double* red = Xp;   // [2 rb][2][KP]
+  if (gid == 0) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int cb = wp + 4 * u;
+      if (cb < NB)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = cb * 8 + 2 * tig + h;
+          red[rb * 2 * KP + c] = gg[u][h];
+          red[rb * 2 * KP + KP + c] = dg[u][h];
+        }
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * KP) p.part_cols[(int64_t)blockIdx.x * 2 * KP + tid] = red[tid] + red[2 * KP + tid];
+}
+
+template <typename T, int KP, int METHOD>
+static void launch_c3(const IterParams& p, int apply, int nblk, cudaStream_t s) {
+  const size_t smem = C3Smem<T, KP, METHOD>::bytes;
+  auto kern = k_update_direction<T, KP, METHOD>;
+  static bool set = false;
+  if (!set) {
+    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = true;
+  }
+  kern<<<nblk, kThreads, smem, s>>>(p, apply);
+  OFSC_LAUNCH_CHECK();
+}
+
+static int stream_grid(int64_t n_rows, size_t smem_bytes) {
+  // resident CTAs per SM allowed by shared memory (227 KB usable, ~1 KB reserved per CTA)
+  int per_sm = (int)((232448) / (smem_bytes + 1024));
+  per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+  const int64_t tiles = (n_rows + kSTR - 1) / kSTR;
+  int64_t g = (int64_t)num_sms() * per_sm;
+  if (tiles < g) g = tiles;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n) {
+  size_t b = 0;
+  OFSC_DISPATCH_KP(KP, {
+    const bool f2 = method == OFSC_OFM_F2 || method == OFSC_TRIOFM_F2;
+    if (dt == OFSC_F64) b = f2 ? C3Smem<double, KPC, 2>::bytes : C3Smem<double, KPC, 0>::bytes;
+    else b = f2 ? C3Smem<float, KPC, 2>::bytes : C3Smem<float, KPC, 0>::bytes;
+  });
+  return stream_grid(n, b);
+}
+
+void launch_update_direction(ofsc_dtype dt, const IterParams& p, int apply_update, int nblk,
+                             cudaStream_t s) {
+  OFSC_DISPATCH_KP(p.KP, {
+    if (dt == OFSC_F64) {
+      switch (p.method) {
+        case 0: launch_c3<double, KPC, 0>(p, apply_update, nblk, s); break;
+        case 1: launch_c3<double, KPC, 1>(p, apply_update, nblk, s); break;
+        case 2: launch_c3<double, KPC, 2>(p, apply_update, nblk, s); break;
+        default: launch_c3<double, KPC, 3>(p, apply_update, nblk, s); break;
+      }
+    } else {
+      switch (p.method) {
+        case 0: launch_c3<float, KPC, 0>(p, apply_update, nblk, s); break;
+        case 1: launch_c3<float, KPC, 1>(p, apply_update, nblk, s); break;
+        case 2: launch_c3<float, KPC, 2>(p, apply_update, nblk, s); break;
+        default: launch_c3<float, KPC, 3>(p, apply_update, nblk, s); break;
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// C4
+// ---------------------------------------------------------------------------
+template <typename T, int KP>
+struct C4Smem {
+  static constexpr int LD = KP + 4;
+  static constexpr size_t pad = (size_t)kSTR * LD * 8;
+  static constexpr size_t arr = (size_t)kSTR * KP * sizeof(T);
+  static constexpr size_t stage = 3 * arr;                           // G, Vp, X
+  static constexpr size_t bytes = 2 * pad + kSST * stage + KP * 8 + kSST * 8;
+};
+
+template <typename T, int KP>
+__global__ void __launch_bounds__(kThreads, 2) k_direction_gram(IterParams p) {
+  using S = C4Smem<T, KP>;
+  constexpr int LD = S::LD;
+  if (p.ctl->stop) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* Vd = (double*)smraw;
+  double* Xd = Vd + kSTR * LD;
+  unsigned char* stg = smraw + 2 * S::pad;
+  double* s_beta = (double*)(stg + kSST * S::stage);
+  uint64_t* bar = (uint64_t*)(s_beta + KP);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (p.n_local + kSTR - 1) / kSTR;
+  const T* gG = (const T*)p.G;
+  T* gV = (T*)p.V;
+  const T* gX = (const T*)p.X;
+  auto arr = [&](int st, int a) { return (T*)(stg + st * S::stage + a * S::arr); };  // 0 G, 1 V, 2 X
+  auto issue = [&](int st, int64_t tile) {
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, p.n_local - row0);
+    const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+    mbar_arrive_expect_tx(&bar[st], 3u * b);
+    bulk_g2s(arr(st, 0), gG + row0 * KP, b, &bar[st]);
+    bulk_g2s(arr(st, 1), gV + row0 * KP, b, &bar[st]);
+    bulk_g2s(arr(st, 2), gX + row0 * KP, b, &bar[st]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kSST; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  if (tid < KP) s_beta[tid] = p.beta[tid];
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < kSST; ++s) {
+      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+      if (tile < ntiles) issue(s, tile);
+    }
+  DmmaGram<KP> acc;
+  acc.zero();
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kSST;
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, p.n_local - row0);
+    mbar_wait(&bar[st], (uint32_t)((it / kSST) & 1));
+    const T* sG = arr(st, 0);
+    T* sV = arr(st, 1);
+    const T* sX = arr(st, 2);
+    for (int e = tid; e < kSTR * KP; e += kThreads) {
+      const int r = e / KP, c = e % KP;
+      double v = 0.0, x = 0.0;
+      if (r < rows) {
+        v = rndT<T>(-(double)sG[e] + s_beta[c] * (double)sV[e]);
+        x = (double)sX[e];
+        sV[e] = (T)v;
+      }
+      Vd[r * LD + c] = v;
+      Xd[r * LD + c] = x;
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(gV + row0 * KP, sV, (uint32_t)rows * KP * sizeof(T));
+      bulk_commit();
+    }
+    acc.accumulate(Vd, Vd, Vd, Xd, (rows + 3) & ~3, warp, lane);   // Q = V^T V, P = V^T X
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t nxt = tile + (int64_t)kSST * gridDim.x;
+      if (nxt < ntiles) {
+        bulk_wait_read_all();
+        issue(st, nxt);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+  acc.store(p.part_g4 + (int64_t)blockIdx.x * 2 * KP * KP, warp, lane);
+}
+
+template <typename T, int KP>
+static void launch_c4(const IterParams& p, int nblk, cudaStream_t s) {
+  const size_t smem = C4Smem<T, KP>::bytes;
+  auto kern = k_direction_gram<T, KP>;
+  static bool set = false;
+  if (!set) {
+    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = true;
+  }
+  kern<<<nblk, kThreads, smem, s>>>(p);
+  OFSC_LAUNCH_CHECK();
+}
+
+int c4_grid(ofsc_dtype dt, int KP, int64_t n) {
+  size_t b = 0;
+  OFSC_DISPATCH_KP(KP, {
+    b = dt == OFSC_F64 ? C4Smem<double, KPC>::bytes : C4Smem<float, KPC>::bytes;
+  });
+  return stream_grid(n, b);
+}
+
+void launch_direction_gram(ofsc_dtype dt, const IterParams& p, int nblk, cudaStream_t s) {
+  OFSC_DISPATCH_KP(p.KP, {
+    if (dt == OFSC_F64) launch_c4<double, KPC>(p, nblk, s);
+    else launch_c4<float, KPC>(p, nblk, s);
+  });
+}
+
+}  // namespace ofsc

@@ -1,0 +1,153 @@
+// sm_100a building blocks: TMA bulk copies (cp.async.bulk) with mbarrier
+// completion, and the fp64 tensor-core MMA (mma.sync m8n8k4 f64 -> DMMA.8x8x4;
+// tcgen05 has no f64 kind, measured 37.1 TF/s vs 33.4 for DFMA, profiles/r01).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ofsc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// ---- mbarrier --------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+// ---- TMA bulk copies (1-D, 16-byte aligned, size multiple of 16) -------------
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy smem writes -> visible to the async proxy (TMA store reads)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---- fp64 MMA: D(8x8) += A(8x4) B(4x8) --------------------------------------
+// Fragments (PTX ISA, m8n8k4 .f64): gid = lane >> 2, tig = lane & 3;
+//   a = A[gid][tig], b = B[tig][gid], d0 = D[gid][2 tig], d1 = D[gid][2 tig + 1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Warp tiling of a KP x KP output into 8x8 MMA blocks for 4 warps:
+// warp wp (0..3) owns blocks ib in [IB0, IB0 + BI), jb in [JB0, JB0 + BJ).
+template <int KP>
+struct WarpTiling;
+template <>
+struct WarpTiling<16> {
+  static constexpr int BI = 1, BJ = 1;
+  __device__ static int ib0(int wp) { return wp >> 1; }
+  __device__ static int jb0(int wp) { return wp & 1; }
+};
+template <>
+struct WarpTiling<32> {
+  static constexpr int BI = 1, BJ = 4;
+  __device__ static int ib0(int wp) { return wp; }
+  __device__ static int jb0(int) { return 0; }
+};
+template <>
+struct WarpTiling<48> {
+  static constexpr int BI = 3, BJ = 3;
+  __device__ static int ib0(int wp) { return 3 * (wp >> 1); }
+  __device__ static int jb0(int wp) { return 3 * (wp & 1); }
+};
+template <>
+struct WarpTiling<64> {
+  static constexpr int BI = 2, BJ = 8;
+  __device__ static int ib0(int wp) { return 2 * wp; }
+  __device__ static int jb0(int) { return 0; }
+};
+
+// Two k x k Gram products over a tile of `rows` rows held in padded smem
+// (row stride LD = KP + 4 doubles: the 4-row x 8-column fragment reads hit
+// every bank exactly twice, i.e. the 2-wavefront minimum):
+//   acc(prod 0) += L1^T R1 (warps 0-3),  acc(prod 1) += L2^T R2 (warps 4-7).
+template <int KP>
+struct DmmaGram {
+  static constexpr int LD = KP + 4;
+  using WT = WarpTiling<KP>;
+  static constexpr int BI = WT::BI, BJ = WT::BJ;
+  double d[BI][BJ][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < BI; ++i)
+#pragma unroll
+      for (int j = 0; j < BJ; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+  }
+  // rows: multiple of 4 (tiles are zero-padded to that); 8 warps
+  __device__ __forceinline__ void accumulate(const double* L1, const double* R1, const double* L2,
+                                             const double* R2, int rows, int warp, int lane) {
+    const int gid = lane >> 2, tig = lane & 3, wp = warp & 3;
+    const double* L = (warp >> 2) ? L2 : L1;
+    const double* R = (warp >> 2) ? R2 : R1;
+    const double* Lc = L + WT::ib0(wp) * 8 + gid;
+    const double* Rc = R + WT::jb0(wp) * 8 + gid;
+    for (int r0 = 0; r0 < rows; r0 += 4) {
+      const int rr = (r0 + tig) * LD;
+      double a[BI], b[BJ];
+#pragma unroll
+      for (int i = 0; i < BI; ++i) a[i] = Lc[rr + i * 8];
+#pragma unroll
+      for (int j = 0; j < BJ; ++j) b[j] = Rc[rr + j * 8];
+#pragma unroll
+      for (int i = 0; i < BI; ++i)
+#pragma unroll
+        for (int j = 0; j < BJ; ++j) dmma(d[i][j][0], d[i][j][1], a[i], b[j]);
+    }
+  }
+  // out[prod][i][j] (row-major KP x KP each); prod = warp >> 2
+  __device__ __forceinline__ void store(double* out, int warp, int lane) const {
+    const int gid = lane >> 2, tig = lane & 3, wp = warp & 3;
+    double* o = out + (warp >> 2) * KP * KP;
+#pragma unroll
+    for (int i = 0; i < BI; ++i)
+#pragma unroll
+      for (int j = 0; j < BJ; ++j) {
+        double* q = o + ((WT::ib0(wp) + i) * 8 + gid) * KP + (WT::jb0(wp) + j) * 8 + 2 * tig;
+        q[0] = d[i][j][0];
+        q[1] = d[i][j][1];
+      }
+  }
+};
+
+}  // namespace ofsc
