@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--method", default="ofm_f2")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--refresh", type=int, default=0)
+    ap.add_argument("--reorder", type=int, default=1, help="1: LPA locality reordering of the rows")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -177,13 +178,17 @@ def run_ours(args):
 
     ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev_a.record(stream)
-    g = ofsc.Graph(cfg.n, src, dst, comm=comm)
+    g = ofsc.Graph(cfg.n, src, dst, comm=comm, reorder=bool(args.reorder))
     ev_b.record(stream)
     torch.cuda.synchronize()
     build_ms = ev_a.elapsed_time(ev_b)
     info = g.info
     rb, re_ = info["row_begin"], info["row_end"]
-    X0 = x0_block(cfg.n, k, cfg.seed_x0)[rb:re_]
+    X0full = x0_block(cfg.n, k, cfg.seed_x0)
+    if world == 1:
+        X0 = X0full                                   # original order; the library permutes
+    else:                                             # p > 1: this rank's internal rows
+        X0 = X0full[g.copy_perm()[rb:re_]] if info["reordered"] else X0full[rb:re_]
     X0d = torch.from_numpy(X0).to(tdt).cuda()
     W, K = args.warmup, args.steps
 
@@ -245,7 +250,11 @@ def run_ours(args):
                    "refresh": args.refresh, "global_batch": cfg.n, "parallelism": f"row-partition p={world}",
                    "l2": "inputs larger than L2 (each N x k block 2.56 GB vs 126 MB L2)" if cfg.n * k * es > 2e8 else "working set partly L2-resident",
                    "graph_gen_s": round(gen_s, 1), "graph_build_ms": round(build_ms, 2),
-                   "load_imbalance": info["load_imbalance"]},
+                   "load_imbalance": info["load_imbalance"],
+                   "reorder": ("LPA locality reordering derived from the graph (%d communities, "
+                               "%.3f of nnz intra-community)" % (info["n_communities"],
+                                                                  info["intra_edge_fraction"]))
+                   if info["reordered"] else "none (random node ids)"},
         "roofline": roofline,
         "iteration_hbm": {"algorithmic_bytes_per_iter_per_gpu": it_bytes,
                           "achieved_gbs_per_gpu": round(it_bytes * (K / (ms / 1e3)) / 1e9, 1),
@@ -266,11 +275,11 @@ def run_ours(args):
 
     # --- e2e through the C ABI with pinned host buffers ---
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, cfg, comm, src, dst, X0, world, rank, barrier, max_over_ranks)
+        out["e2e"] = run_e2e(args, cfg, comm, src, dst, X0full, world, rank, barrier, max_over_ranks)
 
     # --- CPU baseline: the oracle on the host cores (rank 0, N = 1 only) ---
     if world == 1 and rank == 0 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(cfg, args.method, src, dst, X0)
+        out["cpu_baseline"] = cpu_baseline(cfg, args.method, src, dst, X0full)
 
     if world > 1:
         dist.barrier()
@@ -292,10 +301,10 @@ def run_e2e(args, cfg, comm, src, dst, X0, world, rank, barrier, max_over_ranks)
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
     h_src = torch.from_numpy(src).pin_memory()
     h_dst = torch.from_numpy(dst).pin_memory()
-    h_X0 = torch.from_numpy(X0).to(tdt).pin_memory()
+    h_X0 = torch.from_numpy(X0).to(tdt).pin_memory()          # all n rows, original order
     h_X = torch.empty_like(h_X0).pin_memory()
     rows = torch.from_numpy(kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)).pin_memory()
-    h_lab = torch.empty(X0.shape[0], dtype=torch.int32).pin_memory()
+    h_lab = torch.empty(cfg.n, dtype=torch.int32).pin_memory()
     o = ofsc.make_opts(k, T, refresh=args.refresh)
     stream = torch.cuda.current_stream()
     times = []
@@ -305,10 +314,11 @@ def run_e2e(args, cfg, comm, src, dst, X0, world, rank, barrier, max_over_ranks)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         a.record(stream)
+        bo = ofsc.BuildOpts(1 if args.reorder else 0, 8)
         st = L.ofsc_spectral_cluster(comm.handle if comm else None, cfg.n, src.size,
                                      C.c_void_p(h_src.data_ptr()), C.c_void_p(h_dst.data_ptr()),
                                      ofsc.METHODS[args.method], ofsc.DTYPES[args.dtype], C.byref(o),
-                                     C.c_void_p(h_X.data_ptr()), cfg.blocks,
+                                     C.byref(bo), C.c_void_p(h_X.data_ptr()), cfg.blocks,
                                      C.c_void_p(rows.data_ptr()), 100,
                                      C.c_void_p(h_lab.data_ptr()), C.byref(rep),
                                      C.c_void_p(stream.cuda_stream))
@@ -323,7 +333,7 @@ def run_e2e(args, cfg, comm, src, dst, X0, world, rank, barrier, max_over_ranks)
         ari, nmi = ofsc.scores(h_lab.numpy(), config_graph(cfg)[2])
     es = 8 if args.dtype == "f64" else 4
     h2d = src.nbytes + dst.nbytes + X0.shape[0] * k * es + rows.numel() * 8
-    d2h = X0.shape[0] * k * es + X0.shape[0] * 4
+    d2h = X0.shape[0] * k * es + cfg.n * 4
     return {"value": round(T / (ms / 1e3), 3), "unit": "it/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_call": round(ms, 2), "iters_per_call": T,
             "calls_timed": len(times),

@@ -107,19 +107,42 @@ typedef struct {
   int64_t max_degree;
   double fro2_A;                /* ||A||_F^2 = n + sum_ij (s_i s_j)^2 */
   double load_imbalance;        /* p * max_r nnz_r / nnz */
+  int32_t reordered;            /* 1 if rows were reordered by ofsc_build_opts.reorder */
+  int64_t n_communities;        /* label-propagation communities (reordered graphs) */
+  double intra_edge_fraction;   /* fraction of nnz joining two nodes of one community */
 } ofsc_graph_info;
+
+/* Build options.  reorder = 1: a locality reordering of the rows derived from
+ * the graph itself (semi-synchronous label propagation, `lpa_sweeps` sweeps;
+ * nodes ordered by (community, id)) so the SpMM's neighbour gathers hit L2.
+ * The operator is the same matrix with permuted rows/columns (P A P^T); the
+ * mathematics of every call is unchanged.  Internal row i is node perm[i]
+ * (ofsc_graph_copy_perm).  With p == 1, ofsc_run / ofsc_graph_apply(_gram)
+ * take and return rows in the caller's ORIGINAL node order (the library
+ * permutes); with p > 1, a rank's local rows are internal rows
+ * [row_begin, row_end), i.e. nodes perm[row_begin .. row_end). */
+typedef struct {
+  int32_t reorder;     /* 0 = keep node ids (default of ofsc_graph_build), 1 = LPA reorder */
+  int32_t lpa_sweeps;  /* default 8 */
+} ofsc_build_opts;
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
                              const int64_t* dst, int edges_on_device, ofsc_stream stream,
                              ofsc_graph* out);
+ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
+                                const int64_t* dst, int edges_on_device,
+                                const ofsc_build_opts* bopts, ofsc_stream stream, ofsc_graph* out);
 ofsc_status ofsc_graph_info_get(ofsc_graph g, ofsc_graph_info* out);
 /* Copy this rank's CSR to host: h_row_ptr[n_local+1] (offsets from 0),
- * h_col[nnz_local] (global ids), h_s[n] (full). Any pointer may be NULL. */
+ * h_col[nnz_local] (internal global ids), h_s[n] (internal order). Any pointer may be NULL. */
 ofsc_status ofsc_graph_copy_csr(ofsc_graph g, int64_t* h_row_ptr, int32_t* h_col, double* h_s);
+/* h_perm[n]: internal row -> original node id (identity unless reordered). */
+ofsc_status ofsc_graph_copy_perm(ofsc_graph g, int32_t* h_perm);
 ofsc_status ofsc_graph_destroy(ofsc_graph g);
 
 /* Y = A Z for this rank's rows (the SpMM of eq:spmm P:440, values implicit).
- * d_Z: all n rows (n x ldz) on every rank; d_Y: local rows (n_local x ldy). */
+ * d_Z: all n rows (n x ldz, original node order) on every rank; d_Y: local
+ * rows (n_local x ldy; original order when p == 1, internal order when p > 1). */
 ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_Z,
                              int64_t ldz, void* d_Y, int64_t ldy, ofsc_stream stream);
 
@@ -221,16 +244,19 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
 ofsc_status ofsc_scores(int64_t n, const int32_t* h_a, const int32_t* h_b, double* ari,
                         double* nmi);
 
-/* Algorithm 1 end to end from HOST buffers: edges (m, full list) -> build A ->
- * run `method` from h_X (local rows x k, dense ld = k, dtype dt; in: X0, out:
- * features before normalisation) -> row-normalise -> K-means with centroids
- * initialised at the global rows h_init_rows[n_clusters] of the normalised
- * features -> h_labels (local rows).  Copies host<->device inside the call. */
+/* Algorithm 1 end to end from HOST buffers: edges (m, full list) -> build A
+ * (bopts may be NULL: LPA locality reordering on) -> run `method` from h_X
+ * (ALL n rows x k in original node order, dense ld = k, dtype dt; in: X0, out:
+ * features before normalisation for the nodes this rank owns) -> row-normalise
+ * -> K-means with centroids initialised at the original node ids
+ * h_init_rows[n_clusters] of the normalised features -> h_labels[n] (filled
+ * for the nodes this rank owns).  Copies host<->device inside the call. */
 ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t m, const int64_t* h_src,
                                   const int64_t* h_dst, ofsc_method method, ofsc_dtype dt,
-                                  const ofsc_opts* opts, void* h_X, int32_t n_clusters,
-                                  const int64_t* h_init_rows, int32_t km_max_iters,
-                                  int32_t* h_labels, ofsc_report* rep, ofsc_stream stream);
+                                  const ofsc_opts* opts, const ofsc_build_opts* bopts, void* h_X,
+                                  int32_t n_clusters, const int64_t* h_init_rows,
+                                  int32_t km_max_iters, int32_t* h_labels, ofsc_report* rep,
+                                  ofsc_stream stream);
 
 #ifdef __cplusplus
 }

@@ -64,10 +64,16 @@ class GraphInfo(C.Structure):
                 ("row_begin", C.c_int64), ("row_end", C.c_int64), ("nnz_local", C.c_int64),
                 ("n_isolated", C.c_int64), ("n_self_loops_dropped", C.c_int64),
                 ("n_duplicates_dropped", C.c_int64), ("max_degree", C.c_int64),
-                ("fro2_A", C.c_double), ("load_imbalance", C.c_double)]
+                ("fro2_A", C.c_double), ("load_imbalance", C.c_double),
+                ("reordered", C.c_int32), ("n_communities", C.c_int64),
+                ("intra_edge_fraction", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class BuildOpts(C.Structure):
+    _fields_ = [("reorder", C.c_int32), ("lpa_sweeps", C.c_int32)]
 
 
 # exported symbol -> (restype, argtypes); mirrors include/ofsc.h
@@ -83,8 +89,11 @@ SIGNATURES = {
     "ofsc_comm_create": (_ST, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "ofsc_comm_destroy": (_ST, [_P]),
     "ofsc_graph_build": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, _P, C.POINTER(_P)]),
+    "ofsc_graph_build_ex": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, C.POINTER(BuildOpts), _P,
+                                  C.POINTER(_P)]),
     "ofsc_graph_info_get": (_ST, [_P, C.POINTER(GraphInfo)]),
     "ofsc_graph_copy_csr": (_ST, [_P, _P, _P, _P]),
+    "ofsc_graph_copy_perm": (_ST, [_P, _P]),
     "ofsc_graph_destroy": (_ST, [_P]),
     "ofsc_graph_apply": (_ST, [_P, _ST, _I32, _P, _I64, _P, _I64, _P]),
     "ofsc_graph_apply_gram": (_ST, [_P, _ST, _I32, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
@@ -96,8 +105,9 @@ SIGNATURES = {
     "ofsc_row_normalize": (_ST, [_ST, _I64, _I32, _P, _I64, _P, _I64, _P]),
     "ofsc_kmeans": (_ST, [_P, _ST, _I64, _I32, _P, _I64, _I32, _P, _I32, _P, _P, _P, _P]),
     "ofsc_scores": (_ST, [_I64, _P, _P, _P, _P]),
-    "ofsc_spectral_cluster": (_ST, [_P, _I64, _I64, _P, _P, _ST, _ST, C.POINTER(Opts), _P,
-                                    _I32, _P, _I32, _P, C.POINTER(Report), _P]),
+    "ofsc_spectral_cluster": (_ST, [_P, _I64, _I64, _P, _P, _ST, _ST, C.POINTER(Opts),
+                                    C.POINTER(BuildOpts), _P, _I32, _P, _I32, _P,
+                                    C.POINTER(Report), _P]),
 }
 
 _lib = None
@@ -198,24 +208,26 @@ class Comm:
 class Graph:
     """Shifted normalised Laplacian A = L - 2I of an undirected graph."""
 
-    def __init__(self, n, src, dst, comm: Comm | None = None, stream=None):
+    def __init__(self, n, src, dst, comm: Comm | None = None, stream=None, reorder=False,
+                 lpa_sweeps=8):
         torch = _torch()
         self.n = int(n)
         self.comm = comm
         h = C.c_void_p()
+        bo = BuildOpts(1 if reorder else 0, int(lpa_sweeps))
         if isinstance(src, torch.Tensor) and src.is_cuda:
             s = src.to(torch.int64).contiguous()
             d = dst.to(torch.int64).contiguous()
-            _check(lib().ofsc_graph_build(comm.handle if comm else None, self.n, s.numel(),
-                                          C.c_void_p(s.data_ptr()), C.c_void_p(d.data_ptr()), 1,
-                                          _stream(stream), C.byref(h)))
+            _check(lib().ofsc_graph_build_ex(comm.handle if comm else None, self.n, s.numel(),
+                                             C.c_void_p(s.data_ptr()), C.c_void_p(d.data_ptr()),
+                                             1, C.byref(bo), _stream(stream), C.byref(h)))
         else:
             s = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
             d = np.ascontiguousarray(np.asarray(dst, dtype=np.int64))
-            _check(lib().ofsc_graph_build(comm.handle if comm else None, self.n, s.size,
-                                          s.ctypes.data_as(C.c_void_p),
-                                          d.ctypes.data_as(C.c_void_p), 0, _stream(stream),
-                                          C.byref(h)))
+            _check(lib().ofsc_graph_build_ex(comm.handle if comm else None, self.n, s.size,
+                                             s.ctypes.data_as(C.c_void_p),
+                                             d.ctypes.data_as(C.c_void_p), 0, C.byref(bo),
+                                             _stream(stream), C.byref(h)))
         self.handle = h
         self.info = self.get_info()
 
@@ -237,6 +249,12 @@ class Graph:
                                          col.ctypes.data_as(C.c_void_p),
                                          s.ctypes.data_as(C.c_void_p)))
         return rp, col[:self.info["nnz_local"]], s
+
+    def copy_perm(self):
+        """perm[i] = original node id of internal row i (identity unless reordered)."""
+        perm = np.empty(self.n, np.int32)
+        _check(lib().ofsc_graph_copy_perm(self.handle, perm.ctypes.data_as(C.c_void_p)))
+        return perm
 
     def apply(self, Z, Y=None, stream=None):
         """Y = A Z for the local rows (Z holds all n rows)."""
@@ -381,25 +399,28 @@ def scores(a, b):
 
 
 def spectral_cluster(n, src, dst, method, X0, n_clusters, init_rows, *, max_iters,
-                     dtype="f64", km_max_iters=100, comm: Comm | None = None, stream=None,
-                     **run_opts):
+                     dtype="f64", km_max_iters=100, reorder=True, comm: Comm | None = None,
+                     stream=None, **run_opts):
     """Algorithm 1 end to end from host buffers (ofsc_spectral_cluster).
 
-    X0: host (local rows x k) array (copied; features returned); returns
-    (labels int32[n_local], features, report)."""
+    X0: host (n x k) array, original node order (copied; features returned).
+    Returns (labels int32[n], features, report); with several ranks each rank
+    fills the entries of the nodes it owns."""
     npdt = np.float64 if dtype == "f64" else np.float32
     X = np.ascontiguousarray(np.array(X0, dtype=npdt))
     src = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
     dst = np.ascontiguousarray(np.asarray(dst, dtype=np.int64))
     rows = np.ascontiguousarray(np.asarray(init_rows, dtype=np.int64))
-    labels = np.empty(X.shape[0], np.int32)
+    labels = np.full(X.shape[0], -1, np.int32)
     o = make_opts(X.shape[1], max_iters, **run_opts)
+    bo = BuildOpts(1 if reorder else 0, 8)
     rep = Report()
     _check(lib().ofsc_spectral_cluster(comm.handle if comm else None, int(n), src.size,
                                        src.ctypes.data_as(C.c_void_p),
                                        dst.ctypes.data_as(C.c_void_p), METHODS[method],
-                                       DTYPES[dtype], C.byref(o), X.ctypes.data_as(C.c_void_p),
-                                       int(n_clusters), rows.ctypes.data_as(C.c_void_p),
-                                       int(km_max_iters), labels.ctypes.data_as(C.c_void_p),
-                                       C.byref(rep), _stream(stream) if stream is not None else None))
+                                       DTYPES[dtype], C.byref(o), C.byref(bo),
+                                       X.ctypes.data_as(C.c_void_p), int(n_clusters),
+                                       rows.ctypes.data_as(C.c_void_p), int(km_max_iters),
+                                       labels.ctypes.data_as(C.c_void_p), C.byref(rep),
+                                       _stream(stream) if stream is not None else None))
     return labels, X, rep.as_dict()

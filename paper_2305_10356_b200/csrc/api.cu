@@ -110,8 +110,12 @@ struct ofsc_graph_s {
   int32_t* col = nullptr;          // slot ids (== global ids when p == 1)
   double* s_slot = nullptr;        // [p * slot_rows]
   float* s32_slot = nullptr;
+  int32_t* perm = nullptr;         // internal row -> original node (reordered graphs)
+  bool reordered = false;
   ofsc_graph_info info{};
   Workspace ws;
+  // permutation applied at the user boundary (p == 1 only; p > 1 uses internal order)
+  const int32_t* user_perm() const { return (reordered && p == 1) ? perm : nullptr; }
 };
 
 extern "C" {
@@ -197,15 +201,26 @@ static void graph_free(ofsc_graph g) {
   dfree(g->col);
   dfree(g->s_slot);
   dfree(g->s32_slot);
+  dfree(g->perm);
 }
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
                              const int64_t* dst, int edges_on_device, ofsc_stream stream,
                              ofsc_graph* out) {
+  return ofsc_graph_build_ex(comm, n, m, src, dst, edges_on_device, nullptr, stream, out);
+}
+
+ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
+                                const int64_t* dst, int edges_on_device,
+                                const ofsc_build_opts* bopts, ofsc_stream stream,
+                                ofsc_graph* out) {
   ofsc_graph g = nullptr;
   ofsc_status st = guard([&] {
     OFSC_REQUIRE(out && n >= 1 && m >= 0 && (m == 0 || (src && dst)), OFSC_ERR_ARG,
                  "bad graph arguments");
+    const int reorder = bopts ? bopts->reorder : 0;
+    const int sweeps = (bopts && bopts->lpa_sweeps > 0) ? bopts->lpa_sweeps : 8;
+    OFSC_REQUIRE(reorder == 0 || reorder == 1, OFSC_ERR_ARG, "bad reorder option");
     cudaStream_t s = (cudaStream_t)stream;
     g = new ofsc_graph_s();
     g->comm = comm;
@@ -213,6 +228,16 @@ ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t
     g->rank = comm ? comm->rank : 0;
     g->n = n;
     CsrDevice csr;
+    int64_t n_comm = 0;
+    double intra = 0.0;
+    auto free_csr = [&] {
+      dfree(csr.row_ptr);
+      dfree(csr.col);
+      dfree(csr.s);
+      csr.row_ptr = nullptr;
+      csr.col = nullptr;
+      csr.s = nullptr;
+    };
     {
       const size_t eb = (!edges_on_device && m > 0) ? m * sizeof(int64_t) : 0;
       DBuf ds(eb, s), dd(eb, s);
@@ -226,10 +251,19 @@ ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t
       }
       try {
         build_csr(n, m, psrc, pdst, csr, s);
+        if (reorder) {
+          // locality reordering derived from the graph: communities -> contiguous rows
+          OFSC_CUDA(cudaMalloc(&g->perm, n * sizeof(int32_t)));
+          DBuf inv(n * sizeof(int32_t), s);
+          lpa_order(csr, sweeps, g->perm, inv.as<int32_t>(), &n_comm, &intra, s);
+          DBuf s2(m * sizeof(int64_t), s), d2(m * sizeof(int64_t), s);
+          relabel_edges(m, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
+          free_csr();
+          build_csr(n, m, s2.as<int64_t>(), d2.as<int64_t>(), csr, s);
+          g->reordered = true;
+        }
       } catch (...) {
-        dfree(csr.row_ptr);
-        dfree(csr.col);
-        dfree(csr.s);
+        free_csr();
         throw;
       }
     }
@@ -302,6 +336,9 @@ ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t
     in.max_degree = csr.max_deg;
     in.fro2_A = csr.fro2;
     in.load_imbalance = (double)p * (double)max_nnz / total;
+    in.reordered = g->reordered ? 1 : 0;
+    in.n_communities = n_comm;
+    in.intra_edge_fraction = intra;
     *out = g;
   });
   if (st != OFSC_OK && g) {
@@ -345,6 +382,16 @@ ofsc_status ofsc_graph_copy_csr(ofsc_graph g, int64_t* h_row_ptr, int32_t* h_col
   });
 }
 
+ofsc_status ofsc_graph_copy_perm(ofsc_graph g, int32_t* h_perm) {
+  return guard([&] {
+    OFSC_REQUIRE(g && h_perm, OFSC_ERR_ARG, "null argument");
+    if (g->reordered)
+      OFSC_CUDA(cudaMemcpy(h_perm, g->perm, g->n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    else
+      for (int64_t i = 0; i < g->n; ++i) h_perm[i] = (int32_t)i;
+  });
+}
+
 ofsc_status ofsc_graph_destroy(ofsc_graph g) {
   return guard([&] {
     if (!g) return;
@@ -361,8 +408,10 @@ ofsc_status ofsc_graph_destroy(ofsc_graph g) {
 // ---------------------------------------------------------------------------
 namespace ofsc {
 
+// internal global row g (owned by rank r) <- user row perm[g] (original node order)
 __global__ void k_to_slots(int k, int KP, int64_t n, const void* src, int64_t lds, void* dst,
-                           const int64_t* begins, int p, int64_t slot_rows, int f64) {
+                           const int64_t* begins, int p, int64_t slot_rows, int f64,
+                           const int32_t* perm) {
   const int64_t total = n * KP;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -371,8 +420,9 @@ __global__ void k_to_slots(int k, int KP, int64_t n, const void* src, int64_t ld
     int r = 0;
     while (r + 1 < p && begins[r + 1] <= g) ++r;
     const int64_t id = r * slot_rows + (g - begins[r]);
-    if (f64) ((double*)dst)[id * KP + c] = c < k ? ((const double*)src)[g * lds + c] : 0.0;
-    else ((float*)dst)[id * KP + c] = c < k ? ((const float*)src)[g * lds + c] : 0.0f;
+    const int64_t u = perm ? (int64_t)perm[g] : g;
+    if (f64) ((double*)dst)[id * KP + c] = c < k ? ((const double*)src)[u * lds + c] : 0.0;
+    else ((float*)dst)[id * KP + c] = c < k ? ((const float*)src)[u * lds + c] : 0.0f;
   }
 }
 
@@ -380,7 +430,8 @@ static void to_slots(ofsc_graph g, ofsc_dtype dt, int k, int KP, const void* src
                      void* dst, cudaStream_t s) {
   OFSC_CUDA(cudaMemsetAsync(dst, 0, (size_t)g->p * g->slot_rows * KP * esize(dt), s));
   k_to_slots<<<num_sms() * 8, 256, 0, s>>>(k, KP, g->n, src, lds, dst, g->d_begins, g->p,
-                                          g->slot_rows, dt == OFSC_F64);
+                                          g->slot_rows, dt == OFSC_F64,
+                                          g->reordered ? g->perm : nullptr);
   OFSC_LAUNCH_CHECK();
 }
 
@@ -410,14 +461,16 @@ ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void*
     OFSC_REQUIRE(g && d_Z && d_Y && k >= 1 && ldz >= k && ldy >= k, OFSC_ERR_ARG, "bad apply args");
     OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
     cudaStream_t s = (cudaStream_t)stream;
-    if (g->p == 1) {
+    if (g->p == 1 && !g->reordered) {
       launch_spmm_plain(dt, k, g->n_local, 0, g->row_ptr, g->col, g->s_slot, g->s32_slot, d_Z, ldz,
                         d_Y, ldy, s);
     } else {
       DBuf zs((size_t)g->p * g->slot_rows * k * esize(dt), s);
+      DBuf ys(g->user_perm() ? (size_t)std::max<int64_t>(g->n_local, 1) * k * esize(dt) : 0, s);
       to_slots(g, dt, k, k, d_Z, ldz, zs.p, s);
       launch_spmm_plain(dt, k, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
-                        zs.p, k, d_Y, ldy, s);
+                        zs.p, k, g->user_perm() ? ys.p : d_Y, g->user_perm() ? k : ldy, s);
+      if (g->user_perm()) launch_copy_out(dt, k, k, g->n_local, ys.p, d_Y, ldy, g->user_perm(), s);
     }
   });
 }
@@ -437,7 +490,7 @@ ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const 
     DBuf zs((size_t)g->p * g->slot_rows * KP * es, s), xs(std::max<int64_t>(nl, 1) * KP * es, s),
         ys(std::max<int64_t>(nl, 1) * KP * es, s);
     to_slots(g, dt, k, KP, d_Z, ldz, zs.p, s);
-    launch_copy_in(dt, k, KP, nl, d_X, ldx, xs.p, s);
+    launch_copy_in(dt, k, KP, nl, d_X, ldx, xs.p, g->user_perm(), s);
     const int nb = grid_rows(std::max<int64_t>(nl, 1), 2);
     DBuf p4((size_t)nb * 2 * KP * KP * 8, s), p2((size_t)nb * 2 * KP * KP * 8, s),
         gr((size_t)4 * KP * KP * 8, s);
@@ -448,7 +501,7 @@ ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const 
     launch_reduce_partials(p4.as<double>(), nb, 2 * KP * KP, gr.as<double>(), s);
     launch_reduce_partials(p2.as<double>(), nb, 2 * KP * KP, gr.as<double>() + 2 * KP * KP, s);
     allreduce_d(g, gr.as<double>(), 4 * KP * KP, s);
-    launch_copy_out(dt, k, KP, nl, ys.p, d_Y, ldy, s);
+    launch_copy_out(dt, k, KP, nl, ys.p, d_Y, ldy, g->user_perm(), s);
     for (int q = 0; q < 4; ++q)
       k_extract_kk<<<(k * k + 255) / 256, 256, 0, s>>>(gr.as<double>() + q * KP * KP, KP, k,
                                                        d_grams + q * k * k);
@@ -696,7 +749,7 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
     OFSC_CUDA(cudaMemsetAsync(p.hist, 0xff, (size_t)std::max(T, 1) * 4 * 8, s));  // NaN
     const size_t blk = (size_t)std::max<int64_t>(g->n_local, 1) * KP * es;
     const size_t vg = g->p == 1 ? blk : (size_t)g->p * g->slot_rows * KP * es;
-    launch_copy_in(dt, o.k, KP, g->n_local, d_X, ldx, w.X, s);
+    launch_copy_in(dt, o.k, KP, g->n_local, d_X, ldx, w.X, g->user_perm(), s);
     OFSC_CUDA(cudaMemsetAsync(w.G, 0, blk, s));
     OFSC_CUDA(cudaMemsetAsync(w.AV, 0, blk, s));
     OFSC_CUDA(cudaMemsetAsync(w.Vg, 0, vg, s));
@@ -782,7 +835,7 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
     }
     (void)t_last;
     launch_update_x(dt, p, s);  // pending step of the last iteration (no-op after a stop)
-    launch_copy_out(dt, o.k, KP, g->n_local, w.X, d_X, ldx, s);
+    launch_copy_out(dt, o.k, KP, g->n_local, w.X, d_X, ldx, g->user_perm(), s);
     DevCtl c;
     OFSC_CUDA(cudaMemcpyAsync(&c, w.ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, s));
     std::vector<double> hh((size_t)std::max(T, 1) * 4);
@@ -995,57 +1048,116 @@ ofsc_status ofsc_scores(int64_t n, const int32_t* a, const int32_t* b, double* a
 }  // extern "C"
 
 namespace ofsc {
-// C[c] = Y[init_rows[c] - row_begin] for rows owned by this rank, 0 otherwise
-__global__ void k_gather_rows(int K, int dim, const int64_t* rows, int64_t row_begin, int64_t n_local,
-                              const void* Y, int64_t ldy, int f64, double* C) {
+// C[c] = Y[local row of node init_rows[c]] if this rank owns it, else 0 (summed over ranks)
+__global__ void k_gather_rows(int K, int dim, const int64_t* rows, const int32_t* inv,
+                              int64_t row_begin, int64_t n_local, const void* Y, int64_t ldy,
+                              int f64, double* C) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= K * dim) return;
   const int c = e / dim, d = e % dim;
-  const int64_t r = rows[c] - row_begin;
+  const int64_t node = rows[c];
+  const int64_t r = (inv ? (int64_t)inv[node] : node) - row_begin;
   double v = 0.0;
   if (r >= 0 && r < n_local)
     v = f64 ? ((const double*)Y)[r * ldy + d] : (double)((const float*)Y)[r * ldy + d];
   C[e] = v;
+}
+__global__ void k_invert_perm(int64_t n, const int32_t* perm, int32_t* inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[i]] = (int32_t)i;
+}
+// local internal rows <-> rows of a full original-order array
+__global__ void k_scatter_labels(int64_t n_local, int64_t row_begin, const int32_t* perm,
+                                 const int32_t* lab, int32_t* full) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_local;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = row_begin + i;
+    full[perm ? perm[g] : g] = lab[i];
+  }
 }
 }  // namespace ofsc
 
 extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t m,
                                              const int64_t* h_src, const int64_t* h_dst,
                                              ofsc_method method, ofsc_dtype dt,
-                                             const ofsc_opts* opts, void* h_X, int32_t n_clusters,
+                                             const ofsc_opts* opts, const ofsc_build_opts* bopts,
+                                             void* h_X, int32_t n_clusters,
                                              const int64_t* h_init_rows, int32_t km_max_iters,
                                              int32_t* h_labels, ofsc_report* rep,
                                              ofsc_stream stream) {
   ofsc_graph g = nullptr;
   ofsc_status run_st = OFSC_OK;
   ofsc_status st = guard([&] {
-    OFSC_REQUIRE(opts && h_X && h_init_rows && h_labels && n_clusters >= 1, OFSC_ERR_ARG,
-                 "bad spectral_cluster args");
+    OFSC_REQUIRE(opts && h_X && h_init_rows && h_labels && n_clusters >= 1 && opts->k >= 1,
+                 OFSC_ERR_ARG, "bad spectral_cluster args");
     cudaStream_t s = (cudaStream_t)stream;
-    ofsc_status b = ofsc_graph_build(comm, n, m, h_src, h_dst, 0, stream, &g);
+    ofsc_build_opts bo{1, 8};
+    if (bopts) bo = *bopts;
+    ofsc_status b = ofsc_graph_build_ex(comm, n, m, h_src, h_dst, 0, &bo, stream, &g);
     if (b != OFSC_OK) throw Error{b, g_last_error};
     const int k = opts->k;
     const int64_t nl = g->n_local;
     const size_t es = esize(dt);
-    DBuf dX(std::max<int64_t>(nl, 1) * k * es, s), dY(std::max<int64_t>(nl, 1) * k * es, s),
-        dC((size_t)n_clusters * k * 8, s), dL(std::max<int64_t>(nl, 1) * 4, s),
-        dR((size_t)n_clusters * 8, s);
-    OFSC_CUDA(cudaMemcpyAsync(dX.p, h_X, nl * k * es, cudaMemcpyHostToDevice, s));
-    run_st = ofsc_run(g, method, dt, opts, dX.p, k, nullptr, rep, stream);
+    const int32_t* perm = g->reordered ? g->perm : nullptr;
+    DBuf dXf((size_t)n * k * es, s), dX(g->p > 1 ? (size_t)std::max<int64_t>(nl, 1) * k * es : 0, s),
+        dY(std::max<int64_t>(nl, 1) * k * es, s), dC((size_t)n_clusters * k * 8, s),
+        dL(std::max<int64_t>(nl, 1) * 4, s), dLf((size_t)n * 4, s), dR((size_t)n_clusters * 8, s),
+        dInv(perm ? (size_t)n * 4 : 0, s);
+    // all n rows of X0 (original order) -> this rank's internal rows
+    OFSC_CUDA(cudaMemcpyAsync(dXf.p, h_X, (size_t)n * k * es, cudaMemcpyHostToDevice, s));
+    // p == 1: ofsc_run maps original-order rows through perm itself, run on the full
+    // array; p > 1: gather this rank's internal rows first
+    void* Xrun = dXf.p;
+    if (g->p > 1) {
+      launch_copy_in(dt, k, k, nl,
+                     (const char*)dXf.p + (perm ? 0 : (size_t)g->row_begin * k * es), k, dX.p,
+                     perm ? perm + g->row_begin : nullptr, s);
+      Xrun = dX.p;
+    }
+    run_st = ofsc_run(g, method, dt, opts, Xrun, k, nullptr, rep, stream);
     if (run_st != OFSC_OK && run_st != OFSC_ERR_DIVERGED) throw Error{run_st, g_last_error};
-    OFSC_CUDA(cudaMemcpyAsync(h_X, dX.p, nl * k * es, cudaMemcpyDeviceToHost, s));
-    ofsc_status r = ofsc_row_normalize(dt, nl, k, dX.p, k, dY.p, k, stream);
+    // features back to the caller's full array (rows this rank owns)
+    if (g->p == 1) {
+      OFSC_CUDA(cudaMemcpyAsync(h_X, dXf.p, (size_t)n * k * es, cudaMemcpyDeviceToHost, s));
+    } else {
+      launch_copy_out(dt, k, k, nl, dX.p,
+                      (char*)dXf.p + (perm ? 0 : (size_t)g->row_begin * k * es), k,
+                      perm ? perm + g->row_begin : nullptr, s);
+      OFSC_CUDA(cudaMemcpyAsync(h_X, dXf.p, (size_t)n * k * es, cudaMemcpyDeviceToHost, s));
+    }
+    ofsc_status r = ofsc_row_normalize(dt, nl, k, Xrun, k, dY.p, k, stream);
     if (r != OFSC_OK) throw Error{r, g_last_error};
     OFSC_CUDA(cudaMemcpyAsync(dR.p, h_init_rows, (size_t)n_clusters * 8, cudaMemcpyHostToDevice, s));
+    // K-means rows: p == 1 holds original order (no inverse needed); p > 1 internal order
+    const int32_t* inv = nullptr;
+    if (perm && g->p > 1) {
+      k_invert_perm<<<num_sms() * 8, 256, 0, s>>>(n, perm, dInv.as<int32_t>());
+      OFSC_LAUNCH_CHECK();
+      inv = dInv.as<int32_t>();
+    }
     k_gather_rows<<<(n_clusters * k + 255) / 256, 256, 0, s>>>(
-        n_clusters, k, dR.as<int64_t>(), g->row_begin, nl, dY.p, k, dt == OFSC_F64, dC.as<double>());
+        n_clusters, k, dR.as<int64_t>(), inv, g->p == 1 ? 0 : g->row_begin, nl, dY.p, k,
+        dt == OFSC_F64, dC.as<double>());
     OFSC_LAUNCH_CHECK();
     if (comm && comm->nranks > 1)
       OFSC_NCCL(ncclAllReduce(dC.p, dC.p, (size_t)n_clusters * k, ncclFloat64, ncclSum, comm->nccl, s));
     r = ofsc_kmeans(comm, dt, nl, k, dY.p, k, n_clusters, dC.as<double>(), km_max_iters,
                     dL.as<int32_t>(), nullptr, nullptr, stream);
     if (r != OFSC_OK) throw Error{r, g_last_error};
-    OFSC_CUDA(cudaMemcpyAsync(h_labels, dL.p, nl * 4, cudaMemcpyDeviceToHost, s));
+    if (g->p == 1) {
+      OFSC_CUDA(cudaMemcpyAsync(h_labels, dL.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    } else {
+      OFSC_CUDA(cudaMemsetAsync(dLf.p, 0xff, (size_t)n * 4, s));
+      k_scatter_labels<<<num_sms() * 8, 256, 0, s>>>(nl, g->row_begin, perm, dL.as<int32_t>(),
+                                                    dLf.as<int32_t>());
+      OFSC_LAUNCH_CHECK();
+      std::vector<int32_t> tmp(n);
+      OFSC_CUDA(cudaMemcpyAsync(tmp.data(), dLf.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+      OFSC_CUDA(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < n; ++i)
+        if (tmp[i] >= 0) h_labels[i] = tmp[i];
+    }
     OFSC_CUDA(cudaStreamSynchronize(s));
   });
   if (g) ofsc_graph_destroy(g);

@@ -8,6 +8,8 @@
 // cub (CUDA toolkit) supplies the radix sort / unique / scan building blocks.
 #include <cub/cub.cuh>
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace ofsc {
@@ -271,6 +273,184 @@ __global__ void k_rebase(const int64_t* in, int64_t rows, int64_t base, int64_t*
 
 void rebase_row_ptr(const int64_t* in, int64_t rows, int64_t base, int64_t* out, cudaStream_t st) {
   k_rebase<<<blocks_for(rows + 1), 256, 0, st>>>(in, rows, base, out);
+  OFSC_LAUNCH_CHECK();
+}
+
+// ---- locality reordering: label propagation (graph-derived communities) ----
+// Semi-synchronous LPA: each sweep updates the nodes of one hash colour, then
+// the other, from a double-buffered label array (a pure function of the input
+// labels: deterministic).  A node takes the most frequent label among its first
+// kLpaCap neighbours; ties go to the smallest hash(label, sweep); it keeps its
+// own label if that ties the maximum.  Nodes are then ordered by (label, id) so
+// that communities occupy contiguous row ranges and the SpMM's neighbour
+// gathers stay in L2.
+constexpr int kLpaCap = 128;
+constexpr int kLpaSlots = 256;
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x, uint32_t seed) {
+  uint64_t z = (uint64_t)x * 0x9E3779B97F4A7C15ull + (uint64_t)seed * 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 31;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 29;
+  return (uint32_t)z;
+}
+
+__global__ void __launch_bounds__(256) k_lpa_pass(int64_t n, const int64_t* __restrict__ row_ptr,
+                                                  const int32_t* __restrict__ col,
+                                                  const int* __restrict__ lin, int* __restrict__ lout,
+                                                  int colour, uint32_t seed) {
+  __shared__ int keys[8][kLpaSlots];
+  __shared__ int cnts[8][kLpaSlots];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int* K = keys[w];
+  int* Cn = cnts[w];
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + w; i < n; i += nw) {
+    const int own = lin[i];
+    if ((int)(mix32((uint32_t)i, 0x5EEDu) & 1u) != colour) {
+      if (lane == 0) lout[i] = own;
+      continue;
+    }
+    const int64_t beg = row_ptr[i];
+    const int64_t deg = min((int64_t)kLpaCap, row_ptr[i + 1] - beg);
+    if (deg == 0) {
+      if (lane == 0) lout[i] = own;
+      continue;
+    }
+    for (int q = lane; q < kLpaSlots; q += 32) {
+      K[q] = -1;
+      Cn[q] = 0;
+    }
+    __syncwarp();
+    for (int64_t e = lane; e < deg; e += 32) {
+      const int L = lin[col[beg + e]];
+      int slot = (int)(mix32((uint32_t)L, 7u) & (kLpaSlots - 1));
+      while (true) {
+        const int prev = atomicCAS(&K[slot], -1, L);
+        if (prev == -1 || prev == L) {
+          atomicAdd(&Cn[slot], 1);
+          break;
+        }
+        slot = (slot + 1) & (kLpaSlots - 1);
+      }
+    }
+    __syncwarp();
+    int bc = 0, bl = -1, owncnt = 0;
+    uint32_t bh = 0xffffffffu;
+    for (int q = lane; q < kLpaSlots; q += 32) {
+      const int L = K[q];
+      if (L < 0) continue;
+      const int c = Cn[q];
+      if (L == own) owncnt = c;
+      const uint32_t h = mix32((uint32_t)L, seed);
+      if (c > bc || (c == bc && (h < bh || (h == bh && L < bl)))) {
+        bc = c;
+        bl = L;
+        bh = h;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      const uint32_t oh = __shfl_xor_sync(0xffffffffu, bh, o);
+      if (oc > bc || (oc == bc && (oh < bh || (oh == bh && ol < bl)))) {
+        bc = oc;
+        bl = ol;
+        bh = oh;
+      }
+      owncnt = max(owncnt, __shfl_xor_sync(0xffffffffu, owncnt, o));
+    }
+    if (lane == 0) lout[i] = (owncnt >= bc) ? own : bl;
+    __syncwarp();
+  }
+}
+
+__global__ void k_lpa_keys(int64_t n, const int* lab, unsigned long long* keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = ((unsigned long long)(unsigned)lab[i] << 32) | (unsigned long long)i;
+}
+
+__global__ void k_perm_from_keys(int64_t n, const unsigned long long* keys, int32_t* perm,
+                                 int32_t* inv, const int* lab, int* newcomm) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t node = (int32_t)(keys[j] & 0xffffffffull);
+    perm[j] = node;
+    inv[node] = (int32_t)j;
+    if (j == 0 || (keys[j] >> 32) != (keys[j - 1] >> 32)) atomicAdd(newcomm, 1);
+  }
+}
+
+__global__ void k_intra_edges(int64_t n, const int64_t* row_ptr, const int32_t* col, const int* lab,
+                              unsigned long long* cnt) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; ++q) c += lab[col[q]] == lab[i];
+  if (c) atomicAdd(cnt, c);
+}
+
+__global__ void k_relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
+                                int64_t* s2, int64_t* d2) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    s2[e] = inv[src[e]];
+    d2[e] = inv[dst[e]];
+  }
+}
+
+__global__ void k_iota(int64_t n, int* lab) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lab[i] = (int)i;
+}
+
+void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv, int64_t* n_comm,
+               double* intra_frac, cudaStream_t st) {
+  const int64_t n = csr.n;
+  DevBuf<int> la(n, st), lb(n, st), cnt(1, st);
+  DevBuf<unsigned long long> keys(n, st), sorted(n, st), ic(1, st);
+  k_iota<<<blocks_for(n), 256, 0, st>>>(n, la.p);
+  OFSC_LAUNCH_CHECK();
+  int* cur = la.p;
+  int* nxt = lb.p;
+  const int nb = num_sms() * 8;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int colour = 0; colour < 2; ++colour) {
+      k_lpa_pass<<<nb, 256, 0, st>>>(n, csr.row_ptr, csr.col, cur, nxt, colour,
+                                     (uint32_t)(2 * sw + colour + 1));
+      OFSC_LAUNCH_CHECK();
+      std::swap(cur, nxt);
+    }
+  k_lpa_keys<<<blocks_for(n), 256, 0, st>>>(n, cur, keys.p);
+  OFSC_LAUNCH_CHECK();
+  size_t tmp_bytes = 0;
+  OFSC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, sorted.p, n, 0, 64, st));
+  {
+    DevBuf<char> tmp(tmp_bytes, st);
+    OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, n, 0, 64, st));
+  }
+  OFSC_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
+  OFSC_CUDA(cudaMemsetAsync(ic.p, 0, sizeof(unsigned long long), st));
+  k_perm_from_keys<<<blocks_for(n), 256, 0, st>>>(n, sorted.p, d_perm, d_inv, cur, cnt.p);
+  OFSC_LAUNCH_CHECK();
+  k_intra_edges<<<blocks_for(n), 256, 0, st>>>(n, csr.row_ptr, csr.col, cur, ic.p);
+  OFSC_LAUNCH_CHECK();
+  int h_cnt = 0;
+  unsigned long long h_ic = 0;
+  OFSC_CUDA(cudaMemcpyAsync(&h_cnt, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaMemcpyAsync(&h_ic, ic.p, sizeof(h_ic), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaStreamSynchronize(st));
+  *n_comm = h_cnt;
+  *intra_frac = csr.nnz > 0 ? (double)h_ic / (double)csr.nnz : 1.0;
+}
+
+void relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
+                   int64_t* s2, int64_t* d2, cudaStream_t st) {
+  if (m <= 0) return;
+  k_relabel_edges<<<blocks_for(m), 256, 0, st>>>(m, src, dst, inv, s2, d2);
   OFSC_LAUNCH_CHECK();
 }
 

@@ -127,10 +127,12 @@ void launch_linesearch(const IterParams& p, cudaStream_t st);
 void launch_linesearch_hook(int method, int k, int KP, const double* grams, double* M, double* W,
                             double* alpha, int* codes, cudaStream_t st);
 // layout helpers
+// dst row r <- src row perm[r] (perm may be NULL: identity)
 void launch_copy_in(ofsc_dtype dt, int k, int KP, int64_t n, const void* src, int64_t lds,
-                    void* dst, cudaStream_t st);
+                    void* dst, const int32_t* perm, cudaStream_t st);
+// dst row perm[r] <- src row r (perm may be NULL: identity)
 void launch_copy_out(ofsc_dtype dt, int k, int KP, int64_t n, const void* src, void* dst,
-                     int64_t ldd, cudaStream_t st);
+                     int64_t ldd, const int32_t* perm, cudaStream_t st);
 void launch_row_normalize(ofsc_dtype dt, int64_t n, int k, const void* X, int64_t ldx, void* Y,
                           int64_t ldy, cudaStream_t st);
 // K-means
@@ -152,6 +154,11 @@ struct CsrDevice {
 };
 void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst, CsrDevice& out,
                cudaStream_t st);
+// locality reordering (label propagation): perm[new] = old, inv[old] = new
+void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv, int64_t* n_comm,
+               double* intra_frac, cudaStream_t st);
+void relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
+                   int64_t* s2, int64_t* d2, cudaStream_t st);
 void remap_columns(const int32_t* col_in, int64_t nnz, int32_t* col_out, const int64_t* d_begins,
                    int p, int64_t slot_rows, cudaStream_t st);
 void scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,

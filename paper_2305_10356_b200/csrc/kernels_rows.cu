@@ -126,38 +126,44 @@ void launch_reduce_partials(const double* part, int nblk, int per_blk, double* o
 // Layout copies (user ld <-> padded KP), row normalisation.
 // ----------------------------------------------------------------------------
 template <typename T>
-__global__ void k_copy_in(int k, int KP, int64_t n, const T* src, int64_t lds, T* dst) {
+__global__ void k_copy_in(int k, int KP, int64_t n, const T* src, int64_t lds, T* dst,
+                          const int32_t* perm) {
   const int64_t total = n * KP;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / KP;
     const int c = (int)(e % KP);
-    dst[e] = c < k ? src[r * lds + c] : (T)0;
+    const int64_t u = perm ? (int64_t)perm[r] : r;
+    dst[e] = c < k ? src[u * lds + c] : (T)0;
   }
 }
 template <typename T>
-__global__ void k_copy_out(int k, int KP, int64_t n, const T* src, T* dst, int64_t ldd) {
+__global__ void k_copy_out(int k, int KP, int64_t n, const T* src, T* dst, int64_t ldd,
+                           const int32_t* perm) {
   const int64_t total = n * k;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / k;
     const int c = (int)(e % k);
-    dst[r * ldd + c] = src[r * KP + c];
+    const int64_t u = perm ? (int64_t)perm[r] : r;
+    dst[u * ldd + c] = src[r * KP + c];
   }
 }
 
 void launch_copy_in(ofsc_dtype dt, int k, int KP, int64_t n, const void* src, int64_t lds,
-                    void* dst, cudaStream_t st) {
+                    void* dst, const int32_t* perm, cudaStream_t st) {
   const int nb = num_sms() * 8;
-  if (dt == OFSC_F64) k_copy_in<double><<<nb, 256, 0, st>>>(k, KP, n, (const double*)src, lds, (double*)dst);
-  else k_copy_in<float><<<nb, 256, 0, st>>>(k, KP, n, (const float*)src, lds, (float*)dst);
+  if (dt == OFSC_F64)
+    k_copy_in<double><<<nb, 256, 0, st>>>(k, KP, n, (const double*)src, lds, (double*)dst, perm);
+  else k_copy_in<float><<<nb, 256, 0, st>>>(k, KP, n, (const float*)src, lds, (float*)dst, perm);
   OFSC_LAUNCH_CHECK();
 }
 void launch_copy_out(ofsc_dtype dt, int k, int KP, int64_t n, const void* src, void* dst,
-                     int64_t ldd, cudaStream_t st) {
+                     int64_t ldd, const int32_t* perm, cudaStream_t st) {
   const int nb = num_sms() * 8;
-  if (dt == OFSC_F64) k_copy_out<double><<<nb, 256, 0, st>>>(k, KP, n, (const double*)src, (double*)dst, ldd);
-  else k_copy_out<float><<<nb, 256, 0, st>>>(k, KP, n, (const float*)src, (float*)dst, ldd);
+  if (dt == OFSC_F64)
+    k_copy_out<double><<<nb, 256, 0, st>>>(k, KP, n, (const double*)src, (double*)dst, ldd, perm);
+  else k_copy_out<float><<<nb, 256, 0, st>>>(k, KP, n, (const float*)src, (float*)dst, ldd, perm);
   OFSC_LAUNCH_CHECK();
 }
 

@@ -96,3 +96,16 @@ def test_algorithm1_end_to_end_c1(method):
     a_gpu, a_or = ari(labels, lab), ari(lo, lab)
     assert rep["iters"] == cfg.iters
     assert a_gpu >= 0.8 and abs(a_gpu - a_or) <= 0.02
+
+
+def test_algorithm1_reorder_equivalent():
+    cfg = CONFIGS["c2"]
+    s, d, lab = config_graph(cfg)
+    X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
+    rows = kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)
+    l1, f1, _ = ofsc.spectral_cluster(cfg.n, s, d, "ofm_f2", X0, cfg.blocks, rows, max_iters=60,
+                                      reorder=True)
+    l0, f0, _ = ofsc.spectral_cluster(cfg.n, s, d, "ofm_f2", X0, cfg.blocks, rows, max_iters=60,
+                                      reorder=False)
+    assert np.linalg.norm(f1 - f0) / np.linalg.norm(f0) <= 1e-9
+    assert ari(l1, l0) >= 0.999

@@ -196,3 +196,15 @@ def test_full_size_c4_sampled_rows():
     assert np.max(np.abs(Gh[0] - Gh[0].T)) <= 1e-14 * np.max(np.abs(Gh[0]))
     # tr(Z^T Y) = sum_i <Z_i, Y_i> (any size): check against a fp64 torch reduction
     assert abs(np.trace(Gh[2]) - float((Z * Y).sum())) <= 1e-10 * abs(np.trace(Gh[2]))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("method", METHODS)
+def test_p2_reordered_graph(name, method):
+    """The locality-reordered operator P A P^T gives the same iterates (rows mapped
+    back to the original order by the library) within the north-star tolerance."""
+    cfg, op, g, X0, _ = setup(name)
+    gr = ofsc.Graph(cfg.n, *config_graph(cfg)[:2], reorder=True)
+    o = run_ofm(op, method, X0, 10, refresh=0)
+    X, r = gpu_run(gr, method, X0, 10)
+    assert rel(X, o.X) <= 1e-10

@@ -143,3 +143,36 @@ def test_line_search_textbook_cubics_on_device():
     assert alpha[0] == -1.0 and codes[0] in (8, 9, 10)
     alpha, codes, _, _ = ofsc.line_search("ofm_f1", zero, zero, zero, zero, zero, zero)
     assert alpha[0] == 0.0 and codes[0] == 0
+
+
+@pytest.mark.parametrize("name", ["c2", "ragged"])
+def test_reordered_graph_is_a_permutation_of_the_operator(name):
+    """LPA locality reordering: internal CSR = P S P^T, perm is a permutation,
+    communities capture most edges, and the hooks take/return original order."""
+    s, d, n = GRAPHS[name]()
+    op = build_operator(n, s, d)
+    g = ofsc.Graph(n, s, d, reorder=True)
+    info = g.info
+    perm = g.copy_perm()
+    assert info["reordered"] == 1 and np.array_equal(np.sort(perm), np.arange(n))
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    rp, col, sv = g.copy_csr()
+    assert np.array_equal(sv, op.s[perm])
+    for i in np.random.default_rng(0).choice(n, 50, replace=False):
+        got = np.sort(perm[col[rp[i]:rp[i + 1]]])
+        want = op.col[op.row_ptr[perm[i]]:op.row_ptr[perm[i] + 1]]
+        assert np.array_equal(got, want)
+    if name == "c2":
+        assert info["intra_edge_fraction"] > 0.5 and info["n_communities"] < n // 10
+    k = 32
+    Z = np.random.default_rng(5).standard_normal((n, k)) / np.sqrt(n)
+    X = np.random.default_rng(6).standard_normal((n, k)) / np.sqrt(n)
+    Y = g.apply(torch.from_numpy(Z).cuda()).cpu().numpy()
+    Yo = apply_A(op, Z)
+    assert np.max(np.abs(Y - Yo)) <= 4e-14 * np.max(np.abs(Yo))
+    Y2, Gm = g.apply_gram(torch.from_numpy(Z).cuda(), torch.from_numpy(X).cuda())
+    Q, P, T, Rp = grams(Z, X, Yo)
+    assert np.max(np.abs(Y2.cpu().numpy() - Yo)) <= 4e-14 * np.max(np.abs(Yo))
+    for got, want in zip(Gm.cpu().numpy(), (Q, P, T, Rp)):
+        assert rel(got, want) <= 1e-13
