@@ -123,7 +123,7 @@ typedef struct {
  * [row_begin, row_end), i.e. nodes perm[row_begin .. row_end). */
 typedef struct {
   int32_t reorder;     /* 0 = keep node ids (default of ofsc_graph_build), 1 = LPA reorder */
-  int32_t lpa_sweeps;  /* default 8 */
+  int32_t lpa_sweeps;  /* max sweeps (<= 0: 30); stops early when < n/1000 labels change */
 } ofsc_build_opts;
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,

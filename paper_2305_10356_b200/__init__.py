@@ -209,7 +209,7 @@ class Graph:
     """Shifted normalised Laplacian A = L - 2I of an undirected graph."""
 
     def __init__(self, n, src, dst, comm: Comm | None = None, stream=None, reorder=False,
-                 lpa_sweeps=8):
+                 lpa_sweeps=30):
         torch = _torch()
         self.n = int(n)
         self.comm = comm
@@ -413,7 +413,7 @@ def spectral_cluster(n, src, dst, method, X0, n_clusters, init_rows, *, max_iter
     rows = np.ascontiguousarray(np.asarray(init_rows, dtype=np.int64))
     labels = np.full(X.shape[0], -1, np.int32)
     o = make_opts(X.shape[1], max_iters, **run_opts)
-    bo = BuildOpts(1 if reorder else 0, 8)
+    bo = BuildOpts(1 if reorder else 0, 30)
     rep = Report()
     _check(lib().ofsc_spectral_cluster(comm.handle if comm else None, int(n), src.size,
                                        src.ctypes.data_as(C.c_void_p),

@@ -219,7 +219,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     OFSC_REQUIRE(out && n >= 1 && m >= 0 && (m == 0 || (src && dst)), OFSC_ERR_ARG,
                  "bad graph arguments");
     const int reorder = bopts ? bopts->reorder : 0;
-    const int sweeps = (bopts && bopts->lpa_sweeps > 0) ? bopts->lpa_sweeps : 8;
+    const int sweeps = (bopts && bopts->lpa_sweeps > 0) ? bopts->lpa_sweeps : 30;
     OFSC_REQUIRE(reorder == 0 || reorder == 1, OFSC_ERR_ARG, "bad reorder option");
     cudaStream_t s = (cudaStream_t)stream;
     g = new ofsc_graph_s();
@@ -1092,7 +1092,7 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     OFSC_REQUIRE(opts && h_X && h_init_rows && h_labels && n_clusters >= 1 && opts->k >= 1,
                  OFSC_ERR_ARG, "bad spectral_cluster args");
     cudaStream_t s = (cudaStream_t)stream;
-    ofsc_build_opts bo{1, 8};
+    ofsc_build_opts bo{1, 30};
     if (bopts) bo = *bopts;
     ofsc_status b = ofsc_graph_build_ex(comm, n, m, h_src, h_dst, 0, &bo, stream, &g);
     if (b != OFSC_OK) throw Error{b, g_last_error};

@@ -298,12 +298,14 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x, uint32_t seed) {
 __global__ void __launch_bounds__(256) k_lpa_pass(int64_t n, const int64_t* __restrict__ row_ptr,
                                                   const int32_t* __restrict__ col,
                                                   const int* __restrict__ lin, int* __restrict__ lout,
-                                                  int colour, uint32_t seed) {
+                                                  int colour, uint32_t seed,
+                                                  unsigned long long* changes) {
   __shared__ int keys[8][kLpaSlots];
   __shared__ int cnts[8][kLpaSlots];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int* K = keys[w];
   int* Cn = cnts[w];
+  unsigned long long nchg = 0;
   const int64_t nw = (int64_t)gridDim.x * 8;
   for (int64_t i = (int64_t)blockIdx.x * 8 + w; i < n; i += nw) {
     const int own = lin[i];
@@ -312,32 +314,36 @@ __global__ void __launch_bounds__(256) k_lpa_pass(int64_t n, const int64_t* __re
       continue;
     }
     const int64_t beg = row_ptr[i];
-    const int64_t deg = min((int64_t)kLpaCap, row_ptr[i + 1] - beg);
+    const int deg = (int)min((int64_t)kLpaCap, row_ptr[i + 1] - beg);
     if (deg == 0) {
       if (lane == 0) lout[i] = own;
       continue;
     }
-    for (int q = lane; q < kLpaSlots; q += 32) {
+    // open-addressing table sized to the (capped) degree: >= 2 deg slots, >= 32
+    int S = 32;
+    while (S < 2 * deg) S <<= 1;
+    const int mask = S - 1;
+    for (int q = lane; q < S; q += 32) {
       K[q] = -1;
       Cn[q] = 0;
     }
     __syncwarp();
-    for (int64_t e = lane; e < deg; e += 32) {
+    for (int e = lane; e < deg; e += 32) {
       const int L = lin[col[beg + e]];
-      int slot = (int)(mix32((uint32_t)L, 7u) & (kLpaSlots - 1));
+      int slot = (int)(mix32((uint32_t)L, 7u) & (uint32_t)mask);
       while (true) {
         const int prev = atomicCAS(&K[slot], -1, L);
         if (prev == -1 || prev == L) {
           atomicAdd(&Cn[slot], 1);
           break;
         }
-        slot = (slot + 1) & (kLpaSlots - 1);
+        slot = (slot + 1) & mask;
       }
     }
     __syncwarp();
     int bc = 0, bl = -1, owncnt = 0;
     uint32_t bh = 0xffffffffu;
-    for (int q = lane; q < kLpaSlots; q += 32) {
+    for (int q = lane; q < S; q += 32) {
       const int L = K[q];
       if (L < 0) continue;
       const int c = Cn[q];
@@ -361,9 +367,14 @@ __global__ void __launch_bounds__(256) k_lpa_pass(int64_t n, const int64_t* __re
       }
       owncnt = max(owncnt, __shfl_xor_sync(0xffffffffu, owncnt, o));
     }
-    if (lane == 0) lout[i] = (owncnt >= bc) ? own : bl;
+    const int nl = (owncnt >= bc) ? own : bl;
+    if (lane == 0) {
+      lout[i] = nl;
+      nchg += nl != own;
+    }
     __syncwarp();
   }
+  if (lane == 0 && nchg) atomicAdd(changes, nchg);
 }
 
 __global__ void k_lpa_keys(int64_t n, const int* lab, unsigned long long* keys) {
@@ -417,13 +428,24 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
   int* cur = la.p;
   int* nxt = lb.p;
   const int nb = num_sms() * 8;
-  for (int sw = 0; sw < sweeps; ++sw)
+  // sweeps until fewer than n/1000 labels change (at least 6, at most `sweeps`)
+  unsigned long long* h_chg = nullptr;
+  OFSC_CUDA(cudaMallocHost(&h_chg, sizeof(unsigned long long)));
+  for (int sw = 0; sw < sweeps; ++sw) {
+    OFSC_CUDA(cudaMemsetAsync(ic.p, 0, sizeof(unsigned long long), st));
     for (int colour = 0; colour < 2; ++colour) {
       k_lpa_pass<<<nb, 256, 0, st>>>(n, csr.row_ptr, csr.col, cur, nxt, colour,
-                                     (uint32_t)(2 * sw + colour + 1));
+                                     (uint32_t)(2 * sw + colour + 1), ic.p);
       OFSC_LAUNCH_CHECK();
       std::swap(cur, nxt);
     }
+    if (sw >= 5) {
+      OFSC_CUDA(cudaMemcpyAsync(h_chg, ic.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      OFSC_CUDA(cudaStreamSynchronize(st));
+      if (*h_chg * 1000ull < (unsigned long long)n) break;
+    }
+  }
+  cudaFreeHost(h_chg);
   k_lpa_keys<<<blocks_for(n), 256, 0, st>>>(n, cur, keys.p);
   OFSC_LAUNCH_CHECK();
   size_t tmp_bytes = 0;
