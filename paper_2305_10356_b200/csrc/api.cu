@@ -492,14 +492,15 @@ ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const 
     to_slots(g, dt, k, KP, d_Z, ldz, zs.p, s);
     launch_copy_in(dt, k, KP, nl, d_X, ldx, xs.p, g->user_perm(), s);
     const int nb = grid_rows(std::max<int64_t>(nl, 1), 2);
-    DBuf p4((size_t)nb * 2 * KP * KP * 8, s), p2((size_t)nb * 2 * KP * KP * 8, s),
+    const int nb2 = gram_stream_grid(dt, KP, std::max<int64_t>(nl, 1));
+    DBuf p4((size_t)nb * 2 * KP * KP * 8, s), p2((size_t)nb2 * 2 * KP * KP * 8, s),
         gr((size_t)4 * KP * KP * 8, s);
     const char* zown = (const char*)zs.p + (size_t)g->own_off * KP * es;
     launch_gram_pair(dt, KP, nl, zown, zown, xs.p, p4.as<double>(), nb, s);
     launch_spmm_gram(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p,
-                     xs.p, ys.p, p2.as<double>(), 0, nullptr, nb, s);
+                     xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s);
     launch_reduce_partials(p4.as<double>(), nb, 2 * KP * KP, gr.as<double>(), s);
-    launch_reduce_partials(p2.as<double>(), nb, 2 * KP * KP, gr.as<double>() + 2 * KP * KP, s);
+    launch_reduce_partials(p2.as<double>(), nb2, 2 * KP * KP, gr.as<double>() + 2 * KP * KP, s);
     allreduce_d(g, gr.as<double>(), 4 * KP * KP, s);
     launch_copy_out(dt, k, KP, nl, ys.p, d_Y, ldy, g->user_perm(), s);
     for (int q = 0; q < 4; ++q)
@@ -531,7 +532,7 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   const size_t vg = g->p == 1 ? blk : (size_t)g->p * g->slot_rows * KP * es;
   OFSC_CUDA(cudaMalloc(&w.Vg, vg));
   const int nbmax = num_sms() * 4;   // grids of the streaming kernels are chosen per run
-  w.nb2 = grid_rows(nl, 2);
+  w.nb2 = gram_stream_grid(dt, KP, nl);
   OFSC_CUDA(cudaMalloc(&w.part_cols, (size_t)nbmax * 2 * KP * 8));
   OFSC_CUDA(cudaMalloc(&w.part_g4, (size_t)nbmax * 2 * KP * KP * 8));
   OFSC_CUDA(cudaMalloc(&w.part_g2, (size_t)w.nb2 * 2 * KP * KP * 8));

@@ -106,6 +106,15 @@ void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       const int64_t* row_ptr, const int32_t* col, const double* s,
                       const float* s32, const void* Zg, const void* Xown, void* Y,
                       double* part, int mode, const int* stop, int nblk, cudaStream_t st);
+// C2a: Y = A Z only (KP-padded rows)
+void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
+                 const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
+                 const int* stop, cudaStream_t st);
+// C2b: TMA-streamed Gram pair over own rows (mode 0: Z^T Y, X^T Y; mode 1: Z^T Z, Z^T Y)
+int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n);
+void launch_gram_stream(ofsc_dtype dt, int KP, int64_t n, const void* Zown, const void* Xown,
+                        const void* Y, double* part, int mode, const int* stop, int nblk,
+                        cudaStream_t st);
 // plain SpMM (no Grams) into an arbitrary ld
 void launch_spmm_plain(ofsc_dtype dt, int k, int64_t n_local, int64_t own_off,
                        const int64_t* row_ptr, const int32_t* col, const double* s,

@@ -1,4 +1,4 @@
-// C2: the fused SpMM + Gram step (eq:spmm P:440).
+// C2: the SpMM + Gram step (eq:spmm P:440).
 //
 //   Y_i = (A Z)_i = -Z_i - s_i * sum_{j in N(i)} s_j Z_j        (A = L - 2I)
 //
@@ -15,117 +15,99 @@
 
 namespace ofsc {
 
-template <typename T>
-struct Acc2 {
-  T x, y;
-};
-
-template <typename T, int KP, int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
-k_spmm_gram(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
-            const int32_t* __restrict__ col, const double* __restrict__ s,
-            const float* __restrict__ s32, const T* __restrict__ Zg, const T* __restrict__ Xown,
-            T* __restrict__ Y, double* __restrict__ part, const int* stop) {
+// C2a: Y = A Z.  A group of LPR = KP/4 lanes owns a row (each lane 4 consecutive
+// columns = two 16-byte loads per neighbour), RPW = 32/LPR rows per warp; no
+// shared memory and no barriers, so warps stream independently and the register
+// file holds only accumulators and in-flight neighbour rows (8 per row).
+template <typename T, int KP>
+__global__ void __launch_bounds__(kThreads, 3)
+k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
+       const int32_t* __restrict__ col, const double* __restrict__ s,
+       const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
+       const int* stop) {
   if (stop && *stop) return;
-  constexpr int LD = KP + 4;                      // padded: conflict-free DMMA fragments
-  extern __shared__ __align__(16) double sp_sm[];
-  double* Zs = sp_sm;
-  double* Ys = Zs + kTR * LD;
-  double* Xs = Ys + kTR * LD;                    // mode 0 only
-  constexpr int LPR = KP / 2;                    // lanes per row (2 columns per lane)
-  constexpr int RPW = (32 % LPR == 0) ? 32 / LPR : 1;  // rows per warp pass
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  using V2 = typename Vec2<T>::type;
+  constexpr int LPR = KP / 4;
+  constexpr int RPW = 32 / LPR;
+  const int lane = threadIdx.x & 31;
   const int sub = lane / LPR, l = lane % LPR;
-  const bool active = sub < RPW;
-  DmmaGram<KP> acc;
-  acc.zero();
-  const int64_t ntiles = (n_local + kTR - 1) / kTR;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t row0 = tile * kTR;
-    const int rows = (int)imin64(kTR, n_local - row0);
-    for (int r = warp * RPW + sub; r < kTR; r += (kThreads / 32) * RPW) {
-      if (!active) break;
-      double2 y = make_double2(0.0, 0.0), own = y, xo = y;
-      if (r < rows) {
-        const int64_t i = row0 + r;
-        const int64_t beg = row_ptr[i], end = row_ptr[i + 1];
-        const T* zc = Zg + 2 * l;
-        Acc2<T> a{(T)0, (T)0};
-        int64_t e = beg;
-        for (; e + 8 <= end; e += 8) {
-          int c[8];
+  if (sub >= RPW) return;                       // KP = 48: lanes 24..31 idle
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T* zc = Zg + 4 * l;
+  for (int64_t i = gw * RPW + sub; i < n_local; i += nw * RPW) {
+    const int64_t beg = row_ptr[i], end = row_ptr[i + 1];
+    T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    int64_t e = beg;
+    for (; e + 8 <= end; e += 8) {
+      int c[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) c[u] = __ldg(col + e + u);
-          typename Vec2<T>::type z[8];
-          T sv[8];
+      for (int u = 0; u < 8; ++u) c[u] = __ldg(col + e + u);
+      V2 z0[8], z1[8];
+      T sv[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            z[u] = __ldg(reinterpret_cast<const typename Vec2<T>::type*>(zc + (int64_t)c[u] * KP));
-            if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
-            else sv[u] = (T)__ldg(s32 + c[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            a.x = fma(sv[u], z[u].x, a.x);
-            a.y = fma(sv[u], z[u].y, a.y);
-          }
-        }
-        for (; e < end; ++e) {
-          const int c = __ldg(col + e);
-          const typename Vec2<T>::type z =
-              __ldg(reinterpret_cast<const typename Vec2<T>::type*>(zc + (int64_t)c * KP));
-          T sv;
-          if constexpr (sizeof(T) == 8) sv = (T)__ldg(s + c);
-          else sv = (T)__ldg(s32 + c);
-          a.x = fma(sv, z.x, a.x);
-          a.y = fma(sv, z.y, a.y);
-        }
-        const typename Vec2<T>::type zo =
-            *reinterpret_cast<const typename Vec2<T>::type*>(Zg + (own_off + i) * KP + 2 * l);
-        T si;
-        if constexpr (sizeof(T) == 8) si = (T)s[own_off + i];
-        else si = s32[own_off + i];
-        typename Vec2<T>::type yv;
-        yv.x = -zo.x - si * a.x;
-        yv.y = -zo.y - si * a.y;
-        *reinterpret_cast<typename Vec2<T>::type*>(Y + i * KP + 2 * l) = yv;
-        y = make_double2((double)yv.x, (double)yv.y);
-        own = make_double2((double)zo.x, (double)zo.y);
-        if (MODE == 0) xo = ld2(Xown + i * KP + 2 * l);
+      for (int u = 0; u < 8; ++u) {
+        const V2* zr = reinterpret_cast<const V2*>(zc + (int64_t)c[u] * KP);
+        z0[u] = __ldg(zr);
+        z1[u] = __ldg(zr + 1);
+        if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
+        else sv[u] = (T)__ldg(s32 + c[u]);
       }
-      Ys[r * LD + 2 * l] = y.x;
-      Ys[r * LD + 2 * l + 1] = y.y;
-      Zs[r * LD + 2 * l] = own.x;
-      Zs[r * LD + 2 * l + 1] = own.y;
-      if (MODE == 0) {
-        Xs[r * LD + 2 * l] = xo.x;
-        Xs[r * LD + 2 * l + 1] = xo.y;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a0 = fma(sv[u], z0[u].x, a0);
+        a1 = fma(sv[u], z0[u].y, a1);
+        a2 = fma(sv[u], z1[u].x, a2);
+        a3 = fma(sv[u], z1[u].y, a3);
       }
     }
-    __syncthreads();
-    if (part) {
-      const int r4 = (rows + 3) & ~3;
-      if (MODE == 0) acc.accumulate(Zs, Ys, Xs, Ys, r4, warp, lane);   // T = Z^T Y, R' = X^T Y
-      else acc.accumulate(Zs, Zs, Zs, Ys, r4, warp, lane);             // M = Z^T Z, W = Z^T Y
+    for (; e < end; ++e) {
+      const int c = __ldg(col + e);
+      const V2* zr = reinterpret_cast<const V2*>(zc + (int64_t)c * KP);
+      const V2 z0 = __ldg(zr), z1 = __ldg(zr + 1);
+      T sv;
+      if constexpr (sizeof(T) == 8) sv = (T)__ldg(s + c);
+      else sv = (T)__ldg(s32 + c);
+      a0 = fma(sv, z0.x, a0);
+      a1 = fma(sv, z0.y, a1);
+      a2 = fma(sv, z1.x, a2);
+      a3 = fma(sv, z1.y, a3);
     }
-    __syncthreads();
+    const V2* zo = reinterpret_cast<const V2*>(Zg + (own_off + i) * KP + 4 * l);
+    const V2 o0 = zo[0], o1 = zo[1];
+    T si;
+    if constexpr (sizeof(T) == 8) si = (T)s[own_off + i];
+    else si = s32[own_off + i];
+    V2 y0, y1;
+    y0.x = -o0.x - si * a0;
+    y0.y = -o0.y - si * a1;
+    y1.x = -o1.x - si * a2;
+    y1.y = -o1.y - si * a3;
+    V2* yr = reinterpret_cast<V2*>(Y + i * KP + 4 * l);
+    yr[0] = y0;
+    yr[1] = y1;
   }
-  if (part) acc.store(part + (int64_t)blockIdx.x * 2 * KP * KP, warp, lane);
 }
 
-template <typename T, int KP, int MODE>
-static void launch_sg(int64_t n_local, int64_t own_off, const int64_t* row_ptr, const int32_t* col,
-                      const double* s, const float* s32, const void* Zg, const void* Xown, void* Y,
-                      double* part, const int* stop, int nblk, cudaStream_t st) {
-  const size_t smem = (size_t)(MODE == 0 ? 3 : 2) * kTR * (KP + 4) * 8;
-  auto kern = k_spmm_gram<T, KP, MODE>;
-  static bool set = false;
-  if (!set) {
-    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    set = true;
-  }
-  kern<<<nblk, kThreads, smem, st>>>(n_local, own_off, row_ptr, col, s, s32, (const T*)Zg,
-                                     (const T*)Xown, (T*)Y, part, stop);
+int spmm_grid(int64_t n_local) {
+  const int64_t warps = (n_local + 1) / 2;
+  int64_t b = (warps * 32 + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)num_sms() * 3;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
+                 const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
+                 const int* stop, cudaStream_t st) {
+  const int nb = spmm_grid(n_local);
+  OFSC_DISPATCH_KP(KP, {
+    if (dt == OFSC_F64)
+      k_spmm<double, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
+                                                   (const double*)Zg, (double*)Y, stop);
+    else
+      k_spmm<float, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
+                                                  (const float*)Zg, (float*)Y, stop);
+  });
   OFSC_LAUNCH_CHECK();
 }
 
@@ -133,15 +115,13 @@ void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       const int64_t* row_ptr, const int32_t* col, const double* s,
                       const float* s32, const void* Zg, const void* Xown, void* Y, double* part,
                       int mode, const int* stop, int nblk, cudaStream_t st) {
-  OFSC_DISPATCH_KP(KP, {
-    if (dt == OFSC_F64) {
-      if (mode == 0) launch_sg<double, KPC, 0>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
-      else launch_sg<double, KPC, 1>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
-    } else {
-      if (mode == 0) launch_sg<float, KPC, 0>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
-      else launch_sg<float, KPC, 1>(n_local, own_off, row_ptr, col, s, s32, Zg, Xown, Y, part, stop, nblk, st);
-    }
-  });
+  launch_spmm(dt, KP, n_local, own_off, row_ptr, col, s, s32, Zg, Y, stop, st);
+  if (part) {
+    const size_t es = dt == OFSC_F64 ? 8 : 4;
+    const void* Zown = (const char*)Zg + (size_t)own_off * KP * es;
+    launch_gram_stream(dt, KP, n_local, Zown, mode == 0 ? Xown : nullptr, Y, part, mode, stop,
+                       nblk, st);
+  }
 }
 
 // Plain SpMM with arbitrary leading dimensions (ABI hook ofsc_graph_apply):

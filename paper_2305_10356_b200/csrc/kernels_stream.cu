@@ -400,4 +400,119 @@ void launch_direction_gram(ofsc_dtype dt, const IterParams& p, int nblk, cudaStr
   });
 }
 
+// ---------------------------------------------------------------------------
+// C2b: streaming Gram pair over own rows, from the SpMM output Y
+//   mode 0 (iteration): T = Z^T Y (warps 0-3), R' = X^T Y (warps 4-7)
+//   mode 1 (refresh):   M = Z^T Z,             W  = Z^T Y
+// ---------------------------------------------------------------------------
+template <typename T, int KP>
+struct GSmem {
+  static constexpr int LD = KP + 4;
+  static constexpr size_t pad = (size_t)kSTR * LD * 8;
+  static constexpr size_t arr = (size_t)kSTR * KP * sizeof(T);
+  static constexpr size_t stage = 3 * arr;                            // Z, X, Y
+  static constexpr size_t bytes = 3 * pad + kSST * stage + kSST * 8;
+};
+
+template <typename T, int KP, int MODE>
+__global__ void __launch_bounds__(kThreads, 2)
+k_gram_stream(int64_t n_local, const T* __restrict__ gZ, const T* __restrict__ gX,
+              const T* __restrict__ gY, double* __restrict__ part, const int* stop) {
+  using S = GSmem<T, KP>;
+  constexpr int LD = S::LD;
+  if (stop && *stop) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* Zd = (double*)smraw;
+  double* Xd = Zd + kSTR * LD;
+  double* Yd = Xd + kSTR * LD;
+  unsigned char* stg = smraw + 3 * S::pad;
+  uint64_t* bar = (uint64_t*)(stg + kSST * S::stage);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (n_local + kSTR - 1) / kSTR;
+  auto arr = [&](int st, int a) { return (const T*)(stg + st * S::stage + a * S::arr); };
+  auto issue = [&](int st, int64_t tile) {
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, n_local - row0);
+    const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+    mbar_arrive_expect_tx(&bar[st], (MODE == 0 ? 3u : 2u) * b);
+    bulk_g2s((void*)arr(st, 0), gZ + row0 * KP, b, &bar[st]);
+    if (MODE == 0) bulk_g2s((void*)arr(st, 1), gX + row0 * KP, b, &bar[st]);
+    bulk_g2s((void*)arr(st, 2), gY + row0 * KP, b, &bar[st]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kSST; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < kSST; ++s) {
+      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+      if (tile < ntiles) issue(s, tile);
+    }
+  DmmaGram<KP> acc;
+  acc.zero();
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kSST;
+    const int rows = (int)imin64(kSTR, n_local - tile * kSTR);
+    mbar_wait(&bar[st], (uint32_t)((it / kSST) & 1));
+    const T* sZ = arr(st, 0);
+    const T* sX = arr(st, 1);
+    const T* sY = arr(st, 2);
+    for (int e = tid; e < kSTR * KP; e += kThreads) {
+      const int r = e / KP, c = e % KP;
+      const bool ok = r < rows;
+      Zd[r * LD + c] = ok ? (double)sZ[e] : 0.0;
+      if (MODE == 0) Xd[r * LD + c] = ok ? (double)sX[e] : 0.0;
+      Yd[r * LD + c] = ok ? (double)sY[e] : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t nxt = tile + (int64_t)kSST * gridDim.x;
+      if (nxt < ntiles) issue(st, nxt);            // stage st fully consumed above
+    }
+    const int r4 = (rows + 3) & ~3;
+    if (MODE == 0) acc.accumulate(Zd, Yd, Xd, Yd, r4, warp, lane);
+    else acc.accumulate(Zd, Zd, Zd, Yd, r4, warp, lane);
+    __syncthreads();
+  }
+  acc.store(part + (int64_t)blockIdx.x * 2 * KP * KP, warp, lane);
+}
+
+template <typename T, int KP, int MODE>
+static void launch_gs(int64_t n, const void* Z, const void* X, const void* Y, double* part,
+                      const int* stop, int nblk, cudaStream_t st) {
+  const size_t smem = GSmem<T, KP>::bytes;
+  auto kern = k_gram_stream<T, KP, MODE>;
+  static bool set = false;
+  if (!set) {
+    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = true;
+  }
+  kern<<<nblk, kThreads, smem, st>>>(n, (const T*)Z, (const T*)X, (const T*)Y, part, stop);
+  OFSC_LAUNCH_CHECK();
+}
+
+int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n) {
+  size_t b = 0;
+  OFSC_DISPATCH_KP(KP, {
+    b = dt == OFSC_F64 ? GSmem<double, KPC>::bytes : GSmem<float, KPC>::bytes;
+  });
+  return stream_grid(n, b);
+}
+
+void launch_gram_stream(ofsc_dtype dt, int KP, int64_t n, const void* Zown, const void* Xown,
+                        const void* Y, double* part, int mode, const int* stop, int nblk,
+                        cudaStream_t st) {
+  OFSC_DISPATCH_KP(KP, {
+    if (dt == OFSC_F64) {
+      if (mode == 0) launch_gs<double, KPC, 0>(n, Zown, Xown, Y, part, stop, nblk, st);
+      else launch_gs<double, KPC, 1>(n, Zown, Xown, Y, part, stop, nblk, st);
+    } else {
+      if (mode == 0) launch_gs<float, KPC, 0>(n, Zown, Xown, Y, part, stop, nblk, st);
+      else launch_gs<float, KPC, 1>(n, Zown, Xown, Y, part, stop, nblk, st);
+    }
+  });
+}
+
 }  // namespace ofsc
