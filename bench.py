@@ -38,8 +38,8 @@ sys.path.insert(0, ROOT)
 from synth import CONFIGS, config_graph, x0_block, kmeans_init_rows  # noqa: E402
 
 METRIC = "OF-method iterations/sec and HBM GB/s (fraction of peak) at 1/2/4/8 B200"
-PHASES = ("update_direction", "beta", "direction_gram", "spmm_gram", "gram_reduce",
-          "line_search", "refresh", "comm")
+PHASES = ("update_direction", "beta", "direction_gram", "spmm", "gram_reduce",
+          "line_search", "refresh", "comm", "gram_stream", "unused")
 
 
 def parse():
@@ -127,8 +127,10 @@ def algorithmic_bytes(cfg_n_local, nnz_local, n_global, k, es):
     """Compulsory bytes per launch of each hot kernel."""
     B = cfg_n_local * k * es
     return {
-        # C2: V once (own rows; every gathered row is a row of V), X, write AV, CSR + s
-        "spmm_gram": 3 * B + 4 * nnz_local + 8 * (cfg_n_local + 1) + 8 * n_global,
+        # C2a: V once (every gathered row is a row of V), write AV, CSR + s
+        "spmm": 2 * B + 4 * nnz_local + 8 * (cfg_n_local + 1) + 8 * n_global,
+        # C2b: read V, X, AV
+        "gram_stream": 3 * B,
         # C3: read X, V, AX, AV, Gp; write X, AX, G
         "update_direction": 8 * B,
         # C4: read G, Vp, X; write V
@@ -137,9 +139,10 @@ def algorithmic_bytes(cfg_n_local, nnz_local, n_global, k, es):
 
 
 def iteration_bytes(n_local, nnz_local, n_global, k, es):
-    """Compulsory bytes of one whole iteration: 15 N x k block passes + CSR + s."""
+    """Compulsory bytes of one whole iteration: 17 N x k block passes (C3 8, C4 4,
+    C2a 2, C2b 3) + CSR + s."""
     B = n_local * k * es
-    return 15 * B + 4 * nnz_local + 8 * (n_local + 1) + 8 * n_global
+    return 17 * B + 4 * nnz_local + 8 * (n_local + 1) + 8 * n_global
 
 
 def load_traffic():
@@ -221,8 +224,8 @@ def run_ours(args):
     # --- per-kernel profile pass (CUDA events per launch, same stream) ---
     prep = timed_run(args.method, profile=True)
     kern = {PHASES[i]: {"ms_total": prep["kernel_ms"][i], "launches": prep["kernel_launches"][i]}
-            for i in range(8) if prep["kernel_launches"][i] or prep["kernel_ms"][i]}
-    dom = max(("spmm_gram", "update_direction", "direction_gram"),
+            for i in range(10) if prep["kernel_launches"][i] or prep["kernel_ms"][i]}
+    dom = max(("spmm", "update_direction", "direction_gram", "gram_stream"),
               key=lambda n: kern.get(n, {}).get("ms_total", 0.0))
     nl = re_ - rb
     algo = algorithmic_bytes(nl, info["nnz_local"], cfg.n, k, es)

@@ -182,12 +182,13 @@ enum {
   OFSC_PH_UPDATE_DIRECTION = 0, /* C3: X += aV, AX += aAV, G = g_m(X), column dots */
   OFSC_PH_BETA = 1,             /* k x k: beta, ||G||, objective, stop flags */
   OFSC_PH_DIRECTION_GRAM = 2,   /* C4: V = -G + beta Vp, Q = V^T V, P = V^T X */
-  OFSC_PH_SPMM_GRAM = 3,        /* C2: AV = A V, T = V^T AV, R' = X^T AV */
+  OFSC_PH_SPMM_GRAM = 3,        /* C2a: AV = A V (neighbour gathers) */
   OFSC_PH_GRAM_REDUCE = 4,      /* fixed-order reduction of per-CTA Gram partials */
   OFSC_PH_LINE_SEARCH = 5,      /* k x k: cubics, roots, alpha, M/W update */
   OFSC_PH_REFRESH = 6,          /* refresh iterations: X update, A X, X^T X, X^T A X */
   OFSC_PH_COMM = 7,             /* NCCL collectives (p > 1) */
-  OFSC_NUM_PHASES = 8
+  OFSC_PH_GRAM_STREAM = 8,      /* C2b: T = V^T AV, R' = X^T AV (TMA-streamed, DMMA) */
+  OFSC_NUM_PHASES = 10
 };
 
 typedef struct {
@@ -200,8 +201,8 @@ typedef struct {
   int32_t timed_iters;        /* iterations inside the timing window */
   int32_t launches;           /* kernels this library launched inside the timing window */
   double timed_ms;            /* CUDA-event time of the timing window (opts.timing_skip) */
-  double kernel_ms[8];        /* opts.profile: summed per-phase kernel time in the window */
-  int32_t kernel_launches[8]; /* opts.profile: launches per phase in the window */
+  double kernel_ms[10];        /* opts.profile: summed per-phase kernel time in the window */
+  int32_t kernel_launches[10]; /* opts.profile: launches per phase in the window */
 } ofsc_report;
 
 /* d_X (local rows x ldx, dtype dt): in = X0 or a warm start, out = features.

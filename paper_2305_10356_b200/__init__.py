@@ -48,8 +48,8 @@ class Report(C.Structure):
                 ("n_three_root_steps", C.c_int32), ("n_zero_steps", C.c_int32),
                 ("grad_norm0", C.c_double), ("grad_norm", C.c_double),
                 ("objective", C.c_double), ("timed_iters", C.c_int32), ("launches", C.c_int32),
-                ("timed_ms", C.c_double), ("kernel_ms", C.c_double * 8),
-                ("kernel_launches", C.c_int32 * 8)]
+                ("timed_ms", C.c_double), ("kernel_ms", C.c_double * 10),
+                ("kernel_launches", C.c_int32 * 10)]
 
     def as_dict(self):
         out = {}
@@ -293,8 +293,8 @@ class Graph:
             pass
 
 
-PHASES = ("update_direction", "beta", "direction_gram", "spmm_gram", "gram_reduce",
-          "line_search", "refresh", "comm")
+PHASES = ("update_direction", "beta", "direction_gram", "spmm", "gram_reduce",
+          "line_search", "refresh", "comm", "gram_stream", "unused")
 
 
 def make_opts(k, max_iters, tol=0.0, beta_rule="pr+", line_search=True, alpha_fixed=0.0,

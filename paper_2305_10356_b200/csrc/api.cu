@@ -648,7 +648,7 @@ static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaSt
     });
     Zg = w.Xg;
   }
-  pr.ph(OFSC_PH_REFRESH, 2, [&] {
+  pr.ph(OFSC_PH_REFRESH, 3, [&] {
     launch_spmm_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
                      g->s32_slot, Zg, nullptr, w.AX, w.part_g2, 1, &p.ctl->stop, w.nb2, s);
     launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, p.M, s);  // M, W contiguous
@@ -682,8 +682,11 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
                               g->comm->nccl, s));
     });
   pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
-    launch_spmm_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
-                     g->s32_slot, w.Vg, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
+    launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
+                w.Vg, w.AV, &p.ctl->stop, s);
+  });
+  pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {
+    launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
   });
   pr.ph(OFSC_PH_GRAM_REDUCE, 2, [&] {
     launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, s);
