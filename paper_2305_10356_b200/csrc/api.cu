@@ -111,6 +111,8 @@ struct ofsc_graph_s {
   double* s_slot = nullptr;        // [p * slot_rows]
   float* s32_slot = nullptr;
   int32_t* perm = nullptr;         // internal row -> original node (reordered graphs)
+  int32_t* cid = nullptr;          // community of each internal row (reordered graphs)
+  int64_t* cstart = nullptr;       // community start rows [n_comm + 1]
   bool reordered = false;
   ofsc_graph_info info{};
   Workspace ws;
@@ -202,6 +204,8 @@ static void graph_free(ofsc_graph g) {
   dfree(g->s_slot);
   dfree(g->s32_slot);
   dfree(g->perm);
+  dfree(g->cid);
+  dfree(g->cstart);
 }
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
@@ -254,8 +258,9 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
         if (reorder) {
           // locality reordering derived from the graph: communities -> contiguous rows
           OFSC_CUDA(cudaMalloc(&g->perm, n * sizeof(int32_t)));
+          OFSC_CUDA(cudaMalloc(&g->cid, n * sizeof(int32_t)));
           DBuf inv(n * sizeof(int32_t), s);
-          lpa_order(csr, sweeps, g->perm, inv.as<int32_t>(), &n_comm, &intra, s);
+          lpa_order(csr, sweeps, g->perm, inv.as<int32_t>(), &n_comm, &intra, g->cid, &g->cstart, s);
           DBuf s2(m * sizeof(int64_t), s), d2(m * sizeof(int64_t), s);
           relabel_edges(m, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
           free_csr();
@@ -683,7 +688,8 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     });
   pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
     launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
-                w.Vg, w.AV, &p.ctl->stop, s);
+                w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
+                g->p == 1 ? g->cstart : nullptr);
   });
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {
     launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);

@@ -384,13 +384,24 @@ __global__ void k_lpa_keys(int64_t n, const int* lab, unsigned long long* keys) 
 }
 
 __global__ void k_perm_from_keys(int64_t n, const unsigned long long* keys, int32_t* perm,
-                                 int32_t* inv, const int* lab, int* newcomm) {
+                                 int32_t* inv, int* flag) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t node = (int32_t)(keys[j] & 0xffffffffull);
     perm[j] = node;
     inv[node] = (int32_t)j;
-    if (j == 0 || (keys[j] >> 32) != (keys[j - 1] >> 32)) atomicAdd(newcomm, 1);
+    flag[j] = (j == 0 || (keys[j] >> 32) != (keys[j - 1] >> 32)) ? 1 : 0;
+  }
+}
+
+// cid[j] = community index of internal row j (scan of the start flags); cstart[c] = first row
+__global__ void k_comm_index(int64_t n, const int* flag, const int* scan, int32_t* cid,
+                             int64_t* cstart) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int c = scan[j] - 1;
+    cid[j] = c;
+    if (flag[j]) cstart[c] = j;
   }
 }
 
@@ -419,7 +430,7 @@ __global__ void k_iota(int64_t n, int* lab) {
 }
 
 void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv, int64_t* n_comm,
-               double* intra_frac, cudaStream_t st) {
+               double* intra_frac, int32_t* d_cid, int64_t** d_cstart, cudaStream_t st) {
   const int64_t n = csr.n;
   DevBuf<int> la(n, st), lb(n, st), cnt(1, st);
   DevBuf<unsigned long long> keys(n, st), sorted(n, st), ic(1, st);
@@ -454,10 +465,17 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
     DevBuf<char> tmp(tmp_bytes, st);
     OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, n, 0, 64, st));
   }
-  OFSC_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
   OFSC_CUDA(cudaMemsetAsync(ic.p, 0, sizeof(unsigned long long), st));
-  k_perm_from_keys<<<blocks_for(n), 256, 0, st>>>(n, sorted.p, d_perm, d_inv, cur, cnt.p);
+  DevBuf<int> flag(n, st), scan(n, st);
+  k_perm_from_keys<<<blocks_for(n), 256, 0, st>>>(n, sorted.p, d_perm, d_inv, flag.p);
   OFSC_LAUNCH_CHECK();
+  {
+    size_t tb = 0;
+    OFSC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.p, scan.p, n, st));
+    DevBuf<char> tmp(tb, st);
+    OFSC_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, flag.p, scan.p, n, st));
+  }
+  OFSC_CUDA(cudaMemcpyAsync(cnt.p, scan.p + n - 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
   k_intra_edges<<<blocks_for(n), 256, 0, st>>>(n, csr.row_ptr, csr.col, cur, ic.p);
   OFSC_LAUNCH_CHECK();
   int h_cnt = 0;
@@ -467,6 +485,11 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
   OFSC_CUDA(cudaStreamSynchronize(st));
   *n_comm = h_cnt;
   *intra_frac = csr.nnz > 0 ? (double)h_ic / (double)csr.nnz : 1.0;
+  OFSC_CUDA(cudaMalloc(d_cstart, (h_cnt + 1) * sizeof(int64_t)));
+  k_comm_index<<<blocks_for(n), 256, 0, st>>>(n, flag.p, scan.p, d_cid, *d_cstart);
+  OFSC_LAUNCH_CHECK();
+  OFSC_CUDA(cudaMemcpyAsync(*d_cstart + h_cnt, &n, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  OFSC_CUDA(cudaStreamSynchronize(st));
 }
 
 void relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,

@@ -107,9 +107,12 @@ void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       const float* s32, const void* Zg, const void* Xown, void* Y,
                       double* part, int mode, const int* stop, int nblk, cudaStream_t st);
 // C2a: Y = A Z only (KP-padded rows)
+// cid/cstart (may be NULL): community of each row -> L2 evict_last for in-community
+// neighbour rows, evict_first for the rest (p == 1 only)
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
-                 const int* stop, cudaStream_t st);
+                 const int* stop, cudaStream_t st, const int32_t* cid = nullptr,
+                 const int64_t* cstart = nullptr);
 // C2b: TMA-streamed Gram pair over own rows (mode 0: Z^T Y, X^T Y; mode 1: Z^T Z, Z^T Y)
 int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n);
 void launch_gram_stream(ofsc_dtype dt, int KP, int64_t n, const void* Zown, const void* Xown,
@@ -164,8 +167,9 @@ struct CsrDevice {
 void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst, CsrDevice& out,
                cudaStream_t st);
 // locality reordering (label propagation): perm[new] = old, inv[old] = new
+// (also community id per internal row and community start rows, for L2 cache hints)
 void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv, int64_t* n_comm,
-               double* intra_frac, cudaStream_t st);
+               double* intra_frac, int32_t* d_cid, int64_t** d_cstart, cudaStream_t st);
 void relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
                    int64_t* s2, int64_t* d2, cudaStream_t st);
 void remap_columns(const int32_t* col_in, int64_t nnz, int32_t* col_out, const int64_t* d_begins,
