@@ -19,9 +19,9 @@ namespace ofsc {
 // columns = two 16-byte loads per neighbour), RPW = 32/LPR rows per warp; no
 // shared memory and no barriers, so warps stream independently and the register
 // file holds only accumulators and in-flight neighbour rows (8 per row).
-__device__ __forceinline__ uint64_t pol_evict_last() {
+__device__ __forceinline__ uint64_t pol_evict_normal() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t pol_evict_first() {
@@ -62,9 +62,10 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
        const int* stop, const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart) {
   if (stop && *stop) return;
-  // L2 residency: the current community's rows (reordered graphs) and s stay,
-  // streamed data (column ids, out-of-community rows, the output) goes first.
-  const uint64_t keep = pol_evict_last(), stream = pol_evict_first();
+  // L2 residency: the current community's rows (reordered graphs) keep normal
+  // priority; streamed data (column ids, out-of-community rows, the output) is
+  // marked evict-first so it does not push the community's working set out.
+  const uint64_t keep = pol_evict_normal(), stream = pol_evict_first();
   using V2 = typename Vec2<T>::type;
   constexpr int LPR = KP / 4;
   constexpr int RPW = 32 / LPR;
