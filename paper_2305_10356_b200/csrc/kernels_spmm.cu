@@ -19,53 +19,13 @@ namespace ofsc {
 // columns = two 16-byte loads per neighbour), RPW = 32/LPR rows per warp; no
 // shared memory and no barriers, so warps stream independently and the register
 // file holds only accumulators and in-flight neighbour rows (8 per row).
-__device__ __forceinline__ uint64_t pol_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t pol_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double2 ldg2h(const double* p, uint64_t pol) {
-  double2 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ float2 ldg2h(const float* p, uint64_t pol) {
-  float2 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
-               : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int ldg1h(const int32_t* p, uint64_t pol) {
-  int v;
-  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void stg2h(double* p, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
-               "l"(pol));
-}
-__device__ __forceinline__ void stg2h(float* p, float2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y),
-               "l"(pol));
-}
-
 template <typename T, int KP>
 __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
-       const int* stop, const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart) {
+       const int* stop) {
   if (stop && *stop) return;
-  // L2 residency: the current community's rows (reordered graphs) keep normal
-  // priority; streamed data (column ids, out-of-community rows, the output) is
-  // marked evict-first so it does not push the community's working set out.
-  const uint64_t keep = pol_evict_normal(), stream = pol_evict_first();
   using V2 = typename Vec2<T>::type;
   constexpr int LPR = KP / 4;
   constexpr int RPW = 32 / LPR;
@@ -77,26 +37,19 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
   const T* zc = Zg + 4 * l;
   for (int64_t i = gw * RPW + sub; i < n_local; i += nw * RPW) {
     const int64_t beg = row_ptr[i], end = row_ptr[i + 1];
-    int64_t lo = 0, hi = -1;                       // community of row i (hints only)
-    if (cid) {
-      const int ci = cid[i];
-      lo = cstart[ci];
-      hi = cstart[ci + 1];
-    }
     T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     int64_t e = beg;
     for (; e + 8 <= end; e += 8) {
       int c[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = ldg1h(col + e + u, stream);
+      for (int u = 0; u < 8; ++u) c[u] = __ldg(col + e + u);
       V2 z0[8], z1[8];
       T sv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const T* zr = zc + (int64_t)c[u] * KP;
-        const uint64_t pol = (cid == nullptr || (c[u] >= lo && c[u] < hi)) ? keep : stream;
-        z0[u] = ldg2h(zr, pol);
-        z1[u] = ldg2h(zr + 2, pol);
+        const V2* zr = reinterpret_cast<const V2*>(zc + (int64_t)c[u] * KP);
+        z0[u] = __ldg(zr);
+        z1[u] = __ldg(zr + 1);
         if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
         else sv[u] = (T)__ldg(s32 + c[u]);
       }
@@ -130,8 +83,9 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     y0.y = -o0.y - si * a1;
     y1.x = -o1.x - si * a2;
     y1.y = -o1.y - si * a3;
-    stg2h(Y + i * KP + 4 * l, y0, stream);
-    stg2h(Y + i * KP + 4 * l + 2, y1, stream);
+    V2* yr = reinterpret_cast<V2*>(Y + i * KP + 4 * l);
+    yr[0] = y0;
+    yr[1] = y1;
   }
 }
 
@@ -145,15 +99,20 @@ int spmm_grid(int64_t n_local) {
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart) {
+  // cid / cstart: community layout of reordered graphs.  L2 eviction-priority
+  // hints keyed on it (evict_last / evict_normal in-community, evict_first
+  // otherwise) were measured slower (12.3 and 8.0 ms vs 7.7 ms at c4,
+  // profiles/r01/SUMMARY), so the gathers use the default policy.
+  (void)cid;
+  (void)cstart;
   const int nb = spmm_grid(n_local);
   OFSC_DISPATCH_KP(KP, {
     if (dt == OFSC_F64)
       k_spmm<double, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                   (const double*)Zg, (double*)Y, stop, cid,
-                                                   cstart);
+                                                   (const double*)Zg, (double*)Y, stop);
     else
       k_spmm<float, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                  (const float*)Zg, (float*)Y, stop, cid, cstart);
+                                                  (const float*)Zg, (float*)Y, stop);
   });
   OFSC_LAUNCH_CHECK();
 }
