@@ -72,6 +72,7 @@ struct Workspace {
   double *part_cols = nullptr, *part_g4 = nullptr, *part_g2 = nullptr, *grams = nullptr;
   double* state = nullptr;  // M, W [KP*KP each], alpha, beta, gg_prev [KP], colred [2KP]
   DevCtl* ctl = nullptr;
+  unsigned long long* ctr = nullptr;  // SpMM work counter
   int nb3 = 0, nb4 = 0, nb2 = 0;
   cudaGraph_t g_iter = nullptr, g_refresh = nullptr;
   cudaGraphExec_t e_iter = nullptr, e_refresh = nullptr;
@@ -86,8 +87,9 @@ struct Workspace {
     e_iter = e_refresh = nullptr;
     g_iter = g_refresh = nullptr;
     for (void* q : {X, AX, G, AV, Vg, Xg, (void*)part_cols, (void*)part_g4, (void*)part_g2,
-                    (void*)grams, (void*)state, (void*)ctl})
+                    (void*)grams, (void*)state, (void*)ctl, (void*)ctr})
       dfree(q);
+    ctr = nullptr;
     X = AX = G = AV = Vg = Xg = nullptr;
     part_cols = part_g4 = part_g2 = grams = state = nullptr;
     ctl = nullptr;
@@ -544,6 +546,7 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   OFSC_CUDA(cudaMalloc(&w.grams, (size_t)4 * KP * KP * 8));
   OFSC_CUDA(cudaMalloc(&w.state, (size_t)(2 * KP * KP + 5 * KP) * 8));
   OFSC_CUDA(cudaMalloc(&w.ctl, sizeof(DevCtl)));
+  OFSC_CUDA(cudaMalloc(&w.ctr, sizeof(unsigned long long)));
   w.dt = dt;
   w.KP = KP;
   w.have = true;
@@ -689,7 +692,7 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
   pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
     launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
                 w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
-                g->p == 1 ? g->cstart : nullptr);
+                g->p == 1 ? g->cstart : nullptr, w.ctr);
   });
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {
     launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);

@@ -112,7 +112,8 @@ void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid = nullptr,
-                 const int64_t* cstart = nullptr);
+                 const int64_t* cstart = nullptr, unsigned long long* ctr = nullptr);
+constexpr int kSpmmChunk = 8;  // rows per dynamic work grab of the SpMM
 // C2b: TMA-streamed Gram pair over own rows (mode 0: Z^T Y, X^T Y; mode 1: Z^T Z, Z^T Y)
 int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n);
 void launch_gram_stream(ofsc_dtype dt, int KP, int64_t n, const void* Zown, const void* Xown,

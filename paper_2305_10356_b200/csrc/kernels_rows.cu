@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kThreads) k_gram_pair(int64_t n, const T* A, c
   double* Bs = As + kTR * LD;
   double* Cs = Bs + kTR * LD;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  DmmaGram<KP> acc;
+  typename GramSel<KP>::type acc;   // A^T A symmetric
   acc.zero();
   const int64_t ntiles = (n + kTR - 1) / kTR;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {

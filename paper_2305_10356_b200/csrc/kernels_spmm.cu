@@ -24,18 +24,38 @@ __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
-       const int* stop) {
+       const int* stop, unsigned long long* __restrict__ ctr) {
   if (stop && *stop) return;
   using V2 = typename Vec2<T>::type;
   constexpr int LPR = KP / 4;
   constexpr int RPW = 32 / LPR;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR, l = lane % LPR;
-  if (sub >= RPW) return;                       // KP = 48: lanes 24..31 idle
+  const bool active = sub < RPW;                // KP = 48: lanes 24..31 idle
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T* zc = Zg + 4 * l;
-  for (int64_t i = gw * RPW + sub; i < n_local; i += nw * RPW) {
+  // Rows are handed out in order in chunks of kSpmmChunk from a global counter
+  // (ctr != NULL), so all warps work on a narrow, advancing window of rows and
+  // the neighbour rows of the current (reordered) community stay in L2;
+  // ctr == NULL: static interleaved assignment.
+  constexpr int CH = kSpmmChunk;
+  int64_t round = 0;
+  while (true) {
+    int64_t base;
+    if (ctr) {
+      unsigned long long b0 = 0;
+      if (lane == 0) b0 = atomicAdd(ctr, (unsigned long long)CH);
+      base = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+    } else {
+      base = (gw + round * nw) * CH;
+      ++round;
+    }
+    if (base >= n_local) break;
+#pragma unroll 1
+    for (int q = 0; q < CH; q += RPW) {
+    const int64_t i = base + q + sub;
+    if (!active || i >= n_local) continue;
     const int64_t beg = row_ptr[i], end = row_ptr[i + 1];
     T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     int64_t e = beg;
@@ -86,10 +106,11 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     V2* yr = reinterpret_cast<V2*>(Y + i * KP + 4 * l);
     yr[0] = y0;
     yr[1] = y1;
+    }
   }
 }
 
-int spmm_grid(int64_t n_local) {
+int spmm_grid(int64_t n_local) {  // resident CTAs (3 per SM) for the chunked schedule
   const int64_t warps = (n_local + 1) / 2;
   int64_t b = (warps * 32 + kThreads - 1) / kThreads;
   const int64_t cap = (int64_t)num_sms() * 3;
@@ -98,7 +119,8 @@ int spmm_grid(int64_t n_local) {
 
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
-                 const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart) {
+                 const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart,
+                 unsigned long long* ctr) {
   // cid / cstart: community layout of reordered graphs.  L2 eviction-priority
   // hints keyed on it (evict_last / evict_normal in-community, evict_first
   // otherwise) were measured slower (12.3 and 8.0 ms vs 7.7 ms at c4,
@@ -106,13 +128,14 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   (void)cid;
   (void)cstart;
   const int nb = spmm_grid(n_local);
+  if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
   OFSC_DISPATCH_KP(KP, {
     if (dt == OFSC_F64)
       k_spmm<double, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                   (const double*)Zg, (double*)Y, stop);
+                                                   (const double*)Zg, (double*)Y, stop, ctr);
     else
       k_spmm<float, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                  (const float*)Zg, (float*)Y, stop);
+                                                  (const float*)Zg, (float*)Y, stop, ctr);
   });
   OFSC_LAUNCH_CHECK();
 }

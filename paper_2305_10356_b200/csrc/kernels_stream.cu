@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_direction_gram(IterParams p) {
       const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
       if (tile < ntiles) issue(s, tile);
     }
-  DmmaGram<KP> acc;
+  typename GramSel<KP>::type acc;   // Q = V^T V symmetric: upper blocks only at KP = 64
   acc.zero();
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -449,7 +449,7 @@ k_gram_stream(int64_t n_local, const T* __restrict__ gZ, const T* __restrict__ g
       const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
       if (tile < ntiles) issue(s, tile);
     }
-  DmmaGram<KP> acc;
+  typename GramSel<KP>::type acc;   // T (or M) symmetric: upper blocks only at KP = 64
   acc.zero();
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {

@@ -150,4 +150,122 @@ struct DmmaGram {
   }
 };
 
+// KP = 64 with a symmetric first product (Q = V^T V, T = V^T A V, M = X^T X):
+// only its 36 upper 8x8 blocks are computed (mirrored on store), and the 100
+// tiles are balanced over the 8 warps (12 or 13 each):
+//   warps 0-3:      product 1, block rows {2w, 2w+1} x block cols 0..5   (12 tiles)
+//   warps 4+q:      product 0, block rows q (cols q..7) and 7-q (cols 7-q..7) (9 tiles)
+//                   + product 1, block rows {2q, 2q+1} x cols {6, 7}          (4 tiles)
+struct DmmaGramSym64 {
+  static constexpr int KP = 64, LD = 68;
+  double d[13][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int u = 0; u < 13; ++u) d[u][0] = d[u][1] = 0.0;
+  }
+  template <int Q>
+  __device__ __forceinline__ void sym_step(const double* L0, const double* R0, const double* L1,
+                                           const double* R1, int rr, int gid) {
+    const double a0 = L0[rr + Q * 8 + gid];
+    const double a1 = L0[rr + (7 - Q) * 8 + gid];
+    constexpr int J0 = Q < 7 - Q ? Q : 7 - Q;
+    double b[8];
+#pragma unroll
+    for (int j = J0; j < 8; ++j) b[j] = R0[rr + j * 8 + gid];
+#pragma unroll
+    for (int j = Q; j < 8; ++j) dmma(d[j - Q][0], d[j - Q][1], a0, b[j]);
+#pragma unroll
+    for (int j = 7 - Q; j < 8; ++j) dmma(d[(8 - Q) + j - (7 - Q)][0], d[(8 - Q) + j - (7 - Q)][1], a1, b[j]);
+    const double c0 = L1[rr + (2 * Q) * 8 + gid], c1 = L1[rr + (2 * Q + 1) * 8 + gid];
+    const double e6 = R1[rr + 6 * 8 + gid], e7 = R1[rr + 7 * 8 + gid];
+    dmma(d[9][0], d[9][1], c0, e6);
+    dmma(d[10][0], d[10][1], c0, e7);
+    dmma(d[11][0], d[11][1], c1, e6);
+    dmma(d[12][0], d[12][1], c1, e7);
+  }
+  __device__ __forceinline__ void accumulate(const double* L0, const double* R0, const double* L1,
+                                             const double* R1, int rows, int warp, int lane) {
+    const int gid = lane >> 2, tig = lane & 3;
+    if (warp < 4) {
+      for (int r0 = 0; r0 < rows; r0 += 4) {
+        const int rr = (r0 + tig) * LD;
+        const double a0 = L1[rr + (2 * warp) * 8 + gid], a1 = L1[rr + (2 * warp + 1) * 8 + gid];
+        double b[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) b[j] = R1[rr + j * 8 + gid];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          dmma(d[j][0], d[j][1], a0, b[j]);
+          dmma(d[6 + j][0], d[6 + j][1], a1, b[j]);
+        }
+      }
+    } else {
+      const int q = warp - 4;
+      for (int r0 = 0; r0 < rows; r0 += 4) {
+        const int rr = (r0 + tig) * LD;
+        switch (q) {
+          case 0: sym_step<0>(L0, R0, L1, R1, rr, gid); break;
+          case 1: sym_step<1>(L0, R0, L1, R1, rr, gid); break;
+          case 2: sym_step<2>(L0, R0, L1, R1, rr, gid); break;
+          default: sym_step<3>(L0, R0, L1, R1, rr, gid); break;
+        }
+      }
+    }
+  }
+  // out[0] = product 0 (full, mirrored), out[1] = product 1 (row-major 64 x 64 each)
+  __device__ __forceinline__ void put(double* o, int ib, int jb, int gid, int tig, const double* v) const {
+    double* q = o + (ib * 8 + gid) * KP + jb * 8 + 2 * tig;
+    q[0] = v[0];
+    q[1] = v[1];
+  }
+  __device__ __forceinline__ void put_sym(double* o, int ib, int jb, int gid, int tig,
+                                          const double* v) const {
+    put(o, ib, jb, gid, tig, v);
+    if (ib != jb) {   // mirror: (jb*8 + 2tig + h, ib*8 + gid)
+      o[(jb * 8 + 2 * tig) * KP + ib * 8 + gid] = v[0];
+      o[(jb * 8 + 2 * tig + 1) * KP + ib * 8 + gid] = v[1];
+    }
+  }
+  template <int Q>
+  __device__ __forceinline__ void store_q(double* out, int gid, int tig) const {
+#pragma unroll
+    for (int j = Q; j < 8; ++j) put_sym(out, Q, j, gid, tig, d[j - Q]);
+#pragma unroll
+    for (int j = 7 - Q; j < 8; ++j) put_sym(out, 7 - Q, j, gid, tig, d[(8 - Q) + j - (7 - Q)]);
+    double* o1 = out + KP * KP;
+    put(o1, 2 * Q, 6, gid, tig, d[9]);
+    put(o1, 2 * Q, 7, gid, tig, d[10]);
+    put(o1, 2 * Q + 1, 6, gid, tig, d[11]);
+    put(o1, 2 * Q + 1, 7, gid, tig, d[12]);
+  }
+  __device__ __forceinline__ void store(double* out, int warp, int lane) const {
+    const int gid = lane >> 2, tig = lane & 3;
+    if (warp < 4) {
+      double* o1 = out + KP * KP;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        put(o1, 2 * warp, j, gid, tig, d[j]);
+        put(o1, 2 * warp + 1, j, gid, tig, d[6 + j]);
+      }
+    } else {
+      switch (warp - 4) {
+        case 0: store_q<0>(out, gid, tig); break;
+        case 1: store_q<1>(out, gid, tig); break;
+        case 2: store_q<2>(out, gid, tig); break;
+        default: store_q<3>(out, gid, tig); break;
+      }
+    }
+  }
+};
+
+// Gram accumulator for a tile width: the symmetric-aware one at KP = 64.
+template <int KP>
+struct GramSel {
+  using type = DmmaGram<KP>;
+};
+template <>
+struct GramSel<64> {
+  using type = DmmaGramSym64;
+};
+
 }  // namespace ofsc
