@@ -29,34 +29,37 @@ struct StreamTile {
 // ---------------------------------------------------------------------------
 // C3
 // ---------------------------------------------------------------------------
+// C3 tiling: warp w < KP/8 owns output column block cb = w for both 8-row blocks
+// of the 16-row tile; its DMMA B-fragments of M (and W) -- 16 k-steps -- stay in
+// registers for the whole kernel, so shared memory holds only the 2-stage TMA
+// ring and the padded X', AX' tile (2 CTAs per SM).
+constexpr int kC3Stages = 2;
+
 template <typename T, int KP, int METHOD>
 struct C3Smem {
-  static constexpr bool USE_W = (METHOD == OFSC_OFM_F2 || METHOD == OFSC_TRIOFM_F2);
   static constexpr int LD = KP + 4;
-  static constexpr size_t ms = (size_t)KP * LD * 8;
-  static constexpr size_t ws = USE_W ? ms : 0;
   static constexpr size_t xp = (size_t)kSTR * LD * 8;
   static constexpr size_t arr = (size_t)kSTR * KP * sizeof(T);
   static constexpr size_t stage = 5 * arr;                          // X, AX, V, AV, G
-  static constexpr size_t bytes = ms + ws + 2 * xp + kSST * stage + KP * 8 + kSST * 8;
+  static constexpr size_t bytes = 2 * xp + kC3Stages * stage + KP * 8 + kC3Stages * 8;
 };
 
 template <typename T, int KP, int METHOD>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 k_update_direction(IterParams p, int apply_update) {
   using S = C3Smem<T, KP, METHOD>;
   constexpr int LD = S::LD;
+  constexpr int NS = kC3Stages;
   constexpr bool TRI = (METHOD == OFSC_TRIOFM_F1 || METHOD == OFSC_TRIOFM_F2);
   constexpr bool F1 = (METHOD == OFSC_OFM_F1 || METHOD == OFSC_TRIOFM_F1);
   constexpr int NB = KP / 8;
+  constexpr int KS = KP / 4;                     // DMMA k-steps
   if (p.ctl->stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
-  double* Ms = (double*)smraw;
-  double* Ws = (double*)(smraw + S::ms);
-  double* Xp = (double*)(smraw + S::ms + S::ws);
+  double* Xp = (double*)smraw;
   double* AXp = Xp + kSTR * LD;
-  unsigned char* stg = smraw + S::ms + S::ws + 2 * S::xp;
-  double* s_alpha = (double*)(stg + kSST * S::stage);
+  unsigned char* stg = smraw + 2 * S::xp;
+  double* s_alpha = (double*)(stg + NS * S::stage);
   uint64_t* bar = (uint64_t*)(s_alpha + KP);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
@@ -82,31 +85,34 @@ k_update_direction(IterParams p, int apply_update) {
     bulk_g2s(arr(st, 4), gG + off, b, &bar[st]);
   };
   if (tid == 0) {
-    for (int s = 0; s < kSST; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
     fence_barrier_init();
-  }
-  for (int e = tid; e < KP * KP; e += kThreads) {
-    const int j = e / KP, c = e % KP;
-    const bool keep = !TRI || j <= c;              // triu keeps the diagonal (R15)
-    Ms[j * LD + c] = keep ? p.M[e] : 0.0;
-    if (S::USE_W) Ws[j * LD + c] = keep ? p.W[e] : 0.0;
   }
   if (tid < KP) s_alpha[tid] = apply_update ? p.alpha[tid] : 0.0;
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < kSST; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
       if (tile < ntiles) issue(s, tile);
     }
-  // per-lane column dots: columns cb*8 + 2 tig (+1) for the lane's cb slots
-  const int rb = warp >> 2, wp = warp & 3;
-  double gg[2][2] = {{0, 0}, {0, 0}}, dg[2][2] = {{0, 0}, {0, 0}};
+  // register-resident B fragments: B[k][n] = M[4 kk + tig][cb*8 + gid] (triu for TriOFM)
+  const bool mma_warp = warp < NB;
+  const int cb = mma_warp ? warp : 0;
+  double bm[KS], bw[F1 ? 1 : KS];
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int j = 4 * kk + tig, c = cb * 8 + gid;
+    const bool keep = !TRI || j <= c;            // triu keeps the diagonal (R15)
+    bm[kk] = keep ? p.M[j * KP + c] : 0.0;
+    if (!F1) bw[kk] = keep ? p.W[j * KP + c] : 0.0;
+  }
+  double gg[2] = {0.0, 0.0}, dg[2] = {0.0, 0.0};
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % kSST;
+    const int st = it % NS;
     const int64_t row0 = tile * kSTR;
     const int rows = (int)imin64(kSTR, p.n_local - row0);
-    mbar_wait(&bar[st], (uint32_t)((it / kSST) & 1));
+    mbar_wait(&bar[st], (uint32_t)((it / NS) & 1));
     T* sX = arr(st, 0);
     T* sAX = arr(st, 1);
     const T* sV = arr(st, 2);
@@ -137,51 +143,44 @@ k_update_direction(IterParams p, int apply_update) {
       bulk_s2g(gAX + row0 * KP, sAX, b);
       bulk_commit();
     }
-    // phase B: G tile = f(X' M, X' W, AX' M) on DMMA.  Warp: row block rb, column
-    // blocks wp and wp + 4.
-    double a1[2][2] = {{0, 0}, {0, 0}}, a2[2][2] = {{0, 0}, {0, 0}};
-    const double* xrow = Xp + (rb * 8 + gid) * LD + tig;
-    const double* arow = AXp + (rb * 8 + gid) * LD + tig;
-#pragma unroll 4
-    for (int j0 = 0; j0 < KP; j0 += 4) {
-      const double xa = xrow[j0];
-      const double aa = F1 ? 0.0 : arow[j0];
-      const int mrow = (j0 + tig) * LD + gid;
+    if (mma_warp) {
+      // phase B: G tile column block cb = f(X' M, X' W, AX' M) on DMMA (both row blocks)
+      double a1[2][2] = {{0, 0}, {0, 0}}, a2[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int cb = wp + 4 * u;
-        if (cb < NB) {
-          const double m = Ms[mrow + cb * 8];
+      for (int kk = 0; kk < KS; ++kk) {
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb) {
+          const int o = (rb * 8 + gid) * LD + 4 * kk + tig;
+          const double xa = Xp[o];
           if (F1) {
-            dmma(a1[u][0], a1[u][1], xa, m);                 // X M (or X triu M)
+            dmma(a1[rb][0], a1[rb][1], xa, bm[kk]);           // X M (or X triu M)
           } else {
-            const double w = Ws[mrow + cb * 8];
-            dmma(a1[u][0], a1[u][1], xa, w);                 // X W (or X triu W)
-            dmma(a2[u][0], a2[u][1], aa, m);                 // AX M (or AX triu M)
+            const double aa = AXp[o];
+            dmma(a1[rb][0], a1[rb][1], xa, bw[kk]);           // X W (or X triu W)
+            dmma(a2[rb][0], a2[rb][1], aa, bm[kk]);           // AX M (or AX triu M)
           }
         }
       }
-    }
-    // phase C: G, column dots, in-place store into the stage's G tile
-    const int r = rb * 8 + gid;
+      // phase C: G, column dots, in-place store into the stage's G tile
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int cb = wp + 4 * u;
-      if (cb < NB && r < rows) {
+      for (int rb = 0; rb < 2; ++rb) {
+        const int r = rb * 8 + gid;
+        if (r < rows) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = cb * 8 + 2 * tig + h;
-          const double ax = AXp[r * LD + c];
-          double g;
-          if (METHOD == OFSC_OFM_F1) g = 4.0 * ax + 4.0 * a1[u][h];
-          else if (METHOD == OFSC_TRIOFM_F1) g = ax + a1[u][h];
-          else if (METHOD == OFSC_OFM_F2) g = 4.0 * ax - 2.0 * a1[u][h] - 2.0 * a2[u][h];
-          else g = 2.0 * ax - a2[u][h] - a1[u][h];
-          g = rndT<T>(g);
-          const double gp = (double)sG[r * KP + c];
-          sG[r * KP + c] = (T)g;
-          gg[u][h] = fma(g, g, gg[u][h]);
-          dg[u][h] = fma(g - gp, g, dg[u][h]);
+          for (int h = 0; h < 2; ++h) {
+            const int c = cb * 8 + 2 * tig + h;
+            const double ax = AXp[r * LD + c];
+            double g;
+            if (METHOD == OFSC_OFM_F1) g = 4.0 * ax + 4.0 * a1[rb][h];
+            else if (METHOD == OFSC_TRIOFM_F1) g = ax + a1[rb][h];
+            else if (METHOD == OFSC_OFM_F2) g = 4.0 * ax - 2.0 * a1[rb][h] - 2.0 * a2[rb][h];
+            else g = 2.0 * ax - a2[rb][h] - a1[rb][h];
+            g = rndT<T>(g);
+            const double gp = (double)sG[r * KP + c];
+            sG[r * KP + c] = (T)g;
+            gg[h] = fma(g, g, gg[h]);
+            dg[h] = fma(g - gp, g, dg[h]);
+          }
         }
       }
     }
@@ -190,7 +189,7 @@ k_update_direction(IterParams p, int apply_update) {
     if (tid == 0) {
       bulk_s2g(gG + row0 * KP, sG, (uint32_t)rows * KP * sizeof(T));
       bulk_commit();
-      const int64_t nxt = tile + (int64_t)kSST * gridDim.x;
+      const int64_t nxt = tile + (int64_t)NS * gridDim.x;
       if (nxt < ntiles) {
         bulk_wait_read_all();                     // stage st no longer read by the stores
         issue(st, nxt);
@@ -198,33 +197,22 @@ k_update_direction(IterParams p, int apply_update) {
     }
   }
   if (tid == 0) bulk_wait_all();
-  // column partials: reduce over gid (lanes), then over the two row-block warps
+  // column partials: lanes of one tig hold the same two columns -> reduce over gid
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int o = 4; o < 32; o <<= 1) {
+      gg[h] += __shfl_xor_sync(0xffffffffu, gg[h], o);
+      dg[h] += __shfl_xor_sync(0xffffffffu, dg[h], o);
+    }
+  if (mma_warp && gid == 0) {
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        gg[u][h] += __shfl_xor_sync(0xffffffffu, gg[u][h], o);
-        dg[u][h] += __shfl_xor_sync(0xffffffffu, dg[u][h], o);
-      }
-  __syncthreads();
-  double* red = Xp;   // [2 rb][2][KP]
-  if (gid == 0) {
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int cb = wp + 4 * u;
-      if (cb < NB)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = cb * 8 + 2 * tig + h;
-          red[rb * 2 * KP + c] = gg[u][h];
-          red[rb * 2 * KP + KP + c] = dg[u][h];
-        }
+    for (int h = 0; h < 2; ++h) {
+      const int c = cb * 8 + 2 * tig + h;
+      p.part_cols[(int64_t)blockIdx.x * 2 * KP + c] = gg[h];
+      p.part_cols[(int64_t)blockIdx.x * 2 * KP + KP + c] = dg[h];
     }
   }
-  __syncthreads();
-  if (tid < 2 * KP) p.part_cols[(int64_t)blockIdx.x * 2 * KP + tid] = red[tid] + red[2 * KP + tid];
 }
 
 template <typename T, int KP, int METHOD>
