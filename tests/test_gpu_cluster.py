@@ -87,8 +87,10 @@ def test_algorithm1_end_to_end_c1(method):
     s, d, lab = config_graph(cfg)
     X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
     rows = kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)
+    # same operator ordering as the oracle (reorder=False): the 200-iteration
+    # trajectories are compared, which rounding-order changes would perturb (R22)
     labels, feats, rep = ofsc.spectral_cluster(cfg.n, s, d, method, X0, cfg.blocks, rows,
-                                               max_iters=cfg.iters)
+                                               max_iters=cfg.iters, reorder=False)
     op = build_operator(cfg.n, s, d)
     o = run_ofm(op, method, X0, cfg.iters, refresh=0)
     Y = row_normalize(o.X)
