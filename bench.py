@@ -268,6 +268,30 @@ def run_ours(args):
     }
     del iter_hbm
 
+    # --- Algorithm 1 stage breakdown on the resident graph (p == 1) ---
+    if world == 1:
+        def timed(fn):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            out_ = fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return out_, a.elapsed_time(b)
+        X = X0d.clone()
+        _, ms_run = timed(lambda: ofsc.run(g, args.method, X, cfg.iters, refresh=args.refresh))
+        Y, ms_norm = timed(lambda: ofsc.row_normalize(X))
+        rows = torch.from_numpy(kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)).cuda()
+        C0 = Y[rows].contiguous()
+        (lab, km_it, _), ms_km = timed(lambda: ofsc.kmeans(Y, C0, 100))
+        g0, ms_build_plain = timed(lambda: ofsc.Graph(cfg.n, src, dst, reorder=False))
+        g0.close()
+        out["pipeline_ms"] = {
+            "graph_build": round(build_ms, 2), "graph_build_no_reorder": round(ms_build_plain, 2),
+            f"run_{cfg.iters}_iters": round(ms_run, 2), "row_normalize": round(ms_norm, 3),
+            "kmeans": round(ms_km, 2), "kmeans_lloyd_steps": km_it,
+            "ari_vs_planted": round(ofsc.scores(lab.cpu().numpy(), labels)[0], 4)}
+
     # --- all four methods, same protocol ---
     if not args.no_methods:
         per = {}

@@ -113,7 +113,19 @@ __global__ void k_kmeans_partial(int64_t n, int dim, const T* __restrict__ Y, in
   const int64_t r0 = (int64_t)blockIdx.x * per;
   const int64_t r1 = imin64(n, r0 + per);
   if (tid < W) {
-    for (int64_t r = r0; r < r1; ++r) {
+    // rows in order (deterministic sums); loads of 8 rows issued ahead of the adds
+    int64_t r = r0;
+    for (; r + 8 <= r1; r += 8) {
+      int c[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = labels[r + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = tid < dim ? ld1(Y + (r + u) * ldy + tid) : 1.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[c[u] * W + tid] += v[u];
+    }
+    for (; r < r1; ++r) {
       const int c = labels[r];
       acc[c * W + tid] += tid < dim ? ld1(Y + r * ldy + tid) : 1.0;
     }
