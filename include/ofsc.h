@@ -235,7 +235,7 @@ ofsc_status ofsc_row_normalize(ofsc_dtype dt, int64_t n_local, int32_t k, const 
  * out: final).  Assign: argmin_c sum_{d<dim} (y_d - C_cd)^2 (fp64, summed in
  * d order, ties -> lowest c); update: cluster means (empty cluster keeps its
  * centroid); stop when no label changes or after max_iters assignments.
- * d_labels: int32 local rows.  iters_out / inertia_out optional host outputs. */
+ * d_labels: int32 local rows; 1 <= n_clusters <= 128.  iters_out / inertia_out optional host outputs. */
 ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t dim,
                         const void* d_Y, int64_t ldy, int32_t n_clusters, double* d_centroids,
                         int32_t max_iters, int32_t* d_labels, int32_t* iters_out,

@@ -969,7 +969,7 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                         double* inertia_out, ofsc_stream stream) {
   return guard([&] {
     OFSC_REQUIRE(d_Y && d_centroids && d_labels && n_local >= 0 && dim >= 1 && ldy >= dim &&
-                     n_clusters >= 1 && max_iters >= 1,
+                     n_clusters >= 1 && n_clusters <= 128 && max_iters >= 1,
                  OFSC_ERR_ARG, "bad kmeans args");
     OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
     cudaStream_t s = (cudaStream_t)stream;

@@ -12,16 +12,21 @@ namespace ofsc {
 
 constexpr int kKmThreads = 256;
 
-// One warp per row; lane l evaluates centroids l, l+32, ...; centroids are held
-// transposed in smem (Ct[d][c]) so a warp's reads are conflict-free.
-template <typename T>
+// One warp per group of KR rows; lane l evaluates centroids l, l+32, ... (KC per
+// lane) for all KR rows at once (KR*KC independent accumulation chains, each
+// summed in d order); centroids are held transposed in smem (Ct[d][c]) so a
+// warp's reads are conflict-free and each Ct element is reused KR times.
+constexpr int kKmRows = 4;
+
+template <typename T, int KC>
 __global__ void __launch_bounds__(kKmThreads)
 k_kmeans_assign(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
                 const double* __restrict__ C, int* __restrict__ labels,
                 unsigned long long* changes, double* part_inertia) {
+  constexpr int KR = kKmRows;
   extern __shared__ double sm[];
   double* Ct = sm;                         // [dim][K]
-  double* rows = Ct + (size_t)dim * K;     // [8 warps][dim]
+  double* rows = Ct + (size_t)dim * K;     // [8 warps][KR][dim]
   __shared__ double s_in[kKmThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < dim * K; e += kKmThreads) {
@@ -29,38 +34,64 @@ k_kmeans_assign(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
     Ct[d * K + c] = C[e];
   }
   __syncthreads();
-  double* yr = rows + warp * dim;
+  double* yr = rows + (size_t)warp * KR * dim;
   double inertia = 0.0;
   unsigned long long nchg = 0;
   const int64_t nw = (int64_t)gridDim.x * (kKmThreads / 32);
-  for (int64_t r = (int64_t)blockIdx.x * (kKmThreads / 32) + warp; r < n; r += nw) {
-    for (int d = lane; d < dim; d += 32) yr[d] = ld1(Y + r * ldy + d);
+  for (int64_t r0 = ((int64_t)blockIdx.x * (kKmThreads / 32) + warp) * KR; r0 < n; r0 += nw * KR) {
+    for (int e = lane; e < KR * dim; e += 32) {
+      const int q = e / dim, d = e % dim;
+      yr[e] = r0 + q < n ? ld1(Y + (r0 + q) * ldy + d) : 0.0;
+    }
     __syncwarp();
-    double best = 0.0;
-    int bc = 0x7fffffff;
-    for (int c = lane; c < K; c += 32) {
-      double acc = 0.0;
-      for (int d = 0; d < dim; ++d) {
-        const double diff = yr[d] - Ct[d * K + c];
-        acc = acc + diff * diff;
+    double acc[KR][KC];
+#pragma unroll
+    for (int q = 0; q < KR; ++q)
+#pragma unroll
+      for (int j = 0; j < KC; ++j) acc[q][j] = 0.0;
+    for (int d = 0; d < dim; ++d) {
+      double cv[KC];
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        const int c = lane + 32 * j;
+        cv[j] = c < K ? Ct[d * K + c] : 0.0;
       }
-      if (bc == 0x7fffffff || acc < best) {   // c increases: strict < keeps the lowest index
-        best = acc;
-        bc = c;
+#pragma unroll
+      for (int q = 0; q < KR; ++q) {
+        const double y = yr[q * dim + d];
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+          const double diff = y - cv[j];
+          acc[q][j] = acc[q][j] + diff * diff;
+        }
       }
     }
-    for (int o = 16; o; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-      if (oc != 0x7fffffff && (bc == 0x7fffffff || ob < best || (ob == best && oc < bc))) {
-        best = ob;
-        bc = oc;
+#pragma unroll
+    for (int q = 0; q < KR; ++q) {
+      double best = 0.0;
+      int bc = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {
+        const int c = lane + 32 * j;
+        if (c < K && (bc == 0x7fffffff || acc[q][j] < best)) {  // c increases: lowest index wins ties
+          best = acc[q][j];
+          bc = c;
+        }
       }
-    }
-    if (lane == 0) {
-      if (labels[r] != bc) ++nchg;
-      labels[r] = bc;
-      inertia += best;
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (oc != 0x7fffffff && (bc == 0x7fffffff || ob < best || (ob == best && oc < bc))) {
+          best = ob;
+          bc = oc;
+        }
+      }
+      const int64_t r = r0 + q;
+      if (lane == 0 && r < n) {
+        if (labels[r] != bc) ++nchg;
+        labels[r] = bc;
+        inertia += best;
+      }
     }
     __syncwarp();
   }
@@ -82,21 +113,41 @@ int kmeans_blocks(int64_t n) {
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+template <typename T, int KC>
+static void launch_assign_kc(int64_t n, int dim, const T* Y, int64_t ldy, int K, const double* C,
+                             int* labels, unsigned long long* changes, double* part_inertia,
+                             int nblk, size_t smem, cudaStream_t st) {
+  OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_assign<T, KC>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_kmeans_assign<T, KC><<<nblk, kKmThreads, smem, st>>>(n, dim, Y, ldy, K, C, labels, changes,
+                                                         part_inertia);
+  OFSC_LAUNCH_CHECK();
+}
+
+template <typename T>
+static void launch_assign_t(int64_t n, int dim, const T* Y, int64_t ldy, int K, const double* C,
+                            int* labels, unsigned long long* changes, double* part_inertia,
+                            int nblk, size_t smem, cudaStream_t st) {
+  const int kc = (K + 31) / 32;
+  if (kc <= 1) launch_assign_kc<T, 1>(n, dim, Y, ldy, K, C, labels, changes, part_inertia, nblk, smem, st);
+  else if (kc == 2) launch_assign_kc<T, 2>(n, dim, Y, ldy, K, C, labels, changes, part_inertia, nblk, smem, st);
+  else if (kc == 3) launch_assign_kc<T, 3>(n, dim, Y, ldy, K, C, labels, changes, part_inertia, nblk, smem, st);
+  else if (kc == 4) launch_assign_kc<T, 4>(n, dim, Y, ldy, K, C, labels, changes, part_inertia, nblk, smem, st);
+  else throw Error{OFSC_ERR_ARG, "n_clusters > 128 not supported"};
+}
+
 void launch_kmeans_assign(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                           const double* C, int* labels, unsigned long long* changes,
                           double* part_inertia, int nblk, cudaStream_t st) {
-  const size_t smem = ((size_t)dim * K + (size_t)(kKmThreads / 32) * dim) * sizeof(double);
+  const size_t smem =
+      ((size_t)dim * K + (size_t)(kKmThreads / 32) * kKmRows * dim) * sizeof(double);
   OFSC_REQUIRE(smem <= 200 * 1024, OFSC_ERR_ARG, "n_clusters * dim too large for K-means smem");
-  if (dt == OFSC_F64) {
-    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_kmeans_assign<double><<<nblk, kKmThreads, smem, st>>>(n, dim, (const double*)Y, ldy, K, C,
-                                                            labels, changes, part_inertia);
-  } else {
-    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_assign<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_kmeans_assign<float><<<nblk, kKmThreads, smem, st>>>(n, dim, (const float*)Y, ldy, K, C,
-                                                           labels, changes, part_inertia);
-  }
-  OFSC_LAUNCH_CHECK();
+  if (dt == OFSC_F64)
+    launch_assign_t<double>(n, dim, (const double*)Y, ldy, K, C, labels, changes, part_inertia,
+                            nblk, smem, st);
+  else
+    launch_assign_t<float>(n, dim, (const float*)Y, ldy, K, C, labels, changes, part_inertia,
+                           nblk, smem, st);
 }
 
 // Partial cluster sums of a contiguous row range: part[b][c][0..dim-1] = sums,
