@@ -87,6 +87,14 @@ ofsc_status ofsc_get_unique_id(void* h_id128);
 ofsc_status ofsc_comm_create(const void* h_id128, int nranks, int rank, int cuda_device,
                              ofsc_comm* out);
 ofsc_status ofsc_comm_destroy(ofsc_comm comm);
+/* Test communicator for rank `rank` of `nranks` WITHOUT NCCL: graph build and the
+ * kernel hooks (ofsc_graph_apply / _apply_gram) run on this rank's row block with
+ * rank-partial reductions; ofsc_run / ofsc_kmeans reject it (OFSC_ERR_STATE).
+ * Lets one process check the multi-rank partition and layout on one GPU. */
+ofsc_status ofsc_comm_create_local(int nranks, int rank, ofsc_comm* out);
+/* Host-only: contiguous split of rows [0, n) over p ranks with ~equal nnz(A)
+ * = sum_i (deg_i + 1), from CSR offsets h_row_ptr[n+1]; h_begins[p+1] out. */
+ofsc_status ofsc_partition_rows(int64_t n, const int64_t* h_row_ptr, int p, int64_t* h_begins);
 
 /* ---- graph -> operator A = L - 2I (Alg. 1 l.2) ----------
  * Canonical undirected edge set: self-loops dropped, duplicates collapsed

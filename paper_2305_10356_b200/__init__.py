@@ -88,6 +88,8 @@ SIGNATURES = {
     "ofsc_get_unique_id": (_ST, [_P]),
     "ofsc_comm_create": (_ST, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "ofsc_comm_destroy": (_ST, [_P]),
+    "ofsc_comm_create_local": (_ST, [C.c_int, C.c_int, C.POINTER(_P)]),
+    "ofsc_partition_rows": (_ST, [_I64, _P, C.c_int, _P]),
     "ofsc_graph_build": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, _P, C.POINTER(_P)]),
     "ofsc_graph_build_ex": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, C.POINTER(BuildOpts), _P,
                                   C.POINTER(_P)]),
@@ -179,20 +181,27 @@ def _dev2d(t):
 class Comm:
     """NCCL communicator over torch.distributed ranks (one process per GPU)."""
 
-    def __init__(self, group=None):
+    @staticmethod
+    def broadcast_unique_id(group=None) -> bytes:
+        """Rank 0 creates the NCCL unique id; every rank returns the same 128 bytes."""
         import torch.distributed as dist
         torch = _torch()
-        self.rank = dist.get_rank(group)
-        self.size = dist.get_world_size(group)
         uid = torch.zeros(128, dtype=torch.uint8)
-        if self.rank == 0:
+        if dist.get_rank(group) == 0:
             buf = (C.c_ubyte * 128)()
             _check(lib().ofsc_get_unique_id(C.cast(buf, C.c_void_p)))
             uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
         if dist.get_backend(group) == "nccl":
             uid = uid.cuda()
         dist.broadcast(uid, 0, group=group)
-        raw = bytes(uid.cpu().tolist())
+        return bytes(uid.cpu().tolist())
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        raw = Comm.broadcast_unique_id(group)
         buf = (C.c_ubyte * 128).from_buffer_copy(raw)
         h = C.c_void_p()
         _check(lib().ofsc_comm_create(C.cast(buf, C.c_void_p), self.size, self.rank,
@@ -203,6 +212,30 @@ class Comm:
         if self.handle:
             _check(lib().ofsc_comm_destroy(self.handle))
             self.handle = None
+
+
+class LocalComm:
+    """Test communicator (no NCCL): rank `rank` of `size` in this process (see
+    ofsc_comm_create_local).  Graph build and kernel hooks only."""
+
+    def __init__(self, size, rank):
+        h = C.c_void_p()
+        _check(lib().ofsc_comm_create_local(int(size), int(rank), C.byref(h)))
+        self.handle, self.size, self.rank = h, size, rank
+
+    def close(self):
+        if self.handle:
+            _check(lib().ofsc_comm_destroy(self.handle))
+            self.handle = None
+
+
+def partition_rows(row_ptr, p):
+    """nnz-balanced contiguous row split (host function of the library)."""
+    rp = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
+    out = np.empty(int(p) + 1, np.int64)
+    _check(lib().ofsc_partition_rows(rp.size - 1, rp.ctypes.data_as(C.c_void_p), int(p),
+                                     out.ctypes.data_as(C.c_void_p)))
+    return out
 
 
 class Graph:

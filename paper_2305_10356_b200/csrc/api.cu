@@ -198,6 +198,38 @@ ofsc_status ofsc_comm_destroy(ofsc_comm comm) {
 // ---------------------------------------------------------------------------
 // graph build
 // ---------------------------------------------------------------------------
+// Contiguous split of rows [0, n) over p ranks with ~equal nnz(A) = sum (deg_i + 1).
+static void partition_rows(int64_t n, const int64_t* rp, int p, int64_t* begins) {
+  begins[0] = 0;
+  begins[p] = n;
+  const double total = (double)(rp[n] + n);
+  int64_t i = 0;
+  for (int r = 1; r < p; ++r) {
+    const double target = total * r / p;
+    while (i < n && (double)(rp[i] + i) < target) ++i;
+    begins[r] = std::max(i, begins[r - 1]);
+  }
+}
+
+ofsc_status ofsc_partition_rows(int64_t n, const int64_t* h_row_ptr, int p, int64_t* h_begins) {
+  return guard([&] {
+    OFSC_REQUIRE(n >= 1 && h_row_ptr && h_begins && p >= 1, OFSC_ERR_ARG, "bad partition args");
+    partition_rows(n, h_row_ptr, p, h_begins);
+  });
+}
+
+ofsc_status ofsc_comm_create_local(int nranks, int rank, ofsc_comm* out) {
+  return guard([&] {
+    OFSC_REQUIRE(out && nranks >= 1 && rank >= 0 && rank < nranks, OFSC_ERR_ARG,
+                 "bad communicator arguments");
+    auto* c = new ofsc_comm_s();
+    c->nranks = nranks;
+    c->rank = rank;
+    OFSC_CUDA(cudaGetDevice(&c->device));
+    *out = c;  // nccl == nullptr: no collectives (test communicator)
+  });
+}
+
 static void graph_free(ofsc_graph g) {
   g->ws.release();
   dfree(g->d_begins);
@@ -281,14 +313,8 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
                               cudaMemcpyDeviceToHost, s));
     OFSC_CUDA(cudaStreamSynchronize(s));
     g->begins.assign(p + 1, 0);
-    g->begins[p] = n;
+    partition_rows(n, rp.data(), p, g->begins.data());
     const double total = (double)(csr.nnz + n);
-    int64_t i = 0;
-    for (int r = 1; r < p; ++r) {
-      const double target = total * r / p;
-      while (i < n && (double)(rp[i] + i) < target) ++i;
-      g->begins[r] = std::max(i, g->begins[r - 1]);
-    }
     g->row_begin = g->begins[g->rank];
     g->row_end = g->begins[g->rank + 1];
     g->n_local = g->row_end - g->row_begin;
@@ -443,7 +469,8 @@ static void to_slots(ofsc_graph g, ofsc_dtype dt, int k, int KP, const void* src
 }
 
 static void allreduce_d(ofsc_graph g, double* buf, size_t count, cudaStream_t s) {
-  if (g->p > 1) OFSC_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, g->comm->nccl, s));
+  if (g->p > 1 && g->comm->nccl)   // a local test communicator keeps rank-partial sums
+    OFSC_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, g->comm->nccl, s));
 }
 
 __global__ void k_extract_kk(const double* in, int KP, int k, double* out) {
@@ -746,6 +773,8 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
     OFSC_REQUIRE(ldx >= o.k && o.max_iters >= 0, OFSC_ERR_ARG, "bad ldx / max_iters");
     OFSC_REQUIRE(o.beta_rule >= 0 && o.beta_rule <= 2 && o.refresh >= 0 && o.tol >= 0.0,
                  OFSC_ERR_ARG, "bad options");
+    OFSC_REQUIRE(g->p == 1 || g->comm->nccl, OFSC_ERR_STATE,
+                 "ofsc_run needs an NCCL communicator when p > 1 (local test communicator given)");
     cudaStream_t s = (cudaStream_t)stream;
     const int KP = padded_k(o.k);
     ensure_workspace(g, dt, KP, s);
@@ -972,6 +1001,8 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                      n_clusters >= 1 && n_clusters <= 128 && max_iters >= 1,
                  OFSC_ERR_ARG, "bad kmeans args");
     OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
+    OFSC_REQUIRE(!comm || comm->nranks == 1 || comm->nccl, OFSC_ERR_STATE,
+                 "ofsc_kmeans needs an NCCL communicator when p > 1");
     cudaStream_t s = (cudaStream_t)stream;
     const int K = n_clusters;
     const int nb = kmeans_blocks(std::max<int64_t>(n_local, 1));

@@ -176,3 +176,49 @@ def test_reordered_graph_is_a_permutation_of_the_operator(name):
     assert np.max(np.abs(Y2.cpu().numpy() - Yo)) <= 4e-14 * np.max(np.abs(Yo))
     for got, want in zip(Gm.cpu().numpy(), (Q, P, T, Rp)):
         assert rel(got, want) <= 1e-13
+
+
+@pytest.mark.parametrize("p", [2, 3])
+@pytest.mark.parametrize("reorder", [False, True])
+def test_multirank_layout_with_local_comms(p, reorder):
+    """p ranks emulated in one process (local test communicators, no NCCL): each
+    rank's graph holds the nnz-balanced row block with slot-remapped columns;
+    per-rank SpMM rows and rank-partial Grams reassemble the global results."""
+    s, d, n = GRAPHS["c2"]()
+    op = build_operator(n, s, d)
+    k = 32
+    rng = np.random.default_rng(11)
+    Z = rng.standard_normal((n, k)) / np.sqrt(n)
+    X = rng.standard_normal((n, k)) / np.sqrt(n)
+    Yo = apply_A(op, Z)
+    want = grams(Z, X, Yo)
+    Gsum = np.zeros((4, k, k))
+    covered = np.zeros(n, np.int64)
+    for r in range(p):
+        comm = ofsc.LocalComm(p, r)
+        g = ofsc.Graph(n, s, d, comm=comm, reorder=reorder)
+        info = g.info
+        rb, re_ = info["row_begin"], info["row_end"]
+        perm = g.copy_perm()
+        if not reorder:
+            assert np.array_equal(ofsc.partition_rows(op.row_ptr, p)[[r, r + 1]], [rb, re_])
+        nodes = perm[rb:re_]                       # original ids of this rank's rows
+        covered[nodes] += 1
+        rp, col, _ = g.copy_csr()
+        for i in np.random.default_rng(r).choice(re_ - rb, 20, replace=False):
+            got = np.sort(perm[col[rp[i]:rp[i + 1]]])
+            u = nodes[i]
+            assert np.array_equal(got, op.col[op.row_ptr[u]:op.row_ptr[u + 1]])
+        Y = g.apply(torch.from_numpy(Z).cuda()).cpu().numpy()      # local rows, internal order
+        assert np.max(np.abs(Y - Yo[nodes])) <= 4e-14 * np.max(np.abs(Yo))
+        Xl = torch.from_numpy(np.ascontiguousarray(X[nodes])).cuda()
+        Y2, Gm = g.apply_gram(torch.from_numpy(Z).cuda(), Xl)
+        assert np.max(np.abs(Y2.cpu().numpy() - Yo[nodes])) <= 4e-14 * np.max(np.abs(Yo))
+        Gsum += Gm.cpu().numpy()
+        with pytest.raises(ofsc.OfscError):
+            ofsc.run(g, "ofm_f2", Xl.clone(), 2)       # iterations need real collectives
+        g.close()
+        comm.close()
+    assert np.all(covered == 1)
+    for got, w in zip(Gsum, want):
+        assert rel(got, w) <= 1e-13
