@@ -341,11 +341,10 @@ def run_e2e(args, cfg, comm, src, dst, X0, world, rank, barrier, max_over_ranks)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         a.record(stream)
-        bo = ofsc.BuildOpts(1 if args.reorder else 0, 30)
         st = L.ofsc_spectral_cluster(comm.handle if comm else None, cfg.n, src.size,
                                      C.c_void_p(h_src.data_ptr()), C.c_void_p(h_dst.data_ptr()),
                                      ofsc.METHODS[args.method], ofsc.DTYPES[args.dtype], C.byref(o),
-                                     C.byref(bo), C.c_void_p(h_X.data_ptr()), cfg.blocks,
+                                     None, C.c_void_p(h_X.data_ptr()), cfg.blocks,
                                      C.c_void_p(rows.data_ptr()), 100,
                                      C.c_void_p(h_lab.data_ptr()), C.byref(rep),
                                      C.c_void_p(stream.cuda_stream))

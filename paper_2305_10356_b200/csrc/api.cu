@@ -1136,7 +1136,9 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     OFSC_REQUIRE(opts && h_X && h_init_rows && h_labels && n_clusters >= 1 && opts->k >= 1,
                  OFSC_ERR_ARG, "bad spectral_cluster args");
     cudaStream_t s = (cudaStream_t)stream;
-    ofsc_build_opts bo{1, 30};
+    // default: reorder only when the run is long enough to repay the LPA pass
+    // (~0.2 s at 5M nodes vs ~2 ms saved per iteration there)
+    ofsc_build_opts bo{opts->max_iters >= 100 ? 1 : 0, 30};
     if (bopts) bo = *bopts;
     ofsc_status b = ofsc_graph_build_ex(comm, n, m, h_src, h_dst, 0, &bo, stream, &g);
     if (b != OFSC_OK) throw Error{b, g_last_error};
