@@ -432,7 +432,7 @@ def scores(a, b):
 
 
 def spectral_cluster(n, src, dst, method, X0, n_clusters, init_rows, *, max_iters,
-                     dtype="f64", km_max_iters=100, reorder=True, comm: Comm | None = None,
+                     dtype="f64", km_max_iters=100, reorder=None, comm: Comm | None = None,
                      stream=None, **run_opts):
     """Algorithm 1 end to end from host buffers (ofsc_spectral_cluster).
 
@@ -446,12 +446,12 @@ def spectral_cluster(n, src, dst, method, X0, n_clusters, init_rows, *, max_iter
     rows = np.ascontiguousarray(np.asarray(init_rows, dtype=np.int64))
     labels = np.full(X.shape[0], -1, np.int32)
     o = make_opts(X.shape[1], max_iters, **run_opts)
-    bo = BuildOpts(1 if reorder else 0, 30)
+    bo = None if reorder is None else BuildOpts(1 if reorder else 0, 30)   # None: library default
     rep = Report()
     _check(lib().ofsc_spectral_cluster(comm.handle if comm else None, int(n), src.size,
                                        src.ctypes.data_as(C.c_void_p),
                                        dst.ctypes.data_as(C.c_void_p), METHODS[method],
-                                       DTYPES[dtype], C.byref(o), C.byref(bo),
+                                       DTYPES[dtype], C.byref(o), C.byref(bo) if bo else None,
                                        X.ctypes.data_as(C.c_void_p), int(n_clusters),
                                        rows.ctypes.data_as(C.c_void_p), int(km_max_iters),
                                        labels.ctypes.data_as(C.c_void_p), C.byref(rep),
