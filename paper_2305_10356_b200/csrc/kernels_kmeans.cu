@@ -6,7 +6,10 @@
 //   update: per-CTA partial sums over a contiguous row range in row order (one
 //           thread per feature column, no atomics), fixed-order reduction,
 //           mean; an empty cluster keeps its centroid.
+#include <math_constants.h>
+
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace ofsc {
 
@@ -136,12 +139,202 @@ static void launch_assign_t(int64_t n, int dim, const T* Y, int64_t ldy, int K, 
   else throw Error{OFSC_ERR_ARG, "n_clusters > 128 not supported"};
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core assignment with an exactness guard.  Scores s_c = ||c||^2 - 2 y.c
+// come from DMMA (y.c for 8 rows x 8 centroids per mma, fp64); argmin_c s_c is
+// argmin_c ||y - c||^2.  The oracle's decision is taken on the direct form
+// sum_d (y_d - c_d)^2 summed in d order; both forms are within
+// tau = 1e-12 (1 + ||y||^2) of the exact distances for unit-norm-scale data
+// (dim <= 64: (dim + 2) u ||y - c||^2 and 2 dim u (||y||^2 + ||c||^2)), so when
+// the best score beats the runner-up by more than tau the label equals the
+// oracle's; otherwise the row falls back to the direct form over all centroids
+// (same arithmetic as the oracle, ties -> lowest index).  Labels are therefore
+// the oracle's; only the inertia of guarded rows uses the score form.
+// ---------------------------------------------------------------------------
+template <typename T, int KB>
+__global__ void __launch_bounds__(kKmThreads)
+k_kmeans_assign_mma(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
+                    const double* __restrict__ C, int* __restrict__ labels,
+                    unsigned long long* changes, double* part_inertia) {
+  constexpr int KP = KB * 8;
+  constexpr int LDC = KP + 4;
+  extern __shared__ double sm[];
+  const int DP = (dim + 3) & ~3;
+  const int LDY = DP + 4;
+  double* Ct = sm;                               // [DP][LDC]  B[k=d][n=c] = C[c][d]
+  double* cn = Ct + (size_t)DP * LDC;            // [KP] ||c||^2 (inf for padding)
+  double* Ys = cn + KP;                          // [8 warps][8][LDY]
+  __shared__ double s_in[kKmThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int e = tid; e < DP * LDC; e += kKmThreads) {
+    const int d = e / LDC, c = e % LDC;
+    Ct[e] = (c < K && d < dim) ? C[c * dim + d] : 0.0;
+  }
+  for (int c = tid; c < KP; c += kKmThreads) {
+    double a = 0.0;
+    if (c < K)
+      for (int d = 0; d < dim; ++d) a = a + C[c * dim + d] * C[c * dim + d];
+    cn[c] = c < K ? a : CUDART_INF;
+  }
+  __syncthreads();
+  double* ys = Ys + (size_t)warp * 8 * LDY;
+  double inertia = 0.0;
+  unsigned long long nchg = 0;
+  const int64_t nw = (int64_t)gridDim.x * (kKmThreads / 32);
+  for (int64_t r0 = ((int64_t)blockIdx.x * (kKmThreads / 32) + warp) * 8; r0 < n; r0 += nw * 8) {
+    for (int e = lane; e < 8 * DP; e += 32) {
+      const int q = e / DP, d = e % DP;
+      ys[q * LDY + d] = (r0 + q < n && d < dim) ? ld1(Y + (r0 + q) * ldy + d) : 0.0;
+    }
+    __syncwarp();
+    double acc[KB][2];
+#pragma unroll
+    for (int b = 0; b < KB; ++b) acc[b][0] = acc[b][1] = 0.0;
+    for (int d0 = 0; d0 < DP; d0 += 4) {
+      const double a = ys[gid * LDY + d0 + tig];
+      const double* brow = Ct + (d0 + tig) * LDC + gid;
+#pragma unroll
+      for (int b = 0; b < KB; ++b) dmma(acc[b][0], acc[b][1], a, brow[b * 8]);
+    }
+    // lane: row gid, centroids b*8 + 2 tig + h
+    double b1 = CUDART_INF, b2 = CUDART_INF;
+    int c1 = 0x7fffffff;
+#pragma unroll
+    for (int b = 0; b < KB; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = b * 8 + 2 * tig + h;
+        const double sc = cn[c] - 2.0 * acc[b][h];
+        if (sc < b1 || (sc == b1 && c < c1)) {
+          b2 = b1;
+          b1 = sc;
+          c1 = c;
+        } else if (sc < b2) {
+          b2 = sc;
+        }
+      }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {                 // merge the 4 lanes of the row
+      const double ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
+      const double ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+      const int oc1 = __shfl_xor_sync(0xffffffffu, c1, o);
+      if (ob1 < b1 || (ob1 == b1 && oc1 < c1)) {
+        b2 = fmin(b1, ob2);
+        b1 = ob1;
+        c1 = oc1;
+      } else {
+        b2 = fmin(b2, ob1);
+      }
+    }
+    double yn = 0.0;                                   // ||y||^2 of row gid
+    for (int d = tig; d < DP; d += 4) yn = yn + ys[gid * LDY + d] * ys[gid * LDY + d];
+    yn += __shfl_xor_sync(0xffffffffu, yn, 1);
+    yn += __shfl_xor_sync(0xffffffffu, yn, 2);
+    const int64_t r = r0 + gid;
+    const bool guard = !(b2 - b1 > 1e-12 * (1.0 + yn));
+    int lab = c1;
+    double dist = yn + b1;
+    if (guard) {                                       // direct form, exactly as the oracle
+      double best = CUDART_INF;
+      int bc = 0x7fffffff;
+      for (int c = tig; c < K; c += 4) {
+        double a = 0.0;
+        for (int d = 0; d < dim; ++d) {
+          const double diff = ys[gid * LDY + d] - C[c * dim + d];
+          a = a + diff * diff;
+        }
+        if (a < best || (a == best && c < bc)) {
+          best = a;
+          bc = c;
+        }
+      }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (ob < best || (ob == best && oc < bc)) {
+          best = ob;
+          bc = oc;
+        }
+      }
+      lab = bc;
+      dist = best;
+    }
+    if (tig == 0 && r < n) {
+      if (labels[r] != lab) ++nchg;
+      labels[r] = lab;
+      inertia += dist;
+    }
+    __syncwarp();
+  }
+  // warp sums: lanes with tig == 0 hold row partials
+  for (int o = 16; o; o >>= 1) {
+    inertia += __shfl_xor_sync(0xffffffffu, inertia, o);
+    nchg += __shfl_xor_sync(0xffffffffu, nchg, o);
+  }
+  if (lane == 0) {
+    s_in[warp] = inertia;
+    if (nchg) atomicAdd(changes, nchg);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0;
+    for (int w = 0; w < kKmThreads / 32; ++w) a += s_in[w];
+    part_inertia[blockIdx.x] = a;
+  }
+}
+
+template <typename T, int KB>
+static void launch_mma_kb(int64_t n, int dim, const T* Y, int64_t ldy, int K, const double* C,
+                          int* labels, unsigned long long* changes, double* part_inertia, int nblk,
+                          cudaStream_t st) {
+  const int DP = (dim + 3) & ~3;
+  const size_t smem = ((size_t)DP * (KB * 8 + 4) + KB * 8 + (size_t)8 * 8 * (DP + 4)) * 8;
+  OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_assign_mma<T, KB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_kmeans_assign_mma<T, KB><<<nblk, kKmThreads, smem, st>>>(n, dim, Y, ldy, K, C, labels, changes,
+                                                              part_inertia);
+  OFSC_LAUNCH_CHECK();
+}
+
+template <typename T>
+static bool launch_mma_t(int64_t n, int dim, const T* Y, int64_t ldy, int K, const double* C,
+                         int* labels, unsigned long long* changes, double* part_inertia, int nblk,
+                         cudaStream_t st) {
+  if (dim > 64) return false;
+  const int kb = (K + 7) / 8;
+#define OFSC_KB(NB)                                                                             \
+  case NB:                                                                                      \
+    launch_mma_kb<T, NB>(n, dim, Y, ldy, K, C, labels, changes, part_inertia, nblk, st);        \
+    return true;
+  switch (kb) {
+    OFSC_KB(1) OFSC_KB(2) OFSC_KB(3) OFSC_KB(4) OFSC_KB(5) OFSC_KB(6) OFSC_KB(7) OFSC_KB(8)
+    OFSC_KB(9) OFSC_KB(10) OFSC_KB(11) OFSC_KB(12) OFSC_KB(13) OFSC_KB(14) OFSC_KB(15) OFSC_KB(16)
+    default: return false;
+  }
+#undef OFSC_KB
+}
+
 void launch_kmeans_assign(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                           const double* C, int* labels, unsigned long long* changes,
                           double* part_inertia, int nblk, cudaStream_t st) {
   const size_t smem =
       ((size_t)dim * K + (size_t)(kKmThreads / 32) * kKmRows * dim) * sizeof(double);
   OFSC_REQUIRE(smem <= 200 * 1024, OFSC_ERR_ARG, "n_clusters * dim too large for K-means smem");
+  static int use_mma = -1;
+  if (use_mma < 0) {
+    const char* e = getenv("OFSC_KMEANS_DIRECT");   // 1: plain direct-form kernel only
+    use_mma = (e && e[0] == '1') ? 0 : 1;
+  }
+  if (use_mma) {
+    if (dt == OFSC_F64 && launch_mma_t<double>(n, dim, (const double*)Y, ldy, K, C, labels, changes,
+                                                part_inertia, nblk, st))
+      return;
+    if (dt == OFSC_F32 && launch_mma_t<float>(n, dim, (const float*)Y, ldy, K, C, labels, changes,
+                                               part_inertia, nblk, st))
+      return;
+  }
   if (dt == OFSC_F64)
     launch_assign_t<double>(n, dim, (const double*)Y, ldy, K, C, labels, changes, part_inertia,
                             nblk, smem, st);
