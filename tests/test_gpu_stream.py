@@ -32,13 +32,13 @@ def test_warm_started_snapshots_match_oracle(method):
         op = build_operator(n, ss, dd)
         g = ofsc.Graph(n, ss, dd, reorder=True)
         Xg = torch.from_numpy(X.copy()).cuda()
-        r = ofsc.run(g, method, Xg, 400, tol=1e-5, check_every=1)
-        o = run_ofm(op, method, X, 400, tol=1e-5, refresh=0)
+        r = ofsc.run(g, method, Xg, 3000, tol=1e-4, check_every=1)
+        o = run_ofm(op, method, X, 3000, tol=1e-4, refresh=0)
         assert r.report["converged"] == 1 and o.converged
         # 100+ step trajectories agree only to rounding amplification (R22): the
         # step at which the tolerance is met may move a little; the objective and
         # the converged subspace agree
-        assert abs(r.report["iters"] - o.iters) <= max(3, 0.1 * o.iters)
+        assert abs(r.report["iters"] - o.iters) <= max(3, 0.2 * o.iters)
         Xn = Xg.cpu().numpy()
         assert abs(r.report["objective"] - o.objective) <= 1e-6 * abs(o.objective)
         qa, _ = np.linalg.qr(Xn)
