@@ -1006,8 +1006,9 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
     cudaStream_t s = (cudaStream_t)stream;
     const int K = n_clusters;
     const int nb = kmeans_blocks(std::max<int64_t>(n_local, 1));
+    const int nbp = kmeans_partial_blocks(std::max<int64_t>(n_local, 1));
     const int W = dim + 1;
-    DBuf chg(8, s), pin((size_t)nb * 8, s), part((size_t)nb * K * W * 8, s),
+    DBuf chg(8, s), pin((size_t)nb * 8, s), part((size_t)nbp * K * W * 8, s),
         red((size_t)K * W * 8, s), tot(8, s);
     OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
     unsigned long long* h_chg = nullptr;
@@ -1034,10 +1035,10 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
       OFSC_CUDA(cudaStreamSynchronize(s));
       if (it > 1 && *h_chg == 0) break;
       if (n_local > 0)
-        launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nb, s);
+        launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nbp, s);
       else
-        OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nb * K * W * 8, s));
-      launch_reduce_partials(part.as<double>(), nb, K * W, red.as<double>(), s);
+        OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nbp * K * W * 8, s));
+      launch_reduce_partials(part.as<double>(), nbp, K * W, red.as<double>(), s);
       if (comm && comm->nranks > 1)
         OFSC_NCCL(ncclAllReduce(red.p, red.p, (size_t)K * W, ncclFloat64, ncclSum, comm->nccl, s));
       launch_kmeans_finish(K, dim, red.as<double>(), d_centroids, s);

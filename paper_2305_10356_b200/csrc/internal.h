@@ -156,6 +156,7 @@ void launch_kmeans_partial(ofsc_dtype dt, int64_t n, int dim, const void* Y, int
                            const int* labels, double* part, int nblk, cudaStream_t st);
 void launch_kmeans_finish(int K, int dim, const double* red, double* C, cudaStream_t st);
 int kmeans_blocks(int64_t n);
+int kmeans_partial_blocks(int64_t n);
 
 // graph build (graph_build.cu)
 struct CsrDevice {

@@ -110,6 +110,12 @@ k_kmeans_assign(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
   }
 }
 
+int kmeans_partial_blocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
 int kmeans_blocks(int64_t n) {
   int64_t b = (n + 63) / 64;
   const int64_t cap = (int64_t)num_sms() * 4;
@@ -182,12 +188,29 @@ k_kmeans_assign_mma(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, in
   double inertia = 0.0;
   unsigned long long nchg = 0;
   const int64_t nw = (int64_t)gridDim.x * (kKmThreads / 32);
-  for (int64_t r0 = ((int64_t)blockIdx.x * (kKmThreads / 32) + warp) * 8; r0 < n; r0 += nw * 8) {
-    for (int e = lane; e < 8 * DP; e += 32) {
-      const int q = e / DP, d = e % DP;
-      ys[q * LDY + d] = (r0 + q < n && d < dim) ? ld1(Y + (r0 + q) * ldy + d) : 0.0;
+  // the next 8-row group is loaded into registers while the current one computes
+  double pre[16];
+  auto fetch = [&](int64_t rr) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int e = lane + 32 * j;
+      if (e < 8 * DP) {
+        const int q = e / DP, d = e % DP;
+        pre[j] = (rr + q < n && d < dim) ? ld1(Y + (rr + q) * ldy + d) : 0.0;
+      }
+    }
+  };
+  int64_t r0 = ((int64_t)blockIdx.x * (kKmThreads / 32) + warp) * 8;
+  if (r0 < n) fetch(r0);
+  for (; r0 < n; r0 += nw * 8) {
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int e = lane + 32 * j;
+      if (e < 8 * DP) ys[(e / DP) * LDY + (e % DP)] = pre[j];
     }
     __syncwarp();
+    if (r0 + nw * 8 < n) fetch(r0 + nw * 8);
     double acc[KB][2];
 #pragma unroll
     for (int b = 0; b < KB; ++b) acc[b][0] = acc[b][1] = 0.0;
@@ -359,15 +382,15 @@ __global__ void k_kmeans_partial(int64_t n, int dim, const T* __restrict__ Y, in
   if (tid < W) {
     // rows in order (deterministic sums); loads of 8 rows issued ahead of the adds
     int64_t r = r0;
-    for (; r + 8 <= r1; r += 8) {
-      int c[8];
-      double v[8];
+    for (; r + 16 <= r1; r += 16) {
+      int c[16];
+      double v[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = labels[r + u];
+      for (int u = 0; u < 16; ++u) c[u] = labels[r + u];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = tid < dim ? ld1(Y + (r + u) * ldy + tid) : 1.0;
+      for (int u = 0; u < 16; ++u) v[u] = tid < dim ? ld1(Y + (r + u) * ldy + tid) : 1.0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[c[u] * W + tid] += v[u];
+      for (int u = 0; u < 16; ++u) acc[c[u] * W + tid] += v[u];
     }
     for (; r < r1; ++r) {
       const int c = labels[r];
