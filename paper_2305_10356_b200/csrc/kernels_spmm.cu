@@ -10,6 +10,8 @@
 // runs are bitwise reproducible.
 //   mode 0 (iteration):  T = Z^T Y, R' = X^T Y    (Z = V)
 //   mode 1 (refresh):    M = Z^T Z, W = Z^T Y     (Z = X)
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -24,7 +26,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
-       const int* stop, unsigned long long* __restrict__ ctr) {
+       const int* stop, unsigned long long* __restrict__ ctr, int ch) {
   if (stop && *stop) return;
   using V2 = typename Vec2<T>::type;
   constexpr int LPR = KP / 4;
@@ -39,7 +41,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
   // (ctr != NULL), so all warps work on a narrow, advancing window of rows and
   // the neighbour rows of the current (reordered) community stay in L2;
   // ctr == NULL: static interleaved assignment.
-  constexpr int CH = kSpmmChunk;
+  const int CH = ch;
   int64_t round = 0;
   while (true) {
     int64_t base;
@@ -110,10 +112,15 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
   }
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
 int spmm_grid(int64_t n_local) {  // resident CTAs (3 per SM) for the chunked schedule
   const int64_t warps = (n_local + 1) / 2;
   int64_t b = (warps * 32 + kThreads - 1) / kThreads;
-  const int64_t cap = (int64_t)num_sms() * 3;
+  const int64_t cap = (int64_t)num_sms() * env_int("OFSC_SPMM_CTAS_PER_SM", 3);
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
@@ -128,14 +135,15 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   (void)cid;
   (void)cstart;
   const int nb = spmm_grid(n_local);
+  const int ch = env_int("OFSC_SPMM_CHUNK", kSpmmChunk);   // rows per work grab (tuning knob)
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
   OFSC_DISPATCH_KP(KP, {
     if (dt == OFSC_F64)
       k_spmm<double, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                   (const double*)Zg, (double*)Y, stop, ctr);
+                                                   (const double*)Zg, (double*)Y, stop, ctr, ch);
     else
       k_spmm<float, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                  (const float*)Zg, (float*)Y, stop, ctr);
+                                                  (const float*)Zg, (float*)Y, stop, ctr, ch);
   });
   OFSC_LAUNCH_CHECK();
 }
