@@ -573,7 +573,7 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   OFSC_CUDA(cudaMalloc(&w.grams, (size_t)4 * KP * KP * 8));
   OFSC_CUDA(cudaMalloc(&w.state, (size_t)(2 * KP * KP + 5 * KP) * 8));
   OFSC_CUDA(cudaMalloc(&w.ctl, sizeof(DevCtl)));
-  OFSC_CUDA(cudaMalloc(&w.ctr, sizeof(unsigned long long)));
+  OFSC_CUDA(cudaMalloc(&w.ctr, 4 * sizeof(unsigned long long)));  // one per SpMM column pass
   w.dt = dt;
   w.KP = KP;
   w.have = true;

@@ -17,26 +17,75 @@
 
 namespace ofsc {
 
-// C2a: Y = A Z.  A group of LPR = KP/4 lanes owns a row (each lane 4 consecutive
-// columns = two 16-byte loads per neighbour), RPW = 32/LPR rows per warp; no
-// shared memory and no barriers, so warps stream independently and the register
-// file holds only accumulators and in-flight neighbour rows (8 per row).
-template <typename T, int KP>
+// C2a: Y = A Z on the column window [c0, c0 + CW) (CW = KP: one pass; CW < KP:
+// KP/CW passes, each gathering CW-column row segments, so the gathered working
+// set of a community is CW/KP of its rows' bytes and stays L2-resident).
+// A group of LPR = CW/4 lanes owns a row (each lane 4 consecutive columns = two
+// 16-byte loads per neighbour), RPW = 32/LPR rows per warp; no shared memory and
+// no barriers, so warps stream independently and the register file holds only
+// accumulators and in-flight neighbour rows (8 per row).
+// L2 eviction-priority hints (HINT = 1, reordered graphs): the column ids,
+// the output rows and neighbour rows outside the row's community are loaded /
+// stored evict_first, so the current community's rows (reused ~15 times while
+// its rows are processed) keep the L2.
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ldg2h(const double* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float2 ldg2h(const float* p, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ldg1h(const int32_t* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg2h(double* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol));
+}
+__device__ __forceinline__ void stg2h(float* p, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y),
+               "l"(pol));
+}
+
+template <typename T, int KP, int CW, int HINT>
 __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
-       const int* stop, unsigned long long* __restrict__ ctr, int ch) {
+       const int* stop, unsigned long long* __restrict__ ctr, int ch, int c0,
+       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart) {
   if (stop && *stop) return;
+  uint64_t pf = 0, pn = 0;
+  if constexpr (HINT) {
+    pf = pol_evict_first();
+    pn = pol_evict_normal();
+  }
   using V2 = typename Vec2<T>::type;
-  constexpr int LPR = KP / 4;
+  constexpr int LPR = CW / 4;
   constexpr int RPW = 32 / LPR;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR, l = lane % LPR;
   const bool active = sub < RPW;                // KP = 48: lanes 24..31 idle
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const T* zc = Zg + 4 * l;
+  const T* zc = Zg + c0 + 4 * l;
   // Rows are handed out in order in chunks of kSpmmChunk from a global counter
   // (ctr != NULL), so all warps work on a narrow, advancing window of rows and
   // the neighbour rows of the current (reordered) community stay in L2;
@@ -59,19 +108,35 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     const int64_t i = base + q + sub;
     if (!active || i >= n_local) continue;
     const int64_t beg = row_ptr[i], end = row_ptr[i + 1];
+    int lo = 0, hi = 0;                            // community row range of row i (HINT)
+    if constexpr (HINT) {
+      const int ci = cid[i];
+      lo = (int)cstart[ci];
+      hi = (int)cstart[ci + 1];
+    }
     T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     int64_t e = beg;
     for (; e + 8 <= end; e += 8) {
       int c[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = __ldg(col + e + u);
+      for (int u = 0; u < 8; ++u) {
+        if constexpr (HINT) c[u] = ldg1h(col + e + u, pf);
+        else c[u] = __ldg(col + e + u);
+      }
       V2 z0[8], z1[8];
       T sv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const V2* zr = reinterpret_cast<const V2*>(zc + (int64_t)c[u] * KP);
-        z0[u] = __ldg(zr);
-        z1[u] = __ldg(zr + 1);
+        if constexpr (HINT) {
+          const T* zr = zc + (int64_t)c[u] * KP;
+          const uint64_t pol = (c[u] >= lo && c[u] < hi) ? pn : pf;
+          z0[u] = ldg2h(zr, pol);
+          z1[u] = ldg2h(zr + 2, pol);
+        } else {
+          const V2* zr = reinterpret_cast<const V2*>(zc + (int64_t)c[u] * KP);
+          z0[u] = __ldg(zr);
+          z1[u] = __ldg(zr + 1);
+        }
         if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
         else sv[u] = (T)__ldg(s32 + c[u]);
       }
@@ -95,7 +160,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       a2 = fma(sv, z1.x, a2);
       a3 = fma(sv, z1.y, a3);
     }
-    const V2* zo = reinterpret_cast<const V2*>(Zg + (own_off + i) * KP + 4 * l);
+    const V2* zo = reinterpret_cast<const V2*>(Zg + (own_off + i) * KP + c0 + 4 * l);
     const V2 o0 = zo[0], o1 = zo[1];
     T si;
     if constexpr (sizeof(T) == 8) si = (T)s[own_off + i];
@@ -105,9 +170,14 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     y0.y = -o0.y - si * a1;
     y1.x = -o1.x - si * a2;
     y1.y = -o1.y - si * a3;
-    V2* yr = reinterpret_cast<V2*>(Y + i * KP + 4 * l);
-    yr[0] = y0;
-    yr[1] = y1;
+    if constexpr (HINT) {
+      stg2h(Y + i * KP + c0 + 4 * l, y0, pf);
+      stg2h(Y + i * KP + c0 + 4 * l + 2, y1, pf);
+    } else {
+      V2* yr = reinterpret_cast<V2*>(Y + i * KP + c0 + 4 * l);
+      yr[0] = y0;
+      yr[1] = y1;
+    }
     }
   }
 }
@@ -116,6 +186,9 @@ static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return (e && *e) ? atoi(e) : dflt;
 }
+
+// Default column window of the SpMM passes (see k_spmm).
+int spmm_col_window(ofsc_dtype, int KP) { return KP; }
 
 int spmm_grid(int64_t n_local) {  // resident CTAs (3 per SM) for the chunked schedule
   const int64_t warps = (n_local + 1) / 2;
@@ -128,24 +201,36 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart,
                  unsigned long long* ctr) {
-  // cid / cstart: community layout of reordered graphs.  L2 eviction-priority
-  // hints keyed on it (evict_last / evict_normal in-community, evict_first
-  // otherwise) were measured slower (12.3 and 8.0 ms vs 7.7 ms at c4,
-  // profiles/r01/SUMMARY), so the gathers use the default policy.
-  (void)cid;
-  (void)cstart;
+  // cid / cstart: community layout of reordered graphs (p == 1), for the L2 hints.
+  const int hint = (cid && cstart && own_off == 0) ? env_int("OFSC_SPMM_HINT", 0) : 0;
   const int nb = spmm_grid(n_local);
   const int ch = env_int("OFSC_SPMM_CHUNK", kSpmmChunk);   // rows per work grab (tuning knob)
-  if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
-  OFSC_DISPATCH_KP(KP, {
-    if (dt == OFSC_F64)
-      k_spmm<double, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                   (const double*)Zg, (double*)Y, stop, ctr, ch);
-    else
-      k_spmm<float, KPC><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,
-                                                  (const float*)Zg, (float*)Y, stop, ctr, ch);
-  });
-  OFSC_LAUNCH_CHECK();
+  int cw = env_int("OFSC_SPMM_CW", spmm_col_window(dt, KP));  // columns per pass (tuning knob)
+  if (cw != 16 && cw != 32) cw = KP;
+  if (KP % cw) cw = KP;
+  const int passes = KP / cw;
+  if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
+  for (int ps = 0; ps < passes; ++ps) {
+    unsigned long long* c = ctr ? ctr + ps : nullptr;
+    const int c0 = ps * cw;
+#define OFSC_SPMM_LAUNCH_H(CWC, H)                                                              \
+    if (dt == OFSC_F64)                                                                         \
+      k_spmm<double, KPC, CWC, H><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32, \
+          (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart);                         \
+    else                                                                                        \
+      k_spmm<float, KPC, CWC, H><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,  \
+          (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart);
+#define OFSC_SPMM_LAUNCH(CWC) \
+    if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
+    OFSC_DISPATCH_KP(KP, {
+      if (cw == KPC) { OFSC_SPMM_LAUNCH(KPC) }
+      else if (cw == 32) { if constexpr (KPC % 32 == 0) { OFSC_SPMM_LAUNCH(32) } }
+      else { if constexpr (KPC % 16 == 0) { OFSC_SPMM_LAUNCH(16) } }
+    });
+#undef OFSC_SPMM_LAUNCH
+#undef OFSC_SPMM_LAUNCH_H
+    OFSC_LAUNCH_CHECK();
+  }
 }
 
 void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
