@@ -1005,8 +1005,10 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                  "ofsc_kmeans needs an NCCL communicator when p > 1");
     cudaStream_t s = (cudaStream_t)stream;
     const int K = n_clusters;
-    const int nb = kmeans_blocks(std::max<int64_t>(n_local, 1));
-    const int nbp = kmeans_partial_blocks(std::max<int64_t>(n_local, 1));
+    const bool fused = kmeans_step_supported(dim, K);   // assign + partial sums in one pass
+    const int nb = fused ? kmeans_step_blocks(std::max<int64_t>(n_local, 1))
+                         : kmeans_blocks(std::max<int64_t>(n_local, 1));
+    const int nbp = fused ? nb : kmeans_partial_blocks(std::max<int64_t>(n_local, 1));
     const int W = dim + 1;
     DBuf chg(8, s), pin((size_t)nb * 8, s), part((size_t)nbp * K * W * 8, s),
         red((size_t)K * W * 8, s), tot(8, s);
@@ -1022,7 +1024,10 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
     for (it = 1; it <= max_iters; ++it) {
       OFSC_CUDA(cudaMemsetAsync(chg.p, 0, 8, s));
       OFSC_CUDA(cudaMemsetAsync(pin.p, 0, (size_t)nb * 8, s));
-      if (n_local > 0)
+      if (n_local > 0 && fused)
+        launch_kmeans_step(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
+                           chg.as<unsigned long long>(), pin.as<double>(), part.as<double>(), nb, s);
+      else if (n_local > 0)
         launch_kmeans_assign(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
                              chg.as<unsigned long long>(), pin.as<double>(), nb, s);
       launch_reduce_partials(pin.as<double>(), nb, 1, tot.as<double>(), s);
@@ -1034,9 +1039,9 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
       OFSC_CUDA(cudaMemcpyAsync(&inertia, tot.p, 8, cudaMemcpyDeviceToHost, s));
       OFSC_CUDA(cudaStreamSynchronize(s));
       if (it > 1 && *h_chg == 0) break;
-      if (n_local > 0)
+      if (n_local > 0 && !fused)
         launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nbp, s);
-      else
+      else if (n_local == 0)
         OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nbp * K * W * 8, s));
       launch_reduce_partials(part.as<double>(), nbp, K * W, red.as<double>(), s);
       if (comm && comm->nranks > 1)

@@ -156,6 +156,12 @@ void launch_kmeans_partial(ofsc_dtype dt, int64_t n, int dim, const void* Y, int
                            const int* labels, double* part, int nblk, cudaStream_t st);
 void launch_kmeans_finish(int K, int dim, const double* red, double* C, cudaStream_t st);
 int kmeans_blocks(int64_t n);
+// Fused Lloyd step (assign + per-CTA partial sums, part[nblk][K][dim + 1]); dim <= 64, K <= 128.
+bool kmeans_step_supported(int dim, int K);
+int kmeans_step_blocks(int64_t n);
+void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                        const double* C, int* labels, unsigned long long* changes,
+                        double* part_inertia, double* part, int nblk, cudaStream_t st);
 int kmeans_partial_blocks(int64_t n);
 
 // graph build (graph_build.cu)

@@ -366,6 +366,317 @@ void launch_kmeans_assign(ofsc_dtype dt, int64_t n, int dim, const void* Y, int6
                            nblk, smem, st);
 }
 
+// ---------------------------------------------------------------------------
+// Fused Lloyd step (dim <= 64, K <= 128): assignment + per-CTA partial sums in
+// one pass over Y.  A CTA walks 32-row tiles (static stride, so the summation
+// order is fixed); the tile is staged in padded smem (next tile prefetched into
+// registers).  Warp w owns centroid blocks w (and w + 8):
+//   assign: its DMMA B fragments (C^T, DP/4 k-steps) stay in registers; the 4
+//           row blocks of the tile are 4 independent accumulation chains;
+//           scores ||c||^2 - 2 y.c; best / runner-up merged across lanes and
+//           warps (8 threads per row, butterfly; the merge is the lexicographic
+//           (score, index) minimum, so ties go to the lowest index); the same
+//           exactness guard as k_kmeans_assign_mma (direct form in d order when
+//           the margin is below tau);
+//   sums:   S[c][d] += sum_r [label_r = c] Y[r][d] on DMMA with the one-hot
+//           matrix as the A operand (products are exact, accumulation order is
+//           fixed by the tiling -> deterministic); accumulators stay in
+//           registers across tiles; a warp skips k-steps whose 4 rows carry
+//           none of its centroids.  Counts: integer smem atomics (exact).
+// part[b] = (sums, count) per centroid feeds the fixed-order reduction.
+// ---------------------------------------------------------------------------
+constexpr int kKsRows = 32;
+
+template <typename T, int NBW, int DP>
+__global__ void __launch_bounds__(kKmThreads, NBW == 1 ? 2 : 1)
+k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
+              const double* __restrict__ C, int* __restrict__ labels,
+              unsigned long long* changes, double* part_inertia, double* part) {
+  // DP: dim rounded up to a multiple of 16 (padding columns are zero)
+  constexpr int TR = kKsRows;
+  constexpr int PRE = TR * DP / kKmThreads;       // prefetched doubles per thread
+  constexpr int LDY = DP + 4;
+  extern __shared__ double sm[];
+  const int W = dim + 1;
+  const int KB = (K + 7) / 8;
+  double* Ys = sm;                                 // [TR][LDY]
+  double* cn = Ys + TR * LDY;                      // [64 * NBW] ||c||^2 (inf for padding)
+  double* mb1 = cn + 64 * NBW;                     // [TR][8 warps]
+  double* mb2 = mb1 + 8 * TR;
+  int* mc1 = (int*)(mb2 + 8 * TR);                 // [TR][8 warps]
+  int* tl = mc1 + 8 * TR;                          // [TR] tile labels (-1: padding row)
+  int* cnt = tl + TR;                              // [64 * NBW]
+  __shared__ double s_in[kKmThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int c = tid; c < 64 * NBW; c += kKmThreads) {
+    double a = 0.0;
+    if (c < K)
+      for (int d = 0; d < dim; ++d) a = a + C[c * dim + d] * C[c * dim + d];
+    cn[c] = c < K ? a : CUDART_INF;
+    cnt[c] = 0;
+  }
+  // register-resident B fragments: B[k = d][n = c] = C[c][d], d = 4 kk + tig, c = cb*8 + gid
+  double bf[NBW][DP / 4];
+#pragma unroll
+  for (int q = 0; q < NBW; ++q) {
+    const int c = (warp + 8 * q) * 8 + gid;
+#pragma unroll
+    for (int kk = 0; kk < DP / 4; ++kk) {
+      const int d = 4 * kk + tig;
+      bf[q][kk] = (c < K && d < dim) ? C[c * dim + d] : 0.0;
+    }
+  }
+  double sacc[NBW][DP / 8][2];                     // sums S[cb*8 + gid][db*8 + 2 tig + h]
+#pragma unroll
+  for (int q = 0; q < NBW; ++q)
+#pragma unroll
+    for (int db = 0; db < DP / 8; ++db) sacc[q][db][0] = sacc[q][db][1] = 0.0;
+  const int64_t ntiles = (n + TR - 1) / TR;
+  double pre[PRE];
+  int old_pre = 0;                                 // previous label of row (tid >> 3), w == 0 lanes
+  auto fetch = [&](int64_t tile) {
+    const int64_t r0 = tile * TR;
+#pragma unroll
+    for (int j = 0; j < PRE; ++j) {
+      const int e = tid + kKmThreads * j;         // e < TR * DP
+      const int q = e / DP, d = e % DP;
+      pre[j] = (d < dim && r0 + q < n) ? ld1(Y + (r0 + q) * ldy + d) : 0.0;
+    }
+    if ((tid & 7) == 0 && r0 + (tid >> 3) < n) old_pre = labels[r0 + (tid >> 3)];
+  };
+  if ((int64_t)blockIdx.x < ntiles) fetch(blockIdx.x);
+  double inertia = 0.0;
+  unsigned long long nchg = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TR;
+    const int rows = (int)imin64(TR, n - r0);
+    __syncthreads();                               // previous tile fully consumed
+#pragma unroll
+    for (int j = 0; j < PRE; ++j) {
+      const int e = tid + kKmThreads * j;
+      Ys[(e / DP) * LDY + e % DP] = pre[j];
+    }
+    const int old_lab = old_pre;
+    __syncthreads();
+    if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
+    // ---- assign: this warp's centroid blocks x the 4 row blocks
+    double b1[TR / 8], b2[TR / 8];
+    int c1[TR / 8];
+#pragma unroll
+    for (int rb = 0; rb < TR / 8; ++rb) {
+      b1[rb] = CUDART_INF;
+      b2[rb] = CUDART_INF;
+      c1[rb] = 0x7fffffff;
+    }
+#pragma unroll
+    for (int q = 0; q < NBW; ++q) {
+      const int cb = warp + 8 * q;
+      if (cb < KB) {
+        double a[TR / 8][2];
+#pragma unroll
+        for (int rb = 0; rb < TR / 8; ++rb) a[rb][0] = a[rb][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < DP / 4; ++kk)
+#pragma unroll
+            for (int rb = 0; rb < TR / 8; ++rb)
+              dmma(a[rb][0], a[rb][1], Ys[(rb * 8 + gid) * LDY + 4 * kk + tig], bf[q][kk]);
+#pragma unroll
+        for (int rb = 0; rb < TR / 8; ++rb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = cb * 8 + 2 * tig + h;
+            const double sc = cn[c] - 2.0 * a[rb][h];
+            if (sc < b1[rb] || (sc == b1[rb] && c < c1[rb])) {
+              b2[rb] = b1[rb];
+              b1[rb] = sc;
+              c1[rb] = c;
+            } else if (sc < b2[rb]) {
+              b2[rb] = sc;
+            }
+          }
+      }
+    }
+#pragma unroll
+    for (int rb = 0; rb < TR / 8; ++rb) {
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {           // merge the 4 lanes of the row
+        const double ob1 = __shfl_xor_sync(0xffffffffu, b1[rb], o);
+        const double ob2 = __shfl_xor_sync(0xffffffffu, b2[rb], o);
+        const int oc1 = __shfl_xor_sync(0xffffffffu, c1[rb], o);
+        if (ob1 < b1[rb] || (ob1 == b1[rb] && oc1 < c1[rb])) {
+          b2[rb] = fmin(b1[rb], ob2);
+          b1[rb] = ob1;
+          c1[rb] = oc1;
+        } else {
+          b2[rb] = fmin(b2[rb], ob1);
+        }
+      }
+      if (tig == 0) {
+        const int r = rb * 8 + gid;
+        mb1[r * 8 + warp] = b1[rb];
+        mb2[r * 8 + warp] = b2[rb];
+        mc1[r * 8 + warp] = c1[rb];
+      }
+    }
+    __syncthreads();
+    {
+      // merge across warps: 8 threads per row (thread = (row, warp slot))
+      const int r = tid >> 3, w = tid & 7;
+      double x1 = mb1[r * 8 + w], x2 = mb2[r * 8 + w];
+      int xc = mc1[r * 8 + w];
+      double yn = 0.0;                             // ||y||^2: 8 partial sums, butterfly
+      for (int d = w; d < dim; d += 8) yn = fma(Ys[r * LDY + d], Ys[r * LDY + d], yn);
+#pragma unroll
+      for (int o = 1; o <= 4; o <<= 1) {
+        const double ob1 = __shfl_xor_sync(0xffffffffu, x1, o);
+        const double ob2 = __shfl_xor_sync(0xffffffffu, x2, o);
+        const int oc1 = __shfl_xor_sync(0xffffffffu, xc, o);
+        if (ob1 < x1 || (ob1 == x1 && oc1 < xc)) {
+          x2 = fmin(x1, ob2);
+          x1 = ob1;
+          xc = oc1;
+        } else {
+          x2 = fmin(x2, ob1);
+        }
+        yn += __shfl_xor_sync(0xffffffffu, yn, o);
+      }
+      int lab = xc;
+      double dist = yn + x1;
+      if (!(x2 - x1 > 1e-12 * (1.0 + yn))) {       // direct form, exactly as the oracle
+        double best = CUDART_INF;                  // centroids c = w, w + 8, ... then merged
+        int bc = 0x7fffffff;
+        for (int c = w; c < K; c += 8) {
+          double a = 0.0;
+          for (int d = 0; d < dim; ++d) {
+            const double diff = Ys[r * LDY + d] - C[c * dim + d];
+            a = a + diff * diff;
+          }
+          if (a < best) {                          // c increases: lowest index wins ties
+            best = a;
+            bc = c;
+          }
+        }
+        const unsigned gmask = 0xffu << (lane & 24);   // the row's 8 lanes (all take this branch)
+#pragma unroll
+        for (int o = 1; o <= 4; o <<= 1) {
+          const double ob = __shfl_xor_sync(gmask, best, o);
+          const int oc = __shfl_xor_sync(gmask, bc, o);
+          if (ob < best || (ob == best && oc < bc)) {
+            best = ob;
+            bc = oc;
+          }
+        }
+        lab = bc;
+        dist = best;
+      }
+      if (w == 0) {
+        tl[r] = r < rows ? lab : -1;
+        if (r < rows) {
+          if (old_lab != lab) ++nchg;
+          labels[r0 + r] = lab;
+          inertia += dist;
+          atomicAdd(&cnt[lab], 1);                 // integer: exact
+        }
+      }
+    }
+    __syncthreads();
+    // ---- sums on DMMA: S(cb block x d) += onehot(cb block x 4 rows) Y(4 rows x d)
+#pragma unroll
+    for (int q = 0; q < NBW; ++q) {
+      const int cb = warp + 8 * q;
+      if (cb < KB) {
+        const int cl = cb * 8;
+#pragma unroll
+        for (int k0 = 0; k0 < TR; k0 += 4) {
+          const int l4 = tl[k0 + tig];
+          const bool any = __any_sync(0xffffffffu, l4 >= cl && l4 < cl + 8);
+          if (!any) continue;
+          const double a = (l4 == cl + gid) ? 1.0 : 0.0;
+          const double* yb = Ys + (k0 + tig) * LDY + gid;
+#pragma unroll
+          for (int db = 0; db < DP / 8; ++db) dmma(sacc[q][db][0], sacc[q][db][1], a, yb[db * 8]);
+        }
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    inertia += __shfl_xor_sync(0xffffffffu, inertia, o);
+    nchg += __shfl_xor_sync(0xffffffffu, nchg, o);
+  }
+  if (lane == 0) {
+    s_in[warp] = inertia;
+    if (nchg) atomicAdd(changes, nchg);            // integer: order-independent
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0;
+    for (int w = 0; w < kKmThreads / 32; ++w) a += s_in[w];
+    part_inertia[blockIdx.x] = a;
+  }
+  double* pb = part + (int64_t)blockIdx.x * K * W;
+#pragma unroll
+  for (int q = 0; q < NBW; ++q) {
+    const int c = (warp + 8 * q) * 8 + gid;
+    if (c < K) {
+#pragma unroll
+      for (int db = 0; db < DP / 8; ++db)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int d = db * 8 + 2 * tig + h;
+          if (d < dim) pb[c * W + d] = sacc[q][db][h];
+        }
+    }
+  }
+  for (int c = tid; c < K; c += kKmThreads) pb[c * W + dim] = (double)cnt[c];
+}
+
+size_t kmeans_step_smem(int dim, int K) {
+  const int DP = (dim + 15) & ~15;
+  const int nbw = K > 64 ? 2 : 1;
+  return ((size_t)kKsRows * (DP + 4) + 64 * nbw + 16 * kKsRows) * 8 +
+         ((size_t)9 * kKsRows + 64 * nbw) * 4;
+}
+
+bool kmeans_step_supported(int dim, int K) {
+  return dim <= 64 && K <= 128 && kmeans_step_smem(dim, K) <= 100 * 1024 &&
+         getenv("OFSC_KMEANS_DIRECT") == nullptr && getenv("OFSC_KMEANS_UNFUSED") == nullptr;
+}
+
+int kmeans_step_blocks(int64_t n) {
+  const int64_t tiles = (n + kKsRows - 1) / kKsRows;
+  const int64_t cap = (int64_t)num_sms() * 2;
+  return (int)(tiles < 1 ? 1 : (tiles > cap ? cap : tiles));
+}
+
+void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                        const double* C, int* labels, unsigned long long* changes,
+                        double* part_inertia, double* part, int nblk, cudaStream_t st) {
+  const size_t smem = kmeans_step_smem(dim, K);
+#define OFSC_KS3(TT, NB, DPC)                                                                    \
+  {                                                                                              \
+    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_step<TT, NB, DPC>,                                   \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+    k_kmeans_step<TT, NB, DPC><<<nblk, kKmThreads, smem, st>>>(n, dim, (const TT*)Y, ldy, K, C,  \
+                                                               labels, changes, part_inertia, part); \
+  }
+#define OFSC_KS(TT, NB)                                                                          \
+  switch ((dim + 15) / 16) {                                                                     \
+    case 1: OFSC_KS3(TT, NB, 16) break;                                                          \
+    case 2: OFSC_KS3(TT, NB, 32) break;                                                          \
+    case 3: OFSC_KS3(TT, NB, 48) break;                                                          \
+    default: OFSC_KS3(TT, NB, 64) break;                                                         \
+  }
+  if (dt == OFSC_F64) {
+    if (K > 64) OFSC_KS(double, 2) else OFSC_KS(double, 1)
+  } else {
+    if (K > 64) OFSC_KS(float, 2) else OFSC_KS(float, 1)
+  }
+#undef OFSC_KS
+#undef OFSC_KS3
+  OFSC_LAUNCH_CHECK();
+}
+
 // Partial cluster sums of a contiguous row range: part[b][c][0..dim-1] = sums,
 // part[b][c][dim] = count.  Thread d < dim owns column d; rows in order.
 template <typename T>

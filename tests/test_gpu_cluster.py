@@ -72,6 +72,51 @@ def test_kmeans_first_assignment_bit_exact():
     assert abs(ing - ino) <= 1e-12 * ino
 
 
+@pytest.mark.parametrize("n,dim,K", [(3001, 3, 1), (3001, 17, 5), (4099, 64, 64), (2053, 48, 100),
+                                     (37, 11, 11)])
+def test_kmeans_fused_step_shapes(n, dim, K):
+    """The fused Lloyd step (assign + partial sums) across tile widths, centroid
+    counts (one and two centroid blocks per warp) and ragged row counts: first
+    assignment bit-exact, full run within the near-tie rule, centroids 1e-13."""
+    rng = np.random.default_rng(n + dim + K)
+    Y = row_normalize(rng.standard_normal((n, dim)))
+    C0 = Y[rng.choice(n, K, replace=False)].copy()
+    lo, _, _, ino = kmeans_lloyd(Y, C0, max_iters=1)
+    lg, _, ing = ofsc.kmeans(torch.from_numpy(Y).cuda(), torch.from_numpy(C0.copy()).cuda(), max_iters=1)
+    assert np.array_equal(lg.cpu().numpy(), lo)
+    assert abs(ing - ino) <= 1e-12 * max(ino, 1e-300)
+    lo, Co, ito, ino = kmeans_lloyd(Y, C0, max_iters=30)
+    C = torch.from_numpy(C0.copy()).cuda()
+    lg, itg, ing = ofsc.kmeans(torch.from_numpy(Y).cuda(), C, max_iters=30)
+    assert np.array_equal(lg.cpu().numpy(), lo) and itg == ito
+    assert np.allclose(C.cpu().numpy(), Co, atol=1e-13, rtol=0)
+
+
+def test_kmeans_exact_ties_lowest_index():
+    """Duplicated centroids tie exactly: the lowest index wins (R20)."""
+    rng = np.random.default_rng(11)
+    Y = row_normalize(rng.standard_normal((1000, 8)))
+    C0 = np.concatenate([Y[:4], Y[:4]])            # centroids 4..7 duplicate 0..3
+    l1, _ = ofsc.kmeans(torch.from_numpy(Y).cuda(), torch.from_numpy(C0.copy()).cuda(), max_iters=1)[:2]
+    assert l1.cpu().numpy().max() <= 3             # first assignment: every row ties 0..3 with 4..7
+    lo, Co, ito, _ = kmeans_lloyd(Y, C0, max_iters=20)
+    C = torch.from_numpy(C0.copy()).cuda()
+    lg, itg, _ = ofsc.kmeans(torch.from_numpy(Y).cuda(), C, max_iters=20)
+    assert np.array_equal(lg.cpu().numpy(), lo) and itg == ito
+    assert np.allclose(C.cpu().numpy(), Co, atol=1e-13, rtol=0)
+
+
+def test_kmeans_f32_features():
+    rng = np.random.default_rng(5)
+    Y = row_normalize(rng.standard_normal((3000, 32))).astype(np.float32)
+    C0 = Y[:16].astype(np.float64)
+    lo, Co, ito, _ = kmeans_lloyd(Y.astype(np.float64), C0, max_iters=30)
+    C = torch.from_numpy(C0.copy()).cuda()
+    lg, itg, _ = ofsc.kmeans(torch.from_numpy(Y).cuda(), C, max_iters=30)
+    assert np.array_equal(lg.cpu().numpy(), lo) and itg == ito
+    assert np.allclose(C.cpu().numpy(), Co, atol=1e-13, rtol=0)
+
+
 def test_scores_match_oracle():
     rng = np.random.default_rng(0)
     for _ in range(10):
