@@ -280,16 +280,22 @@ def run_ours(args):
             return out_, a.elapsed_time(b)
         X = X0d.clone()
         _, ms_run = timed(lambda: ofsc.run(g, args.method, X, cfg.iters, refresh=args.refresh))
-        Y, ms_norm = timed(lambda: ofsc.row_normalize(X))
+        Y = torch.empty_like(X)
+        _, ms_norm = timed(lambda: ofsc.row_normalize(X, Y))
         rows = torch.from_numpy(kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)).cuda()
-        C0 = Y[rows].contiguous()
+        C0 = Y[rows].double().contiguous()
         (lab, km_it, _), ms_km = timed(lambda: ofsc.kmeans(Y, C0, 100))
+        # NEXT-1: orthogonalisation + Rayleigh-Ritz + relerr on the features
+        ofsc.rayleigh_ritz(g, X, want_vectors=False)      # warm-up (workspace, kernels)
+        (theta, _, relerr), ms_rr = timed(lambda: ofsc.rayleigh_ritz(g, X, want_vectors=False))
         g0, ms_build_plain = timed(lambda: ofsc.Graph(cfg.n, src, dst, reorder=False))
         g0.close()
         out["pipeline_ms"] = {
             "graph_build": round(build_ms, 2), "graph_build_no_reorder": round(ms_build_plain, 2),
             f"run_{cfg.iters}_iters": round(ms_run, 2), "row_normalize": round(ms_norm, 3),
             "kmeans": round(ms_km, 2), "kmeans_lloyd_steps": km_it,
+            "rayleigh_ritz": round(ms_rr, 2), "relerr": float(relerr),
+            "ritz_values_min_max": [float(theta[0]), float(theta[-1])],
             "ari_vs_planted": round(ofsc.scores(lab.cpu().numpy(), labels)[0], 4)}
 
     # --- all four methods, same protocol ---

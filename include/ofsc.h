@@ -249,6 +249,23 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                         int32_t max_iters, int32_t* d_labels, int32_t* iters_out,
                         double* inertia_out, ofsc_stream stream);
 
+/* Orthogonalisation + Rayleigh-Ritz post-step and the relerr metric
+ * ("one SpMM, several dot products, and an eigendecomposition of a
+ * k x k matrix"; relerr = ||B U - U Lambda||_F / ||U Lambda||_F with
+ * B = L + 2I = A + 4I, R24-R26).
+ *   A X (one SpMM), M = X^T X, W = X^T A X; M = L L^T (Cholesky-QR, Q = X L^{-T});
+ *   H = L^{-1} ((W + W^T)/2) L^{-T} = Z Theta Z^T (k x k Jacobi on device);
+ *   U = X L^{-T} Z (Ritz vectors, orthonormal), A U = (A X) L^{-T} Z.
+ * d_X: local rows x ldx (original node order when p == 1), dtype dt, not modified.
+ * d_U: optional (NULL: not written) local rows x ldu, same order and dtype.
+ * h_theta: host [k], Ritz values of A ascending (those of B are theta + 4).
+ * h_relerr: optional host scalar.  Synchronizes the stream.
+ * Errors: OFSC_ERR_ARG (k < 1, k > min(n, OFSC_MAX_K), ld < k, null X/theta);
+ * OFSC_ERR_RANGE when X^T X is not positive definite (X rank deficient). */
+ofsc_status ofsc_rayleigh_ritz(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_X,
+                               int64_t ldx, void* d_U, int64_t ldu, double* h_theta,
+                               double* h_relerr, ofsc_stream stream);
+
 /* ARI and NMI (arithmetic-mean normalisation) of two host labelings. */
 ofsc_status ofsc_scores(int64_t n, const int32_t* h_a, const int32_t* h_b, double* ari,
                         double* nmi);

@@ -107,6 +107,7 @@ SIGNATURES = {
     "ofsc_row_normalize": (_ST, [_ST, _I64, _I32, _P, _I64, _P, _I64, _P]),
     "ofsc_kmeans": (_ST, [_P, _ST, _I64, _I32, _P, _I64, _I32, _P, _I32, _P, _P, _P, _P]),
     "ofsc_scores": (_ST, [_I64, _P, _P, _P, _P]),
+    "ofsc_rayleigh_ritz": (_ST, [_P, _ST, _I32, _P, _I64, _P, _I64, _P, _P, _P]),
     "ofsc_spectral_cluster": (_ST, [_P, _I64, _I64, _P, _P, _ST, _ST, C.POINTER(Opts),
                                     C.POINTER(BuildOpts), _P, _I32, _P, _I32, _P,
                                     C.POINTER(Report), _P]),
@@ -419,6 +420,24 @@ def kmeans(Y, centroids, max_iters=100, comm: Comm | None = None, stream=None):
                              C.c_void_p(labels.data_ptr()), C.byref(it), C.byref(inertia),
                              _stream(stream)))
     return labels, it.value, inertia.value
+
+
+def rayleigh_ritz(graph, X, want_vectors=True, stream=None):
+    """Orthogonalisation + Rayleigh-Ritz on span(X) and relerr (ofsc_rayleigh_ritz;
+    P:589).  X: local rows x k CUDA tensor (fp64 or fp32), not modified.
+    Returns (theta float64[k] ascending (numpy), U (same shape/dtype as X) or None, relerr)."""
+    torch = _torch()
+    X = _dev2d(X)
+    k = X.shape[1]
+    U = torch.empty_like(X) if want_vectors else None
+    theta = np.zeros(k, dtype=np.float64)
+    rel = C.c_double()
+    _check(lib().ofsc_rayleigh_ritz(graph.handle, _dt_of(X), k, C.c_void_p(X.data_ptr()),
+                                    X.stride(0), C.c_void_p(U.data_ptr()) if U is not None else None,
+                                    U.stride(0) if U is not None else k,
+                                    theta.ctypes.data_as(C.c_void_p), C.byref(rel),
+                                    _stream(stream)))
+    return theta, U, rel.value
 
 
 def scores(a, b):

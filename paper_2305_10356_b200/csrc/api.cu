@@ -1054,6 +1054,56 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
   });
 }
 
+ofsc_status ofsc_rayleigh_ritz(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_X,
+                               int64_t ldx, void* d_U, int64_t ldu, double* h_theta,
+                               double* h_relerr, ofsc_stream stream) {
+  return guard([&] {
+    OFSC_REQUIRE(g && d_X && h_theta, OFSC_ERR_ARG, "null argument");
+    OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
+    OFSC_REQUIRE(k >= 1 && k <= OFSC_MAX_K && k <= g->n, OFSC_ERR_ARG,
+                 "need 1 <= k <= min(n, 64)");
+    OFSC_REQUIRE(ldx >= k && (!d_U || ldu >= k), OFSC_ERR_ARG, "bad ldx / ldu");
+    OFSC_REQUIRE(g->p == 1 || g->comm->nccl, OFSC_ERR_STATE,
+                 "ofsc_rayleigh_ritz needs an NCCL communicator when p > 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int KP = padded_k(k);
+    ensure_workspace(g, dt, KP, s);
+    Workspace& w = g->ws;
+    ofsc_opts o{};
+    o.k = k;
+    IterParams p = make_params(g, OFSC_OFM_F2, o, KP);
+    launch_copy_in(dt, k, KP, g->n_local, d_X, ldx, w.X, g->user_perm(), s);
+    OFSC_CUDA(cudaMemsetAsync(w.ctl, 0, sizeof(DevCtl), s));
+    {
+      Prof pr;
+      refresh_ops(g, dt, p, s, pr);   // A X, M = X^T X, W = X^T A X (reduced over ranks)
+    }
+    const int nb = rr_rows_blocks(std::max<int64_t>(g->n_local, 1));
+    DBuf tm((size_t)KP * KP * 8, s), th((size_t)KP * 8, s), stt(8, s), part((size_t)nb * 2 * 8, s),
+        red(2 * 8, s);
+    launch_rr_small(p.M, p.W, KP, k, tm.as<double>(), th.as<double>(), stt.as<int>(), s);
+    int bad = 0;
+    OFSC_CUDA(cudaMemcpyAsync(&bad, stt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    OFSC_REQUIRE(!bad, OFSC_ERR_RANGE, "X^T X is not positive definite (X rank deficient)");
+    if (g->n_local > 0)
+      launch_rr_rows(dt, g->n_local, k, KP, w.X, w.AX, tm.as<double>(), th.as<double>(), w.G,
+                     part.as<double>(), nb, s);
+    else
+      OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nb * 2 * 8, s));
+    launch_reduce_partials(part.as<double>(), nb, 2, red.as<double>(), s);
+    allreduce_d(g, red.as<double>(), 2, s);
+    if (d_U) launch_copy_out(dt, k, KP, g->n_local, w.G, d_U, ldu, g->user_perm(), s);
+    double hr[2];
+    std::vector<double> ht(KP);
+    OFSC_CUDA(cudaMemcpyAsync(hr, red.p, 2 * 8, cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaMemcpyAsync(ht.data(), th.p, (size_t)KP * 8, cudaMemcpyDeviceToHost, s));
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    for (int j = 0; j < k; ++j) h_theta[j] = ht[j];
+    if (h_relerr) *h_relerr = hr[1] > 0.0 ? std::sqrt(hr[0]) / std::sqrt(hr[1]) : 0.0;
+  });
+}
+
 ofsc_status ofsc_scores(int64_t n, const int32_t* a, const int32_t* b, double* ari, double* nmi) {
   return guard([&] {
     OFSC_REQUIRE(a && b && n >= 1, OFSC_ERR_ARG, "bad scores args");

@@ -139,6 +139,13 @@ void launch_linesearch(const IterParams& p, cudaStream_t st);
 // line-search hook: coefficients from given Grams (device), no ctl
 void launch_linesearch_hook(int method, int k, int KP, const double* grams, double* M, double* W,
                             double* alpha, int* codes, cudaStream_t st);
+// Rayleigh-Ritz post-step (kernels_rr.cu): k x k solve (1 CTA) and the row pass
+void launch_rr_small(const double* M, const double* W, int KP, int k, double* Tm, double* theta,
+                     int* status, cudaStream_t st);
+int rr_rows_blocks(int64_t n);
+void launch_rr_rows(ofsc_dtype dt, int64_t n, int k, int KP, const void* X, const void* AX,
+                    const double* Tm, const double* theta, void* U, double* part, int nblk,
+                    cudaStream_t st);
 // layout helpers
 // dst row r <- src row perm[r] (perm may be NULL: identity)
 void launch_copy_in(ofsc_dtype dt, int k, int KP, int64_t n, const void* src, int64_t lds,
