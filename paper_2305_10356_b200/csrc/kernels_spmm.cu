@@ -85,7 +85,11 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
   const bool active = sub < RPW;                // KP = 48: lanes 24..31 idle
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const T* zc = Zg + c0 + 4 * l;
+  // lane l of a row group owns columns {2l, 2l+1} and {CW/2 + 2l, CW/2 + 2l + 1}:
+  // each of the two 16-byte loads of a neighbour row then covers a contiguous
+  // half of the row segment (whole 32-byte sectors, no L1 re-reads)
+  constexpr int H2 = CW / 2;
+  const T* zc = Zg + c0 + 2 * l;
   // Rows are handed out in order in chunks of kSpmmChunk from a global counter
   // (ctr != NULL), so all warps work on a narrow, advancing window of rows and
   // the neighbour rows of the current (reordered) community stay in L2;
@@ -131,11 +135,11 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
           const T* zr = zc + (int64_t)c[u] * KP;
           const uint64_t pol = (c[u] >= lo && c[u] < hi) ? pn : pf;
           z0[u] = ldg2h(zr, pol);
-          z1[u] = ldg2h(zr + 2, pol);
+          z1[u] = ldg2h(zr + H2, pol);
         } else {
-          const V2* zr = reinterpret_cast<const V2*>(zc + (int64_t)c[u] * KP);
-          z0[u] = __ldg(zr);
-          z1[u] = __ldg(zr + 1);
+          const T* zr = zc + (int64_t)c[u] * KP;
+          z0[u] = __ldg(reinterpret_cast<const V2*>(zr));
+          z1[u] = __ldg(reinterpret_cast<const V2*>(zr + H2));
         }
         if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
         else sv[u] = (T)__ldg(s32 + c[u]);
@@ -150,8 +154,9 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     }
     for (; e < end; ++e) {
       const int c = __ldg(col + e);
-      const V2* zr = reinterpret_cast<const V2*>(zc + (int64_t)c * KP);
-      const V2 z0 = __ldg(zr), z1 = __ldg(zr + 1);
+      const T* zr = zc + (int64_t)c * KP;
+      const V2 z0 = __ldg(reinterpret_cast<const V2*>(zr));
+      const V2 z1 = __ldg(reinterpret_cast<const V2*>(zr + H2));
       T sv;
       if constexpr (sizeof(T) == 8) sv = (T)__ldg(s + c);
       else sv = (T)__ldg(s32 + c);
@@ -160,8 +165,8 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       a2 = fma(sv, z1.x, a2);
       a3 = fma(sv, z1.y, a3);
     }
-    const V2* zo = reinterpret_cast<const V2*>(Zg + (own_off + i) * KP + c0 + 4 * l);
-    const V2 o0 = zo[0], o1 = zo[1];
+    const T* zo = Zg + (own_off + i) * KP + c0 + 2 * l;
+    const V2 o0 = *reinterpret_cast<const V2*>(zo), o1 = *reinterpret_cast<const V2*>(zo + H2);
     T si;
     if constexpr (sizeof(T) == 8) si = (T)s[own_off + i];
     else si = s32[own_off + i];
@@ -171,12 +176,11 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     y1.x = -o1.x - si * a2;
     y1.y = -o1.y - si * a3;
     if constexpr (HINT) {
-      stg2h(Y + i * KP + c0 + 4 * l, y0, pf);
-      stg2h(Y + i * KP + c0 + 4 * l + 2, y1, pf);
+      stg2h(Y + i * KP + c0 + 2 * l, y0, pf);
+      stg2h(Y + i * KP + c0 + 2 * l + H2, y1, pf);
     } else {
-      V2* yr = reinterpret_cast<V2*>(Y + i * KP + c0 + 4 * l);
-      yr[0] = y0;
-      yr[1] = y1;
+      *reinterpret_cast<V2*>(Y + i * KP + c0 + 2 * l) = y0;
+      *reinterpret_cast<V2*>(Y + i * KP + c0 + 2 * l + H2) = y1;
     }
     }
   }
