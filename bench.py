@@ -156,6 +156,17 @@ def load_traffic():
     return None
 
 
+def load_gather_peak():
+    """Measured L2-resident random-row gather bandwidth (tools/l2_bw_probe.cu)."""
+    p = os.path.join(ROOT, "profiles", "measured_l2.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
 # ---------------------------------------------------------------------------
 def run_ours(args):
     import torch
@@ -234,13 +245,37 @@ def run_ours(args):
     achieved = algo[dom] / (avg_ms / 1e3) / 1e9
     traffic = load_traffic()
     tr_bytes = None
-    if traffic and traffic.get("config") == cfg.name and traffic.get("kernel") == dom:
-        tr_bytes = traffic.get("dram_bytes_per_launch")
+    if traffic and traffic.get("config") == cfg.name and world == 1 and args.dtype == "f64":
+        tr_bytes = (traffic.get("per_phase_dram_bytes") or {}).get(dom)
+        if tr_bytes is None and traffic.get("kernel") == dom:
+            tr_bytes = traffic.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                 "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                 "traffic": tr_bytes, "algorithmic_bytes_per_launch": algo[dom],
                 "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src,
                 "share_of_step": round(kern[dom]["ms_total"] / max(sum(v["ms_total"] for v in kern.values()), 1e-9), 3)}
+    # The SpMM's neighbour-row gathers are served by L2/L1 (tools/l2_bw_probe.cu):
+    # its second roofline is the measured L2 gather ceiling, with the bytes the
+    # SMs must receive (one KP-wide row per stored nonzero + own row + output).
+    gpk = load_gather_peak()
+    kp = 16 if k <= 16 else 32 if k <= 32 else 48 if k <= 48 else 64
+    gather_bytes = (info["nnz_local"] + 2 * nl) * kp * es
+    sp_ms = kern["spmm"]["ms_total"] / max(kern["spmm"]["launches"], 1)
+    roofline_l2 = None
+    if gpk:
+        ach = gather_bytes / (sp_ms / 1e3) / 1e9
+        roofline_l2 = {"bound": "l2", "kernel": "spmm", "achieved": round(ach, 1),
+                       "peak": gpk["l2_gather_gbs"], "unit": "GB/s",
+                       "frac": round(ach / gpk["l2_gather_gbs"], 4),
+                       "bytes_per_launch": gather_bytes, "avg_launch_ms": round(sp_ms, 4),
+                       "peak_source": gpk["source"]}
+    it_dram = None
+    if traffic and traffic.get("config") == cfg.name and world == 1 and args.dtype == "f64" \
+            and traffic.get("dram_bytes_per_iteration"):
+        tb = traffic["dram_bytes_per_iteration"]
+        it_dram = {"dram_bytes_per_iter": tb, "achieved_gbs": round(tb / (ms / K / 1e3) / 1e9, 1),
+                   "frac": round(tb / (ms / K / 1e3) / 1e9 / hbm_peak, 4),
+                   "source": traffic.get("source")}
     it_bytes = iteration_bytes(nl, info["nnz_local"], cfg.n, k, es)
     iter_hbm = it_bytes * value / 1e9 / max(world, 1) if world == 1 else it_bytes * (K / (ms / 1e3)) / 1e9
 
@@ -259,6 +294,8 @@ def run_ours(args):
                                                                   info["intra_edge_fraction"]))
                    if info["reordered"] else "none (random node ids)"},
         "roofline": roofline,
+        "roofline_l2_gather": roofline_l2,
+        "iteration_dram_ncu": it_dram,
         "iteration_hbm": {"algorithmic_bytes_per_iter_per_gpu": it_bytes,
                           "achieved_gbs_per_gpu": round(it_bytes * (K / (ms / 1e3)) / 1e9, 1),
                           "frac": round(it_bytes * (K / (ms / 1e3)) / 1e9 / hbm_peak, 4)},

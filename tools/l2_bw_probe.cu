@@ -86,7 +86,7 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       const double bytes = (double)nb * 256 / 16 * per * 512;
       printf("gather window %5zu MB, %d CTAs/SM: %.1f GB/s (%.2f ms for 51.2 GB)\n", mb, ctas,
-             bytes / ms / 1e6, 51.2e9 / (bytes / ms / 1e3) * 1e3);
+             bytes / ms / 1e6, 51.2e9 / (bytes / ms));
     }
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
