@@ -148,6 +148,19 @@ ofsc_status ofsc_graph_copy_csr(ofsc_graph g, int64_t* h_row_ptr, int32_t* h_col
 ofsc_status ofsc_graph_copy_perm(ofsc_graph g, int32_t* h_perm);
 ofsc_status ofsc_graph_destroy(ofsc_graph g);
 
+/* Streaming: append a batch of undirected edges to
+ * a built graph in place, so that it equals the graph built from the
+ * concatenation of all batches (same CSR, s = D^{-1/2}, ||A||_F^2 and counts,
+ * bit for bit).  New edges are sorted and deduplicated on the device and merged
+ * row by row into the existing CSR (no re-sort of the old edges).  Endpoints use
+ * the original node ids; a reordered graph keeps its row order (the new edges
+ * are relabelled into it).  Node count n is fixed (snapshots of a graph with
+ * known n, as in the Graph Challenge streams).  Invalidates the run workspace.
+ * Single-rank graphs only (OFSC_ERR_STATE when p > 1: rebuild instead).
+ * OFSC_ERR_RANGE for an endpoint outside [0, n), graph unchanged. */
+ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const int64_t* dst,
+                              int edges_on_device, ofsc_stream stream);
+
 /* Y = A Z for this rank's rows (the SpMM of eq:spmm P:440, values implicit).
  * d_Z: all n rows (n x ldz, original node order) on every rank; d_Y: local
  * rows (n_local x ldy; original order when p == 1, internal order when p > 1). */

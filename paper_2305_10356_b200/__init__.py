@@ -94,6 +94,7 @@ SIGNATURES = {
     "ofsc_graph_build_ex": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, C.POINTER(BuildOpts), _P,
                                   C.POINTER(_P)]),
     "ofsc_graph_info_get": (_ST, [_P, C.POINTER(GraphInfo)]),
+    "ofsc_graph_append": (_ST, [_P, _I64, _P, _P, C.c_int, _P]),
     "ofsc_graph_copy_csr": (_ST, [_P, _P, _P, _P]),
     "ofsc_graph_copy_perm": (_ST, [_P, _P]),
     "ofsc_graph_destroy": (_ST, [_P]),
@@ -263,6 +264,21 @@ class Graph:
                                              d.ctypes.data_as(C.c_void_p), 0, C.byref(bo),
                                              _stream(stream), C.byref(h)))
         self.handle = h
+        self.info = self.get_info()
+
+    def append(self, src, dst, stream=None):
+        """Add a batch of edges in place (ofsc_graph_append; streaming snapshots)."""
+        torch = _torch()
+        if isinstance(src, torch.Tensor) and src.is_cuda:
+            s = src.to(torch.int64).contiguous()
+            d = dst.to(torch.int64).contiguous()
+            _check(lib().ofsc_graph_append(self.handle, s.numel(), C.c_void_p(s.data_ptr()),
+                                           C.c_void_p(d.data_ptr()), 1, _stream(stream)))
+        else:
+            s = np.ascontiguousarray(np.asarray(src, dtype=np.int64))
+            d = np.ascontiguousarray(np.asarray(dst, dtype=np.int64))
+            _check(lib().ofsc_graph_append(self.handle, s.size, s.ctypes.data_as(C.c_void_p),
+                                           d.ctypes.data_as(C.c_void_p), 0, _stream(stream)))
         self.info = self.get_info()
 
     def get_info(self):

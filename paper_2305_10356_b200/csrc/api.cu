@@ -381,6 +381,70 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
   return st;
 }
 
+__global__ void k_invert_perm_b(int64_t n, const int32_t* perm, int32_t* inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[i]] = (int32_t)i;
+}
+
+ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const int64_t* dst,
+                              int edges_on_device, ofsc_stream stream) {
+  return guard([&] {
+    OFSC_REQUIRE(g && m >= 0 && (m == 0 || (src && dst)), OFSC_ERR_ARG, "bad append arguments");
+    OFSC_REQUIRE(g->p == 1, OFSC_ERR_STATE,
+                 "ofsc_graph_append supports single-rank graphs (rebuild for p > 1)");
+    if (m == 0) return;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = g->n;
+    const size_t eb = (size_t)m * sizeof(int64_t);
+    DBuf ds(edges_on_device ? 0 : eb, s), dd(edges_on_device ? 0 : eb, s);
+    const int64_t* psrc = src;
+    const int64_t* pdst = dst;
+    if (!edges_on_device) {
+      OFSC_CUDA(cudaMemcpyAsync(ds.p, src, eb, cudaMemcpyHostToDevice, s));
+      OFSC_CUDA(cudaMemcpyAsync(dd.p, dst, eb, cudaMemcpyHostToDevice, s));
+      psrc = ds.as<int64_t>();
+      pdst = dd.as<int64_t>();
+    }
+    DBuf s2(g->reordered ? eb : 0, s), d2(g->reordered ? eb : 0, s), inv(g->reordered ? n * 4 : 0, s);
+    if (g->reordered) {   // original ids -> internal (community-ordered) rows; the order is kept
+      k_invert_perm_b<<<num_sms() * 8, 256, 0, s>>>(n, g->perm, inv.as<int32_t>());
+      OFSC_LAUNCH_CHECK();
+      relabel_edges(m, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
+      psrc = s2.as<int64_t>();
+      pdst = d2.as<int64_t>();
+    }
+    CsrDevice csr;
+    csr.n = n;
+    csr.row_ptr = g->row_ptr;
+    csr.col = g->col;
+    csr.s = g->s_slot;
+    csr.nnz = g->info.nnz_global;
+    csr.m_kept = g->info.n_edges_kept;
+    csr.n_loops = g->info.n_self_loops_dropped;
+    csr.n_dups = g->info.n_duplicates_dropped;
+    csr.n_isolated = g->info.n_isolated;
+    csr.max_deg = g->info.max_degree;
+    csr.fro2 = g->info.fro2_A;
+    g->ws.release();                 // captured iteration graphs hold the old CSR pointers
+    append_csr(csr, m, psrc, pdst, s);
+    g->row_ptr = csr.row_ptr;
+    g->col = csr.col;
+    scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, 1, n, s);
+    OFSC_CUDA(cudaStreamSynchronize(s));
+    g->nnz_local = csr.nnz;
+    ofsc_graph_info& in = g->info;
+    in.n_edges_kept = csr.m_kept;
+    in.nnz_global = csr.nnz;
+    in.nnz_local = csr.nnz;
+    in.n_isolated = csr.n_isolated;
+    in.n_self_loops_dropped = csr.n_loops;
+    in.n_duplicates_dropped = csr.n_dups;
+    in.max_degree = csr.max_deg;
+    in.fro2_A = csr.fro2;
+  });
+}
+
 ofsc_status ofsc_graph_info_get(ofsc_graph g, ofsc_graph_info* out) {
   return guard([&] {
     OFSC_REQUIRE(g && out, OFSC_ERR_ARG, "null argument");

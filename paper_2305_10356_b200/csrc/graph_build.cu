@@ -132,6 +132,7 @@ int blocks_for(int64_t n) {
 void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst, CsrDevice& out,
                cudaStream_t st) {
   OFSC_REQUIRE(n >= 1 && n < (int64_t(1) << 31), OFSC_ERR_ARG, "need 1 <= n < 2^31");
+  keep_pool();
   out.n = n;
   DevBuf<unsigned long long> counters(2, st);   // [0] loops, [1] isolated
   DevBuf<int> flags(2, st);                     // [0] bad endpoint, [1] max degree
@@ -225,6 +226,238 @@ void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
   out.fro2 = (double)n + f;
   out.n_isolated = (int64_t)iso;
   out.max_deg = md;
+}
+
+// ---- incremental CSR merge (streaming snapshots) --------
+// Appends a batch of undirected edges to an existing CSR so that the result is
+// exactly the CSR build_csr would produce from the concatenated edge list:
+//   1. batch keys (canonical, loops -> sentinel), radix sort + unique;
+//   2. symmetrise, sort by (row, col);
+//   3. drop keys already present in the old CSR (binary search in the row);
+//   4. new degrees = old + added, exclusive scan -> new row_ptr;
+//   5. merge: one warp per row, each old / added column goes to its rank in the
+//      union (binary search in the other sorted list) -> columns ascending;
+//   6. s = D^{-1/2} and ||A||_F^2 recomputed by the same kernels as build_csr.
+namespace {
+
+__global__ void k_exists(int64_t nnz, const unsigned long long* keys, const int64_t* row_ptr,
+                         const int32_t* col, int* keep) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[e];
+    const int64_t u = (int64_t)(k >> 32);
+    const int32_t v = (int32_t)(k & 0xffffffffull);
+    int64_t lo = row_ptr[u], hi = row_ptr[u + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    keep[e] = (lo < row_ptr[u + 1] && col[lo] == v) ? 0 : 1;
+  }
+}
+
+__global__ void k_old_degree(int64_t n, const int64_t* row_ptr, int* deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = (int)(row_ptr[i + 1] - row_ptr[i]);
+}
+
+__global__ void k_add_degree(int64_t nadd, const unsigned long long* keys, int* deg_add) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nadd;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(deg_add + (keys[e] >> 32), 1);
+}
+
+__global__ void k_sum_deg(int64_t n, const int* a, const int* b, int* out, int64_t* out64) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = a[i] + b[i];
+    out64[i] = a[i] + b[i];
+  }
+}
+
+// rank of x in the sorted list p[0..len): number of elements < x
+__device__ __forceinline__ int64_t rank_lt(const int32_t* p, int64_t len, int32_t x) {
+  int64_t lo = 0, hi = len;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (p[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_merge_rows(int64_t n, const int64_t* old_ptr, const int32_t* old_col,
+                             const int64_t* add_ptr, const int32_t* add_col,
+                             const int64_t* new_ptr, int32_t* new_col) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < n; i += nw) {
+    const int64_t ob = old_ptr[i], on = old_ptr[i + 1] - ob;
+    const int64_t ab = add_ptr[i], an = add_ptr[i + 1] - ab;
+    const int64_t nb = new_ptr[i];
+    if (an == 0) {
+      for (int64_t j = lane; j < on; j += 32) new_col[nb + j] = old_col[ob + j];
+      continue;
+    }
+    for (int64_t j = lane; j < on; j += 32) {
+      const int32_t c = old_col[ob + j];
+      new_col[nb + j + rank_lt(add_col + ab, an, c)] = c;
+    }
+    for (int64_t j = lane; j < an; j += 32) {
+      const int32_t c = add_col[ab + j];
+      new_col[nb + j + rank_lt(old_col + ob, on, c)] = c;   // c is not in the old row
+    }
+  }
+}
+
+__global__ void k_cols_of_keys(int64_t nnz, const unsigned long long* keys, int32_t* col) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    col[e] = (int32_t)(keys[e] & 0xffffffffull);
+}
+
+}  // namespace
+
+void append_csr(CsrDevice& csr, int64_t m, const int64_t* d_src, const int64_t* d_dst,
+                cudaStream_t st) {
+  const int64_t n = csr.n;
+  if (m <= 0) return;
+  keep_pool();
+  DevBuf<unsigned long long> counters(2, st);
+  DevBuf<int> flags(2, st);
+  OFSC_CUDA(cudaMemsetAsync(counters.p, 0, 2 * sizeof(unsigned long long), st));
+  OFSC_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), st));
+  // 1. batch keys, sort, unique (within the batch)
+  DevBuf<unsigned long long> ukeys(m, st);
+  int64_t E = 0, loops = 0;
+  {
+    DevBuf<unsigned long long> keys(m, st), sorted(m, st);
+    k_make_keys<<<blocks_for(m), 256, 0, st>>>(m, n, d_src, d_dst, keys.p, counters.p, flags.p);
+    OFSC_LAUNCH_CHECK();
+    size_t tb = 0;
+    OFSC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.p, sorted.p, m, 0, 64, st));
+    {
+      DevBuf<char> tmp(tb, st);
+      OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, sorted.p, m, 0, 64, st));
+    }
+    DevBuf<int64_t> nsel(1, st);
+    tb = 0;
+    OFSC_CUDA(cub::DeviceSelect::Unique(nullptr, tb, sorted.p, ukeys.p, nsel.p, m, st));
+    {
+      DevBuf<char> tmp(tb, st);
+      OFSC_CUDA(cub::DeviceSelect::Unique(tmp.p, tb, sorted.p, ukeys.p, nsel.p, m, st));
+    }
+    int64_t h_nsel = 0;
+    unsigned long long h_cnt[2];
+    int h_flags[2];
+    OFSC_CUDA(cudaMemcpyAsync(&h_nsel, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaMemcpyAsync(h_cnt, counters.p, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaMemcpyAsync(h_flags, flags.p, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaStreamSynchronize(st));
+    OFSC_REQUIRE(!h_flags[0], OFSC_ERR_RANGE, "edge endpoint outside [0, n)");
+    loops = (int64_t)h_cnt[0];
+    unsigned long long last = 0;
+    if (h_nsel > 0)
+      OFSC_CUDA(cudaMemcpy(&last, ukeys.p + h_nsel - 1, sizeof(last), cudaMemcpyDeviceToHost));
+    E = h_nsel - ((h_nsel > 0 && last == kSentinel) ? 1 : 0);
+  }
+  int64_t nadd = 0;
+  DevBuf<unsigned long long> addk(E > 0 ? 2 * E : 1, st);
+  if (E > 0) {
+    // 2. symmetrise + sort by (row, col); 3. drop keys present in the old CSR
+    DevBuf<unsigned long long> sym(2 * E, st), sym_sorted(2 * E, st);
+    k_symmetrise<<<blocks_for(E), 256, 0, st>>>(E, ukeys.p, sym.p);
+    OFSC_LAUNCH_CHECK();
+    int hi = 1;
+    while ((int64_t(1) << hi) < n) ++hi;
+    size_t tb = 0;
+    OFSC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, sym.p, sym_sorted.p, 2 * E, 0, 32 + hi, st));
+    {
+      DevBuf<char> tmp(tb, st);
+      OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, sym.p, sym_sorted.p, 2 * E, 0, 32 + hi, st));
+    }
+    DevBuf<int> keep(2 * E, st);
+    k_exists<<<blocks_for(2 * E), 256, 0, st>>>(2 * E, sym_sorted.p, csr.row_ptr, csr.col, keep.p);
+    OFSC_LAUNCH_CHECK();
+    DevBuf<int64_t> nsel(1, st);
+    tb = 0;
+    OFSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, sym_sorted.p, keep.p, addk.p, nsel.p, 2 * E, st));
+    {
+      DevBuf<char> tmp(tb, st);
+      OFSC_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, sym_sorted.p, keep.p, addk.p, nsel.p, 2 * E,
+                                           st));
+    }
+    OFSC_CUDA(cudaMemcpyAsync(&nadd, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaStreamSynchronize(st));
+  }
+  const int64_t e_new = nadd / 2;                 // symmetric: both directions dropped together
+  csr.n_loops += loops;
+  csr.n_dups += m - loops - e_new;
+  if (nadd == 0) return;
+  // 4. degrees and row pointers
+  DevBuf<int> deg_old(n, st), deg_add(n, st), deg(n, st);
+  DevBuf<int64_t> deg64(n, st), add64(n, st), add_ptr(n + 1, st);
+  OFSC_CUDA(cudaMemsetAsync(deg_add.p, 0, n * sizeof(int), st));
+  k_old_degree<<<blocks_for(n), 256, 0, st>>>(n, csr.row_ptr, deg_old.p);
+  k_add_degree<<<blocks_for(nadd), 256, 0, st>>>(nadd, addk.p, deg_add.p);
+  OFSC_LAUNCH_CHECK();
+  k_deg_to_i64<<<blocks_for(n), 256, 0, st>>>(n, deg_add.p, add64.p);
+  k_sum_deg<<<blocks_for(n), 256, 0, st>>>(n, deg_old.p, deg_add.p, deg.p, deg64.p);
+  OFSC_LAUNCH_CHECK();
+  const int64_t nnz_new = csr.nnz + nadd;
+  int64_t* new_ptr = nullptr;
+  int32_t* new_col = nullptr;
+  OFSC_CUDA(cudaMallocAsync(&new_ptr, (n + 1) * sizeof(int64_t), st));
+  OFSC_CUDA(cudaMallocAsync(&new_col, nnz_new * sizeof(int32_t), st));
+  {
+    size_t tb = 0;
+    OFSC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, deg64.p, new_ptr, n, st));
+    DevBuf<char> tmp(tb, st);
+    OFSC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, deg64.p, new_ptr, n, st));
+    OFSC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, add64.p, add_ptr.p, n, st));
+  }
+  OFSC_CUDA(cudaMemcpyAsync(add_ptr.p + n, &nadd, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  // 5. merge
+  {
+    DevBuf<int32_t> add_col(nadd, st);
+    k_cols_of_keys<<<blocks_for(nadd), 256, 0, st>>>(nadd, addk.p, add_col.p);
+    OFSC_LAUNCH_CHECK();
+    const int64_t warps_blocks = (n * 32 + 255) / 256;
+    const int nbm = (int)std::min<int64_t>(warps_blocks, (int64_t)num_sms() * 16);
+    k_merge_rows<<<nbm, 256, 0, st>>>(n, csr.row_ptr, csr.col, add_ptr.p, add_col.p, new_ptr,
+                                      new_col);
+    OFSC_LAUNCH_CHECK();
+    OFSC_CUDA(cudaStreamSynchronize(st));
+  }
+  cudaFree(csr.row_ptr);
+  cudaFree(csr.col);
+  csr.row_ptr = new_ptr;
+  csr.col = new_col;
+  csr.nnz = nnz_new;
+  csr.m_kept += e_new;
+  // 6. s, isolated count, max degree, ||A||_F^2 (as in build_csr)
+  k_scale<<<blocks_for(n), 256, 0, st>>>(n, deg.p, csr.s, csr.row_ptr + n, counters.p + 1,
+                                         flags.p + 1, csr.nnz);
+  OFSC_LAUNCH_CHECK();
+  const int nb = blocks_for(n) < 1024 ? blocks_for(n) : 1024;
+  DevBuf<double> part(nb, st);
+  k_fro2<<<nb, 256, 0, st>>>(n, csr.row_ptr, csr.col, csr.s, part.p);
+  OFSC_LAUNCH_CHECK();
+  std::vector<double> hp(nb);
+  unsigned long long iso = 0;
+  int md = 0;
+  OFSC_CUDA(cudaMemcpyAsync(hp.data(), part.p, nb * sizeof(double), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaMemcpyAsync(&iso, counters.p + 1, sizeof(iso), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaMemcpyAsync(&md, flags.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaStreamSynchronize(st));
+  double f = 0.0;
+  for (int b = 0; b < nb; ++b) f += hp[b];
+  csr.fro2 = (double)n + f;
+  csr.n_isolated = (int64_t)iso;
+  csr.max_deg = md;
 }
 
 // ---- multi-GPU layout helpers ----------------------------------------------

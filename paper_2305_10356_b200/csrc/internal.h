@@ -90,6 +90,7 @@ struct IterParams {
 // ---- launchers (kernels_*.cu) ----
 int grid_rows(int64_t n_rows, int blocks_per_sm);
 int num_sms();
+void keep_pool();   // default mempool keeps freed scratch (no per-build re-mapping)
 
 // grid sizes of the TMA-pipelined streaming kernels (<= 4 * #SMs)
 int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n);
@@ -181,6 +182,10 @@ struct CsrDevice {
 };
 void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst, CsrDevice& out,
                cudaStream_t st);
+// append a batch of edges (device arrays, ids of the CSR's numbering) in place:
+// the result equals build_csr of the concatenated edge list
+void append_csr(CsrDevice& csr, int64_t m, const int64_t* d_src, const int64_t* d_dst,
+                cudaStream_t st);
 // locality reordering (label propagation): perm[new] = old, inv[old] = new
 // (also community id per internal row and community start rows, for L2 cache hints)
 void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv, int64_t* n_comm,

@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--paper-protocol", action="store_true",
                     help="fixed 2 iterations per stage (P:612) instead of the tolerance stop")
     ap.add_argument("--reorder", type=int, default=1)
+    ap.add_argument("--append", type=int, default=1,
+                    help="1: ofsc_graph_append of each new part (incremental CSR merge, "
+                         "NEXT-2); 0: rebuild each snapshot from the cumulative edge list")
     args = ap.parse_args()
     import torch
     import paper_2305_10356_b200 as ofsc
@@ -52,8 +55,14 @@ def main():
         s = np.concatenate(cs)
         d = np.concatenate(cd)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
         a.record(stream)
-        g = ofsc.Graph(cfg.n, s, d, reorder=bool(args.reorder))
+        if args.append and si > 1:
+            g.append(ps, pd)                 # incremental merge of part si (row order kept)
+        else:
+            if si > 1:
+                g.close()
+            g = ofsc.Graph(cfg.n, s, d, reorder=bool(args.reorder))
         b.record(stream)
         torch.cuda.synchronize()
         build_ms = a.elapsed_time(b)
@@ -69,12 +78,13 @@ def main():
                     "converged": r.report["converged"], "run_ms": round(r.report["timed_ms"], 2),
                     "ms_per_iter": round(r.report["timed_ms"] / max(r.report["iters"], 1), 3),
                     "grad_norm": r.report["grad_norm"], "ari": round(ari, 4), "nmi": round(nmi, 4)})
-        g.close()
         print(json.dumps(out[-1]), file=sys.stderr, flush=True)
+    g.close()
     print(json.dumps({"workload": f"{cfg.name} streaming, {args.parts} edge-sampling snapshots",
                       "method": args.method, "tol": None if args.paper_protocol else args.tol,
                       "protocol": "2 its/stage (P:612)" if args.paper_protocol else "tolerance",
                       "reorder": bool(args.reorder),
+                      "graph_update": "append (incremental CSR merge)" if args.append else "rebuild",
                       "total_iters": sum(o["iters"] for o in out),
                       "total_run_ms": round(sum(o["run_ms"] for o in out), 2),
                       "total_build_ms": round(sum(o["build_ms"] for o in out), 2),
