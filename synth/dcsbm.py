@@ -165,6 +165,39 @@ def stream_parts(src, dst, parts, seed):
     return [(src[idx], dst[idx]) for idx in np.array_split(perm, parts)]
 
 
+def snowball_parts(n, src, dst, parts, seed):
+    """Snowball-sampling streaming parts ("Streaming Graphs - Snowball
+    Sampling"; the paper does not define the procedure, R27 follows
+    SPEC S:88): breadth-first search from a seeded random node (restarting from
+    the lowest-numbered undiscovered node when a component is exhausted) gives
+    every node a discovery rank; an edge is revealed once both endpoints are
+    discovered, i.e. edges are ordered by max(rank(u), rank(v)) (ties in the
+    input order) and split into `parts` contiguous parts whose sizes differ by
+    <= 1.  Input generator only: no method arithmetic."""
+    import scipy.sparse as sp
+    import scipy.sparse.csgraph as csg
+    rng = _rng(seed)
+    src = np.asarray(src, dtype=np.int64)
+    dst = np.asarray(dst, dtype=np.int64)
+    A = sp.csr_matrix((np.ones(src.size, dtype=np.int8), (src, dst)), shape=(n, n))
+    A = ((A + A.T) > 0).astype(np.int8).tocsr()
+    rank = np.full(n, -1, dtype=np.int64)
+    nxt = 0
+    start = int(rng.integers(n))
+    while True:
+        order = csg.breadth_first_order(A, start, directed=False, return_predecessors=False)
+        order = order[rank[order] < 0]
+        rank[order] = np.arange(nxt, nxt + order.size)
+        nxt += order.size
+        left = np.nonzero(rank < 0)[0]
+        if left.size == 0:
+            break
+        start = int(left[0])
+    key = np.maximum(rank[src], rank[dst])
+    idx = np.argsort(key, kind="stable")
+    return [(src[c], dst[c]) for c in np.array_split(idx, parts)]
+
+
 def x0_block(n, k, seed, dtype=np.float64):
     """X0 ~ N(0, 1/N) entries: standard normal / sqrt(N)."""
     x = _rng(seed).standard_normal((n, k)) / np.sqrt(n)

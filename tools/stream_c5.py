@@ -33,17 +33,23 @@ def main():
     ap.add_argument("--paper-protocol", action="store_true",
                     help="fixed 2 iterations per stage (P:612) instead of the tolerance stop")
     ap.add_argument("--reorder", type=int, default=1)
+    ap.add_argument("--sampling", default="edge", choices=["edge", "snowball"],
+                    help="edge: uniform edge sampling (SGES); snowball: BFS-revealed edges "
+                         "(SGSS, DESIGN.md R27); undiscovered nodes are isolated")
     ap.add_argument("--append", type=int, default=1,
                     help="1: ofsc_graph_append of each new part (incremental CSR merge, "
                          "NEXT-2); 0: rebuild each snapshot from the cumulative edge list")
     args = ap.parse_args()
     import torch
     import paper_2305_10356_b200 as ofsc
-    from synth import CONFIGS, config_graph, stream_parts, x0_block, kmeans_init_rows
+    from synth import CONFIGS, config_graph, stream_parts, snowball_parts, x0_block, kmeans_init_rows
 
     cfg = CONFIGS[args.config]
     src, dst, labels = config_graph(cfg)
-    parts = stream_parts(src, dst, args.parts, cfg.seed_graph + 1000)
+    if args.sampling == "edge":
+        parts = stream_parts(src, dst, args.parts, cfg.seed_graph + 1000)
+    else:
+        parts = snowball_parts(cfg.n, src, dst, args.parts, cfg.seed_graph + 2000)
     X = torch.from_numpy(x0_block(cfg.n, cfg.k, cfg.seed_x0)).cuda()
     rows = torch.from_numpy(kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)).cuda()
     stream = torch.cuda.current_stream()
@@ -80,7 +86,7 @@ def main():
                     "grad_norm": r.report["grad_norm"], "ari": round(ari, 4), "nmi": round(nmi, 4)})
         print(json.dumps(out[-1]), file=sys.stderr, flush=True)
     g.close()
-    print(json.dumps({"workload": f"{cfg.name} streaming, {args.parts} edge-sampling snapshots",
+    print(json.dumps({"workload": f"{cfg.name} streaming, {args.parts} {args.sampling}-sampling snapshots",
                       "method": args.method, "tol": None if args.paper_protocol else args.tol,
                       "protocol": "2 its/stage (P:612)" if args.paper_protocol else "tolerance",
                       "reorder": bool(args.reorder),
