@@ -287,6 +287,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
         psrc = ds.as<int64_t>();
         pdst = dd.as<int64_t>();
       }
+      trace_point("graph_build: edges on device", s);
       try {
         build_csr(n, m, psrc, pdst, csr, s);
         if (reorder) {
@@ -296,6 +297,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
           DBuf inv(n * sizeof(int32_t), s);
           lpa_order(csr, sweeps, g->perm, inv.as<int32_t>(), &n_comm, &intra, g->cid, &g->cstart, s);
           DBuf s2(m * sizeof(int64_t), s), d2(m * sizeof(int64_t), s);
+          trace_point("graph_build: LPA order", s);
           relabel_edges(m, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
           free_csr();
           build_csr(n, m, s2.as<int64_t>(), d2.as<int64_t>(), csr, s);
@@ -308,12 +310,18 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     }
     const int p = g->p;
     // nnz-balanced contiguous row split (each row weighted deg + 1: nnz(A) incl. diagonal)
-    std::vector<int64_t> rp(n + 1);
-    OFSC_CUDA(cudaMemcpyAsync(rp.data(), csr.row_ptr, (n + 1) * sizeof(int64_t),
-                              cudaMemcpyDeviceToHost, s));
+    // p == 1 needs only row_ptr[0] = 0 and row_ptr[n] = nnz (no 8(n+1)-byte download)
+    std::vector<int64_t> rp(p == 1 ? 0 : n + 1);
+    if (p > 1) {
+      OFSC_CUDA(cudaMemcpyAsync(rp.data(), csr.row_ptr, (n + 1) * sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, s));
+    }
     OFSC_CUDA(cudaStreamSynchronize(s));
+    trace_point("graph_build: row_ptr on host", s);
+    auto rp_at = [&](int64_t i) -> int64_t { return p == 1 ? (i == 0 ? 0 : csr.nnz) : rp[i]; };
     g->begins.assign(p + 1, 0);
-    partition_rows(n, rp.data(), p, g->begins.data());
+    if (p == 1) g->begins[1] = n;
+    else partition_rows(n, rp.data(), p, g->begins.data());
     const double total = (double)(csr.nnz + n);
     g->row_begin = g->begins[g->rank];
     g->row_end = g->begins[g->rank + 1];
@@ -321,12 +329,12 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     int64_t slot = 0, max_nnz = 0;
     for (int r = 0; r < p; ++r) {
       slot = std::max(slot, g->begins[r + 1] - g->begins[r]);
-      const int64_t nz = rp[g->begins[r + 1]] - rp[g->begins[r]] + (g->begins[r + 1] - g->begins[r]);
+      const int64_t nz = rp_at(g->begins[r + 1]) - rp_at(g->begins[r]) + (g->begins[r + 1] - g->begins[r]);
       max_nnz = std::max(max_nnz, nz);
     }
     g->slot_rows = p == 1 ? n : std::max<int64_t>(slot, 1);
     g->own_off = (int64_t)g->rank * g->slot_rows;
-    const int64_t e0 = rp[g->row_begin], e1 = rp[g->row_end];
+    const int64_t e0 = rp_at(g->row_begin), e1 = rp_at(g->row_end);
     g->nnz_local = e1 - e0;
     if (p == 1) {
       g->row_ptr = csr.row_ptr;
@@ -372,6 +380,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     in.reordered = g->reordered ? 1 : 0;
     in.n_communities = n_comm;
     in.intra_edge_fraction = intra;
+    trace_point("graph_build: done", s);
     *out = g;
   });
   if (st != OFSC_OK && g) {
@@ -1256,22 +1265,44 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     OFSC_REQUIRE(opts && h_X && h_init_rows && h_labels && n_clusters >= 1 && opts->k >= 1,
                  OFSC_ERR_ARG, "bad spectral_cluster args");
     cudaStream_t s = (cudaStream_t)stream;
+    // copies overlap compute on a side stream: X0 upload || graph build,
+    // feature download || normalise + K-means (pinned host buffers make them async)
+    // (declared after dXf: destroyed first, so the side stream is drained before
+    // dXf is released on `s`, also on error paths)
+    const int k = opts->k;
+    const size_t es = esize(dt);
+    DBuf dXf((size_t)n * k * es, s);
+    struct Side {
+      cudaStream_t st = nullptr;
+      cudaEvent_t a = nullptr, b = nullptr;
+      ~Side() {
+        if (st) cudaStreamSynchronize(st);
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+        if (st) cudaStreamDestroy(st);
+      }
+    } side;
+    OFSC_CUDA(cudaStreamCreateWithFlags(&side.st, cudaStreamNonBlocking));
+    OFSC_CUDA(cudaEventCreateWithFlags(&side.a, cudaEventDisableTiming));
+    OFSC_CUDA(cudaEventCreateWithFlags(&side.b, cudaEventDisableTiming));
+    OFSC_CUDA(cudaEventRecord(side.b, s));                 // dXf allocated
+    OFSC_CUDA(cudaStreamWaitEvent(side.st, side.b, 0));
+    OFSC_CUDA(cudaMemcpyAsync(dXf.p, h_X, (size_t)n * k * es, cudaMemcpyHostToDevice, side.st));
+    OFSC_CUDA(cudaEventRecord(side.a, side.st));
     // default: reorder only when the run is long enough to repay the LPA pass
     // (~0.2 s at 5M nodes vs ~2 ms saved per iteration there)
     ofsc_build_opts bo{opts->max_iters >= 100 ? 1 : 0, 30};
     if (bopts) bo = *bopts;
     ofsc_status b = ofsc_graph_build_ex(comm, n, m, h_src, h_dst, 0, &bo, stream, &g);
     if (b != OFSC_OK) throw Error{b, g_last_error};
-    const int k = opts->k;
     const int64_t nl = g->n_local;
-    const size_t es = esize(dt);
     const int32_t* perm = g->reordered ? g->perm : nullptr;
-    DBuf dXf((size_t)n * k * es, s), dX(g->p > 1 ? (size_t)std::max<int64_t>(nl, 1) * k * es : 0, s),
+    DBuf dX(g->p > 1 ? (size_t)std::max<int64_t>(nl, 1) * k * es : 0, s),
         dY(std::max<int64_t>(nl, 1) * k * es, s), dC((size_t)n_clusters * k * 8, s),
         dL(std::max<int64_t>(nl, 1) * 4, s), dLf((size_t)n * 4, s), dR((size_t)n_clusters * 8, s),
         dInv(perm ? (size_t)n * 4 : 0, s);
     // all n rows of X0 (original order) -> this rank's internal rows
-    OFSC_CUDA(cudaMemcpyAsync(dXf.p, h_X, (size_t)n * k * es, cudaMemcpyHostToDevice, s));
+    OFSC_CUDA(cudaStreamWaitEvent(s, side.a, 0));
     // p == 1: ofsc_run maps original-order rows through perm itself, run on the full
     // array; p > 1: gather this rank's internal rows first
     void* Xrun = dXf.p;
@@ -1285,7 +1316,9 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     if (run_st != OFSC_OK && run_st != OFSC_ERR_DIVERGED) throw Error{run_st, g_last_error};
     // features back to the caller's full array (rows this rank owns)
     if (g->p == 1) {
-      OFSC_CUDA(cudaMemcpyAsync(h_X, dXf.p, (size_t)n * k * es, cudaMemcpyDeviceToHost, s));
+      OFSC_CUDA(cudaEventRecord(side.b, s));
+      OFSC_CUDA(cudaStreamWaitEvent(side.st, side.b, 0));
+      OFSC_CUDA(cudaMemcpyAsync(h_X, dXf.p, (size_t)n * k * es, cudaMemcpyDeviceToHost, side.st));
     } else {
       launch_copy_out(dt, k, k, nl, dX.p,
                       (char*)dXf.p + (perm ? 0 : (size_t)g->row_begin * k * es), k,
@@ -1324,6 +1357,7 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
       for (int64_t i = 0; i < n; ++i)
         if (tmp[i] >= 0) h_labels[i] = tmp[i];
     }
+    OFSC_CUDA(cudaStreamSynchronize(side.st));
     OFSC_CUDA(cudaStreamSynchronize(s));
   });
   if (g) ofsc_graph_destroy(g);

@@ -134,6 +134,7 @@ void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
   OFSC_REQUIRE(n >= 1 && n < (int64_t(1) << 31), OFSC_ERR_ARG, "need 1 <= n < 2^31");
   keep_pool();
   out.n = n;
+  trace_point("build_csr: start", st);
   DevBuf<unsigned long long> counters(2, st);   // [0] loops, [1] isolated
   DevBuf<int> flags(2, st);                     // [0] bad endpoint, [1] max degree
   OFSC_CUDA(cudaMemsetAsync(counters.p, 0, 2 * sizeof(unsigned long long), st));
@@ -151,6 +152,7 @@ void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
       DevBuf<char> tmp(tmp_bytes, st);
       OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, m, 0, 64, st));
     }
+    trace_point("build_csr: keys sorted", st);
     DevBuf<int64_t> nsel(1, st);
     tmp_bytes = 0;
     OFSC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp_bytes, sorted.p, ukeys.p, nsel.p, m, st));
@@ -172,6 +174,7 @@ void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
       OFSC_CUDA(cudaMemcpy(&last, ukeys.p + h_nsel - 1, sizeof(last), cudaMemcpyDeviceToHost));
     E = h_nsel - ((h_nsel > 0 && last == kSentinel) ? 1 : 0);
   }
+  trace_point("build_csr: unique", st);
   out.m_kept = E;
   out.n_dups = m - out.n_loops - E;
   out.nnz = 2 * E;
@@ -197,6 +200,7 @@ void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
     }
     k_split_keys<<<blocks_for(out.nnz), 256, 0, st>>>(out.nnz, sym_sorted.p, out.col, deg.p);
     OFSC_LAUNCH_CHECK();
+    trace_point("build_csr: symmetrised + sorted", st);
   }
   {
     DevBuf<int64_t> deg64(n, st);
@@ -226,6 +230,7 @@ void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
   out.fro2 = (double)n + f;
   out.n_isolated = (int64_t)iso;
   out.max_deg = md;
+  trace_point("build_csr: scan, s, fro2 done", st);
 }
 
 // ---- incremental CSR merge (streaming snapshots) --------

@@ -90,7 +90,8 @@ struct IterParams {
 // ---- launchers (kernels_*.cu) ----
 int grid_rows(int64_t n_rows, int blocks_per_sm);
 int num_sms();
-void keep_pool();   // default mempool keeps freed scratch (no per-build re-mapping)
+void keep_pool();
+void trace_point(const char* what, cudaStream_t st);   // OFSC_TRACE=1: phase timestamps   // default mempool keeps freed scratch (no per-build re-mapping)
 
 // grid sizes of the TMA-pipelined streaming kernels (<= 4 * #SMs)
 int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n);

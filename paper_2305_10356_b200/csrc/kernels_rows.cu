@@ -9,6 +9,10 @@
 #include "common.cuh"
 #include "sm100.cuh"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace ofsc {
 
 template <typename T>
@@ -22,6 +26,20 @@ int num_sms() {
     OFSC_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   }
   return n;
+}
+
+// OFSC_TRACE=1: host-side phase timestamps of the graph build to stderr.
+void trace_point(const char* what, cudaStream_t st) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("OFSC_TRACE");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!on) return;
+  static std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(st);
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  fprintf(stderr, "[ofsc trace] %10.2f ms  %s\n", ms, what);
 }
 
 // The graph build allocates its sort / scan scratch from the device's default
