@@ -420,53 +420,91 @@ def oracle_threads():
         return 1
 
 
-def cpu_baseline(cfg, method, src, dst, X0, iters=2):
-    """Oracle (numpy + scipy, as it stands) on the host: `iters` iterations of Algorithm 2."""
-    from oracle import build_operator, run_ofm
-    op = build_operator(cfg.n, src, dst)
-    marks = []
-    t0 = time.perf_counter()
-    run_ofm(op, method, X0, iters, refresh=0, callback=lambda t: marks.append(time.perf_counter()))
-    tot = marks[-1] - t0
-    per = (marks[-1] - marks[0]) / (iters - 1) if iters > 1 else tot
-    return {"value": round(1.0 / per, 5), "unit": "it/s", "cores": oracle_threads(),
-            "kind": "oracle", "host_cpus": os.cpu_count(),
-            "sample": f"{cfg.name} full graph, {method}, {iters} oracle iterations (refresh=0), "
-                      f"per-iteration time from iteration 2 (first includes setup); scipy SpMM "
-                      f"single-threaded, BLAS Grams with {oracle_threads()} threads"}
+class OracleSampler:
+    """Bounded samples of the oracle's iteration (oracle/sample.py): one sample =
+    Algorithm 2's arithmetic on a block of ~N/blocks rows, timed and scaled by
+    N / rows to a full-iteration rate.  Setup (operator build, the first A X and
+    direction over all rows) is untimed."""
+
+    def __init__(self, cfg, method, src, dst, X0):
+        from oracle import build_operator, apply_A, direction
+        self.method = method
+        self.op = build_operator(cfg.n, src, dst)
+        self.X = np.asarray(X0, dtype=np.float64)
+        self.AX = apply_A(self.op, self.X)
+        self.M = self.X.T @ self.X
+        self.W = self.X.T @ self.AX
+        self.Gp = direction(method, self.X, self.AX, self.M, self.W)
+        self.Vp = -self.Gp
+        n = cfg.n
+        self.blocks = 1 if n <= 250_000 else max(1, int(round(n / 312_500)))   # ~1-2 s per sample at c4
+        self.bounds = np.linspace(0, n, self.blocks + 1).astype(np.int64)
+        self.n = n
+        self.i = 0
+
+    def step(self):
+        """Run one sample; return (seconds, rows)."""
+        from oracle.sample import iteration_rows
+        b = self.i % self.blocks
+        self.i += 1
+        r0, r1 = int(self.bounds[b]), int(self.bounds[b + 1])
+        t = time.perf_counter()
+        iteration_rows(self.op, self.method, self.X, self.AX, self.Gp, self.Vp, self.M, self.W,
+                       r0, r1)
+        return time.perf_counter() - t, r1 - r0
+
+    def describe(self, cfg, nsteps):
+        return (f"{nsteps} samples of one {self.method} iteration of {cfg.name}, each on a block of "
+                f"~{self.n // self.blocks:,} of the {self.n:,} rows (Algorithm 2's arithmetic: direction, "
+                f"SpMM rows, Grams, k x k line search, update; oracle/sample.py), time scaled by "
+                f"N / rows; scipy SpMM single-threaded, numpy BLAS with {oracle_threads()} threads")
+
+
+def cpu_baseline(cfg, method, src, dst, X0, samples=8):
+    """Oracle (numpy + scipy, as it stands) on the host: a bounded sample (~10-30 s)."""
+    smp = OracleSampler(cfg, method, src, dst, X0)
+    smp.step()                                   # warm-up
+    secs = rows = 0.0
+    for _ in range(samples):
+        dt, r = smp.step()
+        secs += dt
+        rows += r
+    per_iter = secs * cfg.n / rows
+    return {"value": round(1.0 / per_iter, 5), "unit": "it/s", "cores": oracle_threads(),
+            "kind": "oracle", "host_cpus": os.cpu_count(), "sample": smp.describe(cfg, samples)}
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args):
-    """Reference arm: the oracle, as it stands, on this box's host cores (rank 0 only)."""
+    """Reference arm: the oracle, as it stands, on this box's host cores (rank 0 only).
+    Each step is a bounded sample of the workload (OracleSampler): one iteration's
+    arithmetic on a block of rows, scaled to the full-iteration rate."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    from oracle import build_operator, run_ofm
     cfg = CONFIGS[args.config]
     src, dst, _ = config_graph(cfg)
     X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
-    op = build_operator(cfg.n, src, dst)
+    smp = OracleSampler(cfg, args.method, src, dst, X0)
     W, K = args.warmup, args.steps
-    marks = []
-    run_ofm(op, args.method, X0, W + K, refresh=0,
-            callback=lambda t: marks.append(time.perf_counter()))
-    # step t ends at marks[t]; the K timed steps are W .. W+K-1
-    start = marks[W - 1] if W >= 1 else None
-    if start is None:
-        raise SystemExit("--warmup must be >= 1 for the reference arm")
-    sec = marks[W + K - 1] - start
-    value = K / sec
+    for _ in range(W):
+        smp.step()
+    secs = rows = 0.0
+    for _ in range(K):
+        dt, r = smp.step()
+        secs += dt
+        rows += r
+    per_iter = secs * cfg.n / rows
+    value = 1.0 / per_iter
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "it/s",
-        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(1e3 * sec / K, 2),
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(1e3 * per_iter, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic seeded DCSBM graph", "config": {"workload": workload_desc(cfg, "f64"),
                                                          "method": args.method, "k": cfg.k},
         "cpu_baseline": {"value": round(value, 5), "unit": "it/s", "cores": oracle_threads(),
-                         "kind": "oracle", "sample": f"{K} full oracle iterations of {cfg.name} "
-                                                     f"after {W} warm-up iterations"},
+                         "kind": "oracle", "sample": smp.describe(cfg, K)},
         "e2e": {"value": round(value, 5), "unit": "it/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)

@@ -107,3 +107,27 @@ def test_fp32_mode_tracks_fp64(c1):
         b = run_ofm(op, m, X0, 10, precision="f32")
         assert np.array_equal(b.X, b.X.astype(np.float32).astype(np.float64))
         assert np.linalg.norm(a.X - b.X) / np.linalg.norm(a.X) < 1e-2
+
+
+def test_row_sample_covers_the_iteration():
+    """oracle/sample.py (bounded CPU timing): the row blocks partition the rows and
+    the block direction / update equal the full-array ones restricted to the block."""
+    from oracle import build_operator, apply_A, direction
+    from oracle.sample import iteration_rows
+    from synth import dcsbm_graph, x0_block
+    n, k = 600, 5
+    s, d, _ = dcsbm_graph(n, 4, 2400, 3.0, 5, 5.0)
+    op = build_operator(n, s, d)
+    X = x0_block(n, k, 6)
+    AX = apply_A(op, X)
+    M, W = X.T @ X, X.T @ AX
+    Gp = direction("ofm_f2", X, AX, M, W)
+    Vp = -Gp
+    beta = np.full(k, 0.3)
+    G = direction("ofm_f2", X, AX, M, W)
+    V = -G + Vp * beta[None, :]
+    AVp = apply_A(op, Vp)
+    for r0, r1 in ((0, 200), (200, 450), (450, 600)):
+        alpha, Xn, AXn = iteration_rows(op, "ofm_f2", X, AX, Gp, Vp, M, W, r0, r1, beta=beta)
+        assert np.allclose(Xn, X[r0:r1] + V[r0:r1] * alpha[None, :], rtol=0, atol=1e-15)
+        assert np.allclose(AXn, AX[r0:r1] + AVp[r0:r1] * alpha[None, :], rtol=0, atol=1e-14)
