@@ -441,6 +441,10 @@ class OracleSampler:
         self.bounds = np.linspace(0, n, self.blocks + 1).astype(np.int64)
         self.n = n
         self.i = 0
+        # untimed views: the row slices of S (a copy in scipy) and s * Vp (each
+        # sample recomputes its own rows' share of it)
+        self.S_rows = [self.op.S[int(self.bounds[b]):int(self.bounds[b + 1])] for b in range(self.blocks)]
+        self.sVp = self.op.s[:, None] * self.Vp
 
     def step(self):
         """Run one sample; return (seconds, rows)."""
@@ -450,7 +454,7 @@ class OracleSampler:
         r0, r1 = int(self.bounds[b]), int(self.bounds[b + 1])
         t = time.perf_counter()
         iteration_rows(self.op, self.method, self.X, self.AX, self.Gp, self.Vp, self.M, self.W,
-                       r0, r1)
+                       r0, r1, S_rows=self.S_rows[b], sVp=self.sVp)
         return time.perf_counter() - t, r1 - r0
 
     def describe(self, cfg, nsteps):

@@ -23,9 +23,11 @@ from .cubic import select_step
 from .methods import cubic_coefficients, direction, grams
 
 
-def iteration_rows(op, method, X, AX, Gp, Vp, M, W, r0, r1, beta=None):
+def iteration_rows(op, method, X, AX, Gp, Vp, M, W, r0, r1, beta=None, S_rows=None, sVp=None):
     """One Algorithm-2 iteration on rows [r0, r1).  X, AX, Gp, Vp are
-    full n x k arrays (V is gathered through S at all rows); returns alpha."""
+    full n x k arrays (V is gathered through S at all rows); returns alpha.
+    S_rows = op.S[r0:r1] and sVp = s * Vp (all rows) may be passed precomputed:
+    the block's share of s * Vp is then recomputed inside (its per-block cost)."""
     k = X.shape[1]
     rows = slice(r0, r1)
     G = direction(method, X[rows], AX[rows], M, W)                  # Alg. 2 l.8
@@ -35,7 +37,13 @@ def iteration_rows(op, method, X, AX, Gp, Vp, M, W, r0, r1, beta=None):
         beta = np.maximum(num / np.maximum(gg, 1e-300), 0.0)
     V = -G + Vp[rows] * beta[None, :]                               # Alg. 2 l.10
     s = op.s[:, None]
-    AVb = -Vp[rows] - s[rows] * (op.S[r0:r1] @ (s * Vp))            # A V on the block's rows
+    if S_rows is None:
+        S_rows = op.S[r0:r1]
+    if sVp is None:
+        sVp = s * Vp
+    else:
+        sVp[rows] = s[rows] * Vp[rows]                              # this block's share of s * V
+    AVb = -Vp[rows] - s[rows] * (S_rows @ sVp)                      # A V on the block's rows
     Q, P, T, Rp = grams(V, X[rows], AVb)
     c3, c2, c1, c0 = cubic_coefficients(method, Q, P, T, Rp, M, W)  # Alg. 2 l.11
     if method.startswith("tri"):
