@@ -118,6 +118,8 @@ typedef struct {
   int32_t reordered;            /* 1 if rows were reordered by ofsc_build_opts.reorder */
   int64_t n_communities;        /* label-propagation communities (reordered graphs) */
   double intra_edge_fraction;   /* fraction of nnz joining two nodes of one community */
+  int64_t halo_rows;            /* p > 1: remote rows this rank's columns reference */
+  int64_t send_rows;            /* p > 1: own rows sent to peers per exchange (sum over peers) */
 } ofsc_graph_info;
 
 /* Build options.  reorder = 1: a locality reordering of the rows derived from
@@ -147,6 +149,18 @@ ofsc_status ofsc_graph_copy_csr(ofsc_graph g, int64_t* h_row_ptr, int32_t* h_col
 /* h_perm[n]: internal row -> original node id (identity unless reordered). */
 ofsc_status ofsc_graph_copy_perm(ofsc_graph g, int32_t* h_perm);
 ofsc_status ofsc_graph_destroy(ofsc_graph g);
+
+/* Multi-GPU exchange plan of this rank (p > 1):
+ * the gather buffer holds the rank's own rows then its halo -- the remote rows
+ * its columns reference, ascending global id.  Per exchange the rank sends to
+ * peer q the own rows that have a neighbour in q's range (h_send_gids, grouped
+ * by q, ascending) and receives from q its halo segment (h_recv_gids).  Both
+ * sides derive the plan from the symmetric graph, so q's send list to r equals
+ * r's receive list from q.  Counts are per peer [p]; id arrays hold
+ * info.send_rows / info.halo_rows global ids (internal row order).  Any output
+ * may be NULL.  p == 1: all counts are 0. */
+ofsc_status ofsc_graph_exchange_plan(ofsc_graph g, int64_t* h_send_counts, int32_t* h_send_gids,
+                                     int64_t* h_recv_counts, int32_t* h_recv_gids);
 
 /* Streaming: append a batch of undirected edges to
  * a built graph in place, so that it equals the graph built from the

@@ -66,7 +66,8 @@ class GraphInfo(C.Structure):
                 ("n_duplicates_dropped", C.c_int64), ("max_degree", C.c_int64),
                 ("fro2_A", C.c_double), ("load_imbalance", C.c_double),
                 ("reordered", C.c_int32), ("n_communities", C.c_int64),
-                ("intra_edge_fraction", C.c_double)]
+                ("intra_edge_fraction", C.c_double), ("halo_rows", C.c_int64),
+                ("send_rows", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -95,6 +96,7 @@ SIGNATURES = {
                                   C.POINTER(_P)]),
     "ofsc_graph_info_get": (_ST, [_P, C.POINTER(GraphInfo)]),
     "ofsc_graph_append": (_ST, [_P, _I64, _P, _P, C.c_int, _P]),
+    "ofsc_graph_exchange_plan": (_ST, [_P, _P, _P, _P, _P]),
     "ofsc_graph_copy_csr": (_ST, [_P, _P, _P, _P]),
     "ofsc_graph_copy_perm": (_ST, [_P, _P]),
     "ofsc_graph_destroy": (_ST, [_P]),
@@ -280,6 +282,19 @@ class Graph:
             _check(lib().ofsc_graph_append(self.handle, s.size, s.ctypes.data_as(C.c_void_p),
                                            d.ctypes.data_as(C.c_void_p), 0, _stream(stream)))
         self.info = self.get_info()
+
+    def exchange_plan(self):
+        """(send_counts[p], send_gids, recv_counts[p], recv_gids) of this rank (p > 1)."""
+        p = self.comm.size if self.comm is not None else 1
+        sc = np.zeros(p, np.int64)
+        rc = np.zeros(p, np.int64)
+        sg = np.zeros(max(self.info["send_rows"], 1), np.int32)
+        rg = np.zeros(max(self.info["halo_rows"], 1), np.int32)
+        _check(lib().ofsc_graph_exchange_plan(self.handle, sc.ctypes.data_as(C.c_void_p),
+                                              sg.ctypes.data_as(C.c_void_p),
+                                              rc.ctypes.data_as(C.c_void_p),
+                                              rg.ctypes.data_as(C.c_void_p)))
+        return sc, sg[:self.info["send_rows"]], rc, rg[:self.info["halo_rows"]]
 
     def get_info(self):
         gi = GraphInfo()

@@ -69,6 +69,7 @@ struct Workspace {
   ofsc_dtype dt = OFSC_F64;
   int KP = 0;
   void *X = nullptr, *AX = nullptr, *G = nullptr, *AV = nullptr, *Vg = nullptr, *Xg = nullptr;
+  void* sendbuf = nullptr;  // p > 1: packed rows of the halo exchange
   double *part_cols = nullptr, *part_g4 = nullptr, *part_g2 = nullptr, *grams = nullptr;
   double* state = nullptr;  // M, W [KP*KP each], alpha, beta, gg_prev [KP], colred [2KP]
   DevCtl* ctl = nullptr;
@@ -86,11 +87,11 @@ struct Workspace {
     if (g_refresh) cudaGraphDestroy(g_refresh);
     e_iter = e_refresh = nullptr;
     g_iter = g_refresh = nullptr;
-    for (void* q : {X, AX, G, AV, Vg, Xg, (void*)part_cols, (void*)part_g4, (void*)part_g2,
+    for (void* q : {X, AX, G, AV, Vg, Xg, sendbuf, (void*)part_cols, (void*)part_g4, (void*)part_g2,
                     (void*)grams, (void*)state, (void*)ctl, (void*)ctr})
       dfree(q);
     ctr = nullptr;
-    X = AX = G = AV = Vg = Xg = nullptr;
+    X = AX = G = AV = Vg = Xg = sendbuf = nullptr;
     part_cols = part_g4 = part_g2 = grams = state = nullptr;
     ctl = nullptr;
     have = false;
@@ -109,10 +110,18 @@ struct ofsc_graph_s {
   std::vector<int64_t> begins;     // p + 1
   int64_t* d_begins = nullptr;
   int64_t* row_ptr = nullptr;      // n_local + 1, from 0
-  int32_t* col = nullptr;          // slot ids (== global ids when p == 1)
-  double* s_slot = nullptr;        // [p * slot_rows]
+  int32_t* col = nullptr;          // gather-buffer row ids (== global ids when p == 1)
+  double* s_slot = nullptr;        // s on the gather rows: [n] (p == 1) or [ext_rows] (halo)
   float* s32_slot = nullptr;
   int32_t* perm = nullptr;         // internal row -> original node (reordered graphs)
+  // gather layout (p > 1: halo layout, graph_build.cu build_halo): ext rows = own rows then
+  // the remote rows this rank's columns reference; the SpMM gathers from a buffer of ext_rows
+  int64_t ext_rows = 0;
+  int32_t* d_gid = nullptr;        // [ext_rows] global id of each ext row (NULL when p == 1)
+  std::vector<int32_t> h_gid;
+  std::vector<int64_t> recv_cnt, recv_off, send_cnt, send_off;
+  int32_t* d_send_idx = nullptr;   // own rows to send, grouped by peer
+  int64_t total_send = 0;
   int32_t* cid = nullptr;          // community of each internal row (reordered graphs)
   int64_t* cstart = nullptr;       // community start rows [n_comm + 1]
   bool reordered = false;
@@ -240,6 +249,8 @@ static void graph_free(ofsc_graph g) {
   dfree(g->perm);
   dfree(g->cid);
   dfree(g->cstart);
+  dfree(g->d_gid);
+  dfree(g->d_send_idx);
 }
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
@@ -332,8 +343,10 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       const int64_t nz = rp_at(g->begins[r + 1]) - rp_at(g->begins[r]) + (g->begins[r + 1] - g->begins[r]);
       max_nnz = std::max(max_nnz, nz);
     }
-    g->slot_rows = p == 1 ? n : std::max<int64_t>(slot, 1);
-    g->own_off = (int64_t)g->rank * g->slot_rows;
+    g->slot_rows = n;     // p == 1: the gather buffer is the whole X (p > 1: set below)
+    g->own_off = 0;
+    g->ext_rows = n;
+    (void)slot;
     const int64_t e0 = rp_at(g->row_begin), e1 = rp_at(g->row_end);
     g->nnz_local = e1 - e0;
     if (p == 1) {
@@ -349,15 +362,30 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       OFSC_CUDA(cudaMalloc(&g->d_begins, (p + 1) * sizeof(int64_t)));
       OFSC_CUDA(cudaMemcpyAsync(g->d_begins, g->begins.data(), (p + 1) * sizeof(int64_t),
                                 cudaMemcpyHostToDevice, s));
-      OFSC_CUDA(cudaMalloc(&g->row_ptr, (g->n_local + 1) * sizeof(int64_t)));
-      OFSC_CUDA(cudaMalloc(&g->col, std::max<int64_t>(g->nnz_local, 1) * sizeof(int32_t)));
-      OFSC_CUDA(cudaMalloc(&g->s_slot, (size_t)p * g->slot_rows * sizeof(double)));
-      OFSC_CUDA(cudaMalloc(&g->s32_slot, (size_t)p * g->slot_rows * sizeof(float)));
-      OFSC_CUDA(cudaMemsetAsync(g->s_slot, 0, (size_t)p * g->slot_rows * sizeof(double), s));
-      OFSC_CUDA(cudaMemsetAsync(g->s32_slot, 0, (size_t)p * g->slot_rows * sizeof(float), s));
-      rebase_row_ptr(csr.row_ptr + g->row_begin, g->n_local, e0, g->row_ptr, s);
-      remap_columns(csr.col + e0, g->nnz_local, g->col, g->d_begins, p, g->slot_rows, s);
-      scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, p, g->slot_rows, s);
+      HaloLayout hl;
+      try {
+        build_halo(csr, g->begins.data(), g->d_begins, p, g->rank, hl, s);
+      } catch (...) {
+        dfree(hl.row_ptr); dfree(hl.col); dfree(hl.s_ext); dfree(hl.s32_ext);
+        dfree(hl.d_gid); dfree(hl.d_send_idx);
+        free_csr();
+        throw;
+      }
+      g->row_ptr = hl.row_ptr;
+      g->col = hl.col;
+      g->s_slot = hl.s_ext;
+      g->s32_slot = hl.s32_ext;
+      g->d_gid = hl.d_gid;
+      g->h_gid = std::move(hl.h_gid);
+      g->ext_rows = hl.ext_rows;
+      g->recv_cnt = hl.recv_cnt;
+      g->recv_off = hl.recv_off;
+      g->send_cnt = hl.send_cnt;
+      g->send_off = hl.send_off;
+      g->d_send_idx = hl.d_send_idx;
+      g->total_send = hl.total_send;
+      g->own_off = 0;
+      g->slot_rows = hl.ext_rows;
       OFSC_CUDA(cudaStreamSynchronize(s));
       dfree(csr.row_ptr);
       dfree(csr.col);
@@ -380,6 +408,8 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     in.reordered = g->reordered ? 1 : 0;
     in.n_communities = n_comm;
     in.intra_edge_fraction = intra;
+    in.halo_rows = g->ext_rows - g->n_local;
+    in.send_rows = g->total_send;
     trace_point("graph_build: done", s);
     *out = g;
   });
@@ -454,6 +484,26 @@ ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const
   });
 }
 
+ofsc_status ofsc_graph_exchange_plan(ofsc_graph g, int64_t* h_send_counts, int32_t* h_send_gids,
+                                     int64_t* h_recv_counts, int32_t* h_recv_gids) {
+  return guard([&] {
+    OFSC_REQUIRE(g, OFSC_ERR_ARG, "null graph");
+    for (int q = 0; q < g->p; ++q) {
+      if (h_send_counts) h_send_counts[q] = g->p > 1 ? g->send_cnt[q] : 0;
+      if (h_recv_counts) h_recv_counts[q] = g->p > 1 ? g->recv_cnt[q] : 0;
+    }
+    if (g->p == 1) return;
+    if (h_send_gids && g->total_send > 0) {
+      std::vector<int32_t> idx(g->total_send);
+      OFSC_CUDA(cudaMemcpy(idx.data(), g->d_send_idx, idx.size() * sizeof(int32_t),
+                           cudaMemcpyDeviceToHost));
+      for (int64_t t = 0; t < g->total_send; ++t) h_send_gids[t] = (int32_t)(g->row_begin + idx[t]);
+    }
+    if (h_recv_gids)
+      for (int64_t e = g->n_local; e < g->ext_rows; ++e) h_recv_gids[e - g->n_local] = g->h_gid[e];
+  });
+}
+
 ofsc_status ofsc_graph_info_get(ofsc_graph g, ofsc_graph_info* out) {
   return guard([&] {
     OFSC_REQUIRE(g && out, OFSC_ERR_ARG, "null argument");
@@ -469,21 +519,19 @@ ofsc_status ofsc_graph_copy_csr(ofsc_graph g, int64_t* h_row_ptr, int32_t* h_col
                            cudaMemcpyDeviceToHost));
     if (h_col && g->nnz_local > 0) {
       OFSC_CUDA(cudaMemcpy(h_col, g->col, g->nnz_local * sizeof(int32_t), cudaMemcpyDeviceToHost));
-      if (g->p > 1) {  // slot ids -> global ids
-        for (int64_t e = 0; e < g->nnz_local; ++e) {
-          const int64_t sid = h_col[e];
-          const int r = (int)(sid / g->slot_rows);
-          h_col[e] = (int32_t)(g->begins[r] + (sid - (int64_t)r * g->slot_rows));
-        }
-      }
+      if (g->p > 1)    // ext ids -> global ids
+        for (int64_t e = 0; e < g->nnz_local; ++e) h_col[e] = g->h_gid[h_col[e]];
     }
     if (h_s) {
-      std::vector<double> slot((size_t)g->p * g->slot_rows);
-      OFSC_CUDA(cudaMemcpy(slot.data(), g->s_slot, slot.size() * sizeof(double),
-                           cudaMemcpyDeviceToHost));
-      for (int r = 0; r < g->p; ++r)
-        for (int64_t q = g->begins[r]; q < g->begins[r + 1]; ++q)
-          h_s[q] = slot[(size_t)r * g->slot_rows + (q - g->begins[r])];
+      if (g->p == 1) {
+        OFSC_CUDA(cudaMemcpy(h_s, g->s_slot, g->n * sizeof(double), cudaMemcpyDeviceToHost));
+      } else {   // s of the rows this rank sees (own + halo); other entries are not held here
+        std::vector<double> ext(g->ext_rows);
+        OFSC_CUDA(cudaMemcpy(ext.data(), g->s_slot, ext.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost));
+        for (int64_t q = 0; q < g->n; ++q) h_s[q] = 0.0;
+        for (int64_t e = 0; e < g->ext_rows; ++e) h_s[g->h_gid[e]] = ext[e];
+      }
     }
   });
 }
@@ -514,31 +562,62 @@ ofsc_status ofsc_graph_destroy(ofsc_graph g) {
 // ---------------------------------------------------------------------------
 namespace ofsc {
 
-// internal global row g (owned by rank r) <- user row perm[g] (original node order)
-__global__ void k_to_slots(int k, int KP, int64_t n, const void* src, int64_t lds, void* dst,
-                           const int64_t* begins, int p, int64_t slot_rows, int f64,
-                           const int32_t* perm) {
-  const int64_t total = n * KP;
+// ext row e (global row gid[e], identity when gid == NULL) <- user row perm[gid]
+__global__ void k_to_ext(int k, int KP, int64_t rows, const void* src, int64_t lds, void* dst,
+                         const int32_t* gid, int f64, const int32_t* perm) {
+  const int64_t total = rows * KP;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = e / KP;
+    const int64_t r = e / KP;
     const int c = (int)(e % KP);
-    int r = 0;
-    while (r + 1 < p && begins[r + 1] <= g) ++r;
-    const int64_t id = r * slot_rows + (g - begins[r]);
+    const int64_t g = gid ? (int64_t)gid[r] : r;
     const int64_t u = perm ? (int64_t)perm[g] : g;
-    if (f64) ((double*)dst)[id * KP + c] = c < k ? ((const double*)src)[u * lds + c] : 0.0;
-    else ((float*)dst)[id * KP + c] = c < k ? ((const float*)src)[u * lds + c] : 0.0f;
+    if (f64) ((double*)dst)[r * KP + c] = c < k ? ((const double*)src)[u * lds + c] : 0.0;
+    else ((float*)dst)[r * KP + c] = c < k ? ((const float*)src)[u * lds + c] : 0.0f;
   }
 }
 
+// full user array (all n rows, original order) -> this rank's gather buffer
 static void to_slots(ofsc_graph g, ofsc_dtype dt, int k, int KP, const void* src, int64_t lds,
                      void* dst, cudaStream_t s) {
-  OFSC_CUDA(cudaMemsetAsync(dst, 0, (size_t)g->p * g->slot_rows * KP * esize(dt), s));
-  k_to_slots<<<num_sms() * 8, 256, 0, s>>>(k, KP, g->n, src, lds, dst, g->d_begins, g->p,
-                                          g->slot_rows, dt == OFSC_F64,
-                                          g->reordered ? g->perm : nullptr);
+  k_to_ext<<<num_sms() * 8, 256, 0, s>>>(k, KP, g->ext_rows, src, lds, dst, g->d_gid,
+                                         dt == OFSC_F64, g->reordered ? g->perm : nullptr);
   OFSC_LAUNCH_CHECK();
+}
+
+// Halo exchange (p > 1): pack the own rows each peer needs, then one grouped
+// send/recv per peer into the peer's halo segment of the gather buffer.
+__global__ void k_pack_rows(int64_t rows, int KP, const int32_t* idx, const void* src, void* dst,
+                            int f64) {
+  const int64_t total = rows * KP;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / KP, c = e % KP;
+    const int64_t from = (int64_t)idx[r] * KP + c;
+    if (f64) ((double*)dst)[e] = ((const double*)src)[from];
+    else ((float*)dst)[e] = ((const float*)src)[from];
+  }
+}
+
+static void halo_exchange(ofsc_graph g, ofsc_dtype dt, int KP, void* ext, void* sendbuf,
+                          cudaStream_t s) {
+  const size_t es = esize(dt);
+  if (g->total_send > 0) {
+    k_pack_rows<<<num_sms() * 8, 256, 0, s>>>(g->total_send, KP, g->d_send_idx, ext, sendbuf,
+                                             dt == OFSC_F64);
+    OFSC_LAUNCH_CHECK();
+  }
+  OFSC_NCCL(ncclGroupStart());
+  for (int q = 0; q < g->p; ++q) {
+    if (q == g->rank) continue;
+    if (g->send_cnt[q] > 0)
+      OFSC_NCCL(ncclSend((const char*)sendbuf + (size_t)g->send_off[q] * KP * es,
+                         (size_t)g->send_cnt[q] * KP, nccl_type(dt), q, g->comm->nccl, s));
+    if (g->recv_cnt[q] > 0)
+      OFSC_NCCL(ncclRecv((char*)ext + (size_t)g->recv_off[q] * KP * es,
+                         (size_t)g->recv_cnt[q] * KP, nccl_type(dt), q, g->comm->nccl, s));
+  }
+  OFSC_NCCL(ncclGroupEnd());
 }
 
 static void allreduce_d(ofsc_graph g, double* buf, size_t count, cudaStream_t s) {
@@ -572,7 +651,7 @@ ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void*
       launch_spmm_plain(dt, k, g->n_local, 0, g->row_ptr, g->col, g->s_slot, g->s32_slot, d_Z, ldz,
                         d_Y, ldy, s);
     } else {
-      DBuf zs((size_t)g->p * g->slot_rows * k * esize(dt), s);
+      DBuf zs((size_t)g->ext_rows * k * esize(dt), s);
       DBuf ys(g->user_perm() ? (size_t)std::max<int64_t>(g->n_local, 1) * k * esize(dt) : 0, s);
       to_slots(g, dt, k, k, d_Z, ldz, zs.p, s);
       launch_spmm_plain(dt, k, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
@@ -594,7 +673,7 @@ ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const 
     const int KP = padded_k(k);
     const size_t es = esize(dt);
     const int64_t nl = g->n_local;
-    DBuf zs((size_t)g->p * g->slot_rows * KP * es, s), xs(std::max<int64_t>(nl, 1) * KP * es, s),
+    DBuf zs((size_t)g->ext_rows * KP * es, s), xs(std::max<int64_t>(nl, 1) * KP * es, s),
         ys(std::max<int64_t>(nl, 1) * KP * es, s);
     to_slots(g, dt, k, KP, d_Z, ldz, zs.p, s);
     launch_copy_in(dt, k, KP, nl, d_X, ldx, xs.p, g->user_perm(), s);
@@ -636,8 +715,9 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   OFSC_CUDA(cudaMalloc(&w.AX, blk));
   OFSC_CUDA(cudaMalloc(&w.G, blk));
   OFSC_CUDA(cudaMalloc(&w.AV, blk));
-  const size_t vg = g->p == 1 ? blk : (size_t)g->p * g->slot_rows * KP * es;
+  const size_t vg = g->p == 1 ? blk : (size_t)g->ext_rows * KP * es;
   OFSC_CUDA(cudaMalloc(&w.Vg, vg));
+  if (g->p > 1) OFSC_CUDA(cudaMalloc(&w.sendbuf, (size_t)std::max<int64_t>(g->total_send, 1) * KP * es));
   const int nbmax = num_sms() * 4;   // grids of the streaming kernels are chosen per run
   w.nb2 = gram_stream_grid(dt, KP, nl);
   OFSC_CUDA(cudaMalloc(&w.part_cols, (size_t)nbmax * 2 * KP * 8));
@@ -746,13 +826,11 @@ static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaSt
   const size_t es = esize(dt);
   const void* Zg = w.X;
   if (g->p > 1) {
-    if (!w.Xg) OFSC_CUDA(cudaMalloc(&w.Xg, (size_t)g->p * g->slot_rows * p.KP * es));
-    char* slot = (char*)w.Xg + (size_t)g->own_off * p.KP * es;
+    if (!w.Xg) OFSC_CUDA(cudaMalloc(&w.Xg, (size_t)g->ext_rows * p.KP * es));
     pr.ph(OFSC_PH_COMM, 0, [&] {
-      OFSC_CUDA(cudaMemcpyAsync(slot, w.X, (size_t)g->n_local * p.KP * es,
+      OFSC_CUDA(cudaMemcpyAsync(w.Xg, w.X, (size_t)g->n_local * p.KP * es,
                                 cudaMemcpyDeviceToDevice, s));
-      OFSC_NCCL(ncclAllGather(slot, w.Xg, (size_t)g->slot_rows * p.KP, nccl_type(dt),
-                              g->comm->nccl, s));
+      halo_exchange(g, dt, p.KP, w.Xg, w.sendbuf, s);
     });
     Zg = w.Xg;
   }
@@ -786,8 +864,7 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
   pr.ph(OFSC_PH_DIRECTION_GRAM, 1, [&] { launch_direction_gram(dt, p, w.nb4, s); });
   if (g->p > 1)
     pr.ph(OFSC_PH_COMM, 0, [&] {
-      OFSC_NCCL(ncclAllGather(p.V, w.Vg, (size_t)g->slot_rows * p.KP, nccl_type(dt),
-                              g->comm->nccl, s));
+      halo_exchange(g, dt, p.KP, w.Vg, w.sendbuf, s);
     });
   pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
     launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
@@ -863,7 +940,7 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
     p.hist_code = hcode.as<int>();
     OFSC_CUDA(cudaMemsetAsync(p.hist, 0xff, (size_t)std::max(T, 1) * 4 * 8, s));  // NaN
     const size_t blk = (size_t)std::max<int64_t>(g->n_local, 1) * KP * es;
-    const size_t vg = g->p == 1 ? blk : (size_t)g->p * g->slot_rows * KP * es;
+    const size_t vg = g->p == 1 ? blk : (size_t)g->ext_rows * KP * es;
     launch_copy_in(dt, o.k, KP, g->n_local, d_X, ldx, w.X, g->user_perm(), s);
     OFSC_CUDA(cudaMemsetAsync(w.G, 0, blk, s));
     OFSC_CUDA(cudaMemsetAsync(w.AV, 0, blk, s));

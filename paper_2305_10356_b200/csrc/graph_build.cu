@@ -8,7 +8,9 @@
 // cub (CUDA toolkit) supplies the radix sort / unique / scan building blocks.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -501,6 +503,202 @@ void scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
                    const int64_t* d_begins, int p, int64_t slot_rows, cudaStream_t st) {
   k_scatter_slots<<<blocks_for(n), 256, 0, st>>>(s, n, s_slot, s32_slot, d_begins, p, slot_rows);
   OFSC_LAUNCH_CHECK();
+}
+
+// ---- halo layout (p > 1) -----------------------------
+// A rank's gather buffer holds its own rows (ext ids 0..n_local-1) followed by
+// the remote rows its columns reference ("halo"), in ascending global id, so
+// the rows owned by peer q form one contiguous segment.  The graph is
+// symmetric, so the rows q must send to r -- q's rows with a neighbour in r's
+// range -- are exactly r's halo segment from q, in the same (ascending) order:
+// both sides derive the exchange plan from the CSR alone, with no handshake.
+namespace {
+
+__device__ __forceinline__ int owner_of(int64_t g, const int64_t* begins, int p) {
+  int r = 0;
+  while (r + 1 < p && begins[r + 1] <= g) ++r;
+  return r;
+}
+
+__global__ void k_remote_flags(int64_t nnz, const int32_t* col, int64_t rb, int64_t re, int* flag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    flag[e] = (col[e] < rb || col[e] >= re) ? 1 : 0;
+}
+
+__global__ void k_remap_ext(int64_t nnz, const int32_t* col, int64_t rb, int64_t re,
+                            int64_t n_local, const int32_t* halo, int64_t h, int32_t* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = col[e];
+    if (c >= rb && c < re) {
+      out[e] = (int32_t)(c - rb);
+    } else {
+      int64_t lo = 0, hi = h;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (halo[mid] < c) lo = mid + 1;
+        else hi = mid;
+      }
+      out[e] = (int32_t)(n_local + lo);
+    }
+  }
+}
+
+// flag[r * n_local + i] = 1 iff own row i has a neighbour owned by rank r != self
+__global__ void k_send_flags(int64_t n_local, const int64_t* row_ptr, const int32_t* col,
+                             const int64_t* begins, int p, int self, unsigned char* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < n_local; i += nw)
+    for (int64_t q = row_ptr[i] + lane; q < row_ptr[i + 1]; q += 32) {
+      const int r = owner_of(col[q], begins, p);
+      if (r != self) flag[(int64_t)r * n_local + i] = 1;   // benign race: all write 1
+    }
+}
+
+__global__ void k_gather_s(int64_t rows, const int32_t* gid, const double* s, double* s_ext,
+                           float* s32_ext) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = gid[e] >= 0 ? s[gid[e]] : 0.0;
+    s_ext[e] = v;
+    s32_ext[e] = (float)v;
+  }
+}
+
+__global__ void k_iota32(int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+}  // namespace
+
+void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_begins, int p,
+                int rank, HaloLayout& out, cudaStream_t st) {
+  keep_pool();
+  const int64_t rb = h_begins[rank], re = h_begins[rank + 1];
+  const int64_t nl = re - rb;
+  std::vector<int64_t> rp_ends(2);
+  OFSC_CUDA(cudaMemcpyAsync(&rp_ends[0], csr.row_ptr + rb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaMemcpyAsync(&rp_ends[1], csr.row_ptr + re, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaStreamSynchronize(st));
+  const int64_t e0 = rp_ends[0], nnz = rp_ends[1] - rp_ends[0];
+  const int32_t* gcol = csr.col + e0;
+  out.n_local = nl;
+  // 1. halo ids: unique remote columns, ascending
+  int64_t h = 0;
+  DevBuf<int32_t> halo(nnz > 0 ? nnz : 1, st);
+  if (nnz > 0) {
+    DevBuf<int> flag(nnz, st);
+    DevBuf<int32_t> rem(nnz, st), rem_sorted(nnz, st);
+    DevBuf<int64_t> nsel(1, st);
+    k_remote_flags<<<blocks_for(nnz), 256, 0, st>>>(nnz, gcol, rb, re, flag.p);
+    OFSC_LAUNCH_CHECK();
+    size_t tb = 0;
+    OFSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, gcol, flag.p, rem.p, nsel.p, nnz, st));
+    {
+      DevBuf<char> tmp(tb, st);
+      OFSC_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, gcol, flag.p, rem.p, nsel.p, nnz, st));
+    }
+    int64_t nrem = 0;
+    OFSC_CUDA(cudaMemcpyAsync(&nrem, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaStreamSynchronize(st));
+    if (nrem > 0) {
+      tb = 0;
+      OFSC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, rem.p, rem_sorted.p, nrem, 0, 32, st));
+      {
+        DevBuf<char> tmp(tb, st);
+        OFSC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, rem.p, rem_sorted.p, nrem, 0, 32, st));
+      }
+      tb = 0;
+      OFSC_CUDA(cub::DeviceSelect::Unique(nullptr, tb, rem_sorted.p, halo.p, nsel.p, nrem, st));
+      {
+        DevBuf<char> tmp(tb, st);
+        OFSC_CUDA(cub::DeviceSelect::Unique(tmp.p, tb, rem_sorted.p, halo.p, nsel.p, nrem, st));
+      }
+      OFSC_CUDA(cudaMemcpyAsync(&h, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      OFSC_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  out.ext_rows = nl + h;
+  out.h_gid.resize(out.ext_rows);
+  for (int64_t i = 0; i < nl; ++i) out.h_gid[i] = (int32_t)(rb + i);
+  if (h > 0)
+    OFSC_CUDA(cudaMemcpy(out.h_gid.data() + nl, halo.p, h * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  OFSC_CUDA(cudaMalloc(&out.d_gid, std::max<int64_t>(out.ext_rows, 1) * sizeof(int32_t)));
+  OFSC_CUDA(cudaMemcpy(out.d_gid, out.h_gid.data(), out.ext_rows * sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
+  // 2. local CSR: rebased row pointers, columns -> ext ids; s on the ext rows
+  OFSC_CUDA(cudaMalloc(&out.row_ptr, (nl + 1) * sizeof(int64_t)));
+  OFSC_CUDA(cudaMalloc(&out.col, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+  rebase_row_ptr(csr.row_ptr + rb, nl, e0, out.row_ptr, st);
+  if (nnz > 0) {
+    k_remap_ext<<<blocks_for(nnz), 256, 0, st>>>(nnz, gcol, rb, re, nl, halo.p, h, out.col);
+    OFSC_LAUNCH_CHECK();
+  }
+  out.nnz_local = nnz;
+  OFSC_CUDA(cudaMalloc(&out.s_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(double)));
+  OFSC_CUDA(cudaMalloc(&out.s32_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(float)));
+  k_gather_s<<<blocks_for(std::max<int64_t>(out.ext_rows, 1)), 256, 0, st>>>(
+      out.ext_rows, out.d_gid, csr.s, out.s_ext, out.s32_ext);
+  OFSC_LAUNCH_CHECK();
+  // 3. receive plan: halo segment owned by each peer
+  out.recv_cnt.assign(p, 0);
+  out.recv_off.assign(p, nl);
+  for (int q = 0; q < p; ++q) {
+    const auto lo = std::lower_bound(out.h_gid.begin() + nl, out.h_gid.end(), (int32_t)h_begins[q]);
+    const auto hi = std::lower_bound(out.h_gid.begin() + nl, out.h_gid.end(), (int32_t)h_begins[q + 1]);
+    out.recv_off[q] = lo - out.h_gid.begin();
+    out.recv_cnt[q] = hi - lo;
+  }
+  // 4. send plan: own rows with a neighbour owned by each peer (ascending)
+  out.send_cnt.assign(p, 0);
+  out.send_off.assign(p + 1, 0);
+  DevBuf<unsigned char> sflag((size_t)p * std::max<int64_t>(nl, 1), st);
+  OFSC_CUDA(cudaMemsetAsync(sflag.p, 0, (size_t)p * std::max<int64_t>(nl, 1), st));
+  if (nnz > 0) {
+    const int64_t wb = (nl * 32 + 255) / 256;
+    k_send_flags<<<(int)std::min<int64_t>(std::max<int64_t>(wb, 1), (int64_t)num_sms() * 16), 256, 0,
+                   st>>>(nl, csr.row_ptr + rb, csr.col, d_begins, p, rank, sflag.p);
+    // (global row pointers: absolute offsets into the full csr.col)
+    OFSC_LAUNCH_CHECK();
+  }
+  std::vector<int32_t> send_idx;
+  {
+    DevBuf<int32_t> iota(std::max<int64_t>(nl, 1), st), sel(std::max<int64_t>(nl, 1), st);
+    DevBuf<int64_t> nsel(1, st);
+    k_iota32<<<blocks_for(std::max<int64_t>(nl, 1)), 256, 0, st>>>(nl, iota.p);
+    OFSC_LAUNCH_CHECK();
+    for (int q = 0; q < p; ++q) {
+      out.send_off[q + 1] = out.send_off[q];
+      if (q == rank || nl == 0) continue;
+      size_t tb = 0;
+      OFSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, sflag.p + (size_t)q * nl, sel.p,
+                                           nsel.p, nl, st));
+      DevBuf<char> tmp(tb, st);
+      OFSC_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, iota.p, sflag.p + (size_t)q * nl, sel.p,
+                                           nsel.p, nl, st));
+      int64_t cnt = 0;
+      OFSC_CUDA(cudaMemcpyAsync(&cnt, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      OFSC_CUDA(cudaStreamSynchronize(st));
+      const size_t old = send_idx.size();
+      send_idx.resize(old + cnt);
+      if (cnt > 0)
+        OFSC_CUDA(cudaMemcpy(send_idx.data() + old, sel.p, cnt * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost));
+      out.send_cnt[q] = cnt;
+      out.send_off[q + 1] = out.send_off[q] + cnt;
+    }
+  }
+  out.total_send = (int64_t)send_idx.size();
+  OFSC_CUDA(cudaMalloc(&out.d_send_idx, std::max<int64_t>(out.total_send, 1) * sizeof(int32_t)));
+  if (out.total_send > 0)
+    OFSC_CUDA(cudaMemcpy(out.d_send_idx, send_idx.data(), out.total_send * sizeof(int32_t),
+                         cudaMemcpyHostToDevice));
+  OFSC_CUDA(cudaStreamSynchronize(st));
 }
 
 __global__ void k_rebase(const int64_t* in, int64_t rows, int64_t base, int64_t* out) {

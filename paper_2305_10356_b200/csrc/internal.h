@@ -198,6 +198,21 @@ void remap_columns(const int32_t* col_in, int64_t nnz, int32_t* col_out, const i
 void scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
                    const int64_t* d_begins, int p, int64_t slot_rows, cudaStream_t st);
 void rebase_row_ptr(const int64_t* in, int64_t rows, int64_t base, int64_t* out, cudaStream_t st);
+// halo layout of one rank (p > 1): own rows then the referenced remote rows
+struct HaloLayout {
+  int64_t n_local = 0, ext_rows = 0, nnz_local = 0, total_send = 0;
+  int64_t* row_ptr = nullptr;        // [n_local + 1], from 0
+  int32_t* col = nullptr;            // [nnz_local] ext ids
+  double* s_ext = nullptr;           // [ext_rows]
+  float* s32_ext = nullptr;
+  int32_t* d_gid = nullptr;          // [ext_rows] global id of each ext row
+  std::vector<int32_t> h_gid;
+  std::vector<int64_t> recv_cnt, recv_off;   // per peer: rows, first ext row
+  std::vector<int64_t> send_cnt, send_off;   // per peer: rows, offset into d_send_idx
+  int32_t* d_send_idx = nullptr;     // [total_send] own row index to send (grouped by peer)
+};
+void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_begins, int p,
+                int rank, HaloLayout& out, cudaStream_t st);
 
 }  // namespace ofsc
 

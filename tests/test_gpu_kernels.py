@@ -222,3 +222,38 @@ def test_multirank_layout_with_local_comms(p, reorder):
     assert np.all(covered == 1)
     for got, w in zip(Gsum, want):
         assert rel(got, w) <= 1e-13
+
+
+@pytest.mark.parametrize("p", [2, 3, 8])
+@pytest.mark.parametrize("reorder", [False, True])
+def test_halo_exchange_plan_is_consistent(p, reorder):
+    """Halo layout (p > 1): every rank's receive list from q is exactly q's send
+    list to it (same rows, same order), the halo is the set of remote columns
+    of the rank's rows, and with reordering the halo shrinks (communities stay
+    on one rank).  The grouped ncclSend/ncclRecv of the iteration moves exactly
+    these rows, so this is the exchange's correctness condition."""
+    s, d, n = GRAPHS["c2"]()
+    plans, halos = {}, {}
+    for r in range(p):
+        comm = ofsc.LocalComm(p, r)
+        g = ofsc.Graph(n, s, d, comm=comm, reorder=reorder)
+        info = g.info
+        rb, re_ = info["row_begin"], info["row_end"]
+        sc, sg, rc, rg = g.exchange_plan()
+        assert sc[r] == 0 and rc[r] == 0 and sc.sum() == info["send_rows"] and rc.sum() == info["halo_rows"]
+        rp, col, _ = g.copy_csr()                  # global (internal-order) column ids
+        remote = np.unique(col[(col < rb) | (col >= re_)])
+        assert np.array_equal(rg, remote)
+        plans[r] = (np.concatenate([[0], np.cumsum(sc)]), sg, np.concatenate([[0], np.cumsum(rc)]), rg)
+        halos[r] = remote.size
+        g.close()
+        comm.close()
+    for q in range(p):
+        for r in range(p):
+            if q == r:
+                continue
+            so, sg = plans[q][0], plans[q][1]
+            ro, rg = plans[r][2], plans[r][3]
+            assert np.array_equal(sg[so[r]:so[r + 1]], rg[ro[q]:ro[q + 1]]), (q, r)
+    if reorder:
+        assert sum(halos.values()) < 0.9 * (p - 1) * n     # far below an all-gather
