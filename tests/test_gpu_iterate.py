@@ -208,3 +208,54 @@ def test_p2_reordered_graph(name, method):
     o = run_ofm(op, method, X0, 10, refresh=0)
     X, r = gpu_run(gr, method, X0, 10)
     assert rel(X, o.X) <= 1e-10
+
+
+_WIDE = {}
+
+
+def setup_wide(k):
+    """c3-shaped DCSBM at a ragged N = 20,011 for the KP = 48 / 64 kernels
+    (symmetric DMMA Grams, register-resident M/W fragments), k = 48 or 64."""
+    if k not in _WIDE:
+        n = 20_011
+        s, d, _ = dcsbm_graph(n, 24, 160_000, 3.0, 401 + k, 5.0)
+        op = build_operator(n, s, d)
+        g = ofsc.Graph(n, s, d, reorder=True)
+        X0 = x0_block(n, k, 402 + k)
+        _WIDE[k] = (op, g, X0)
+    return _WIDE[k]
+
+
+@pytest.mark.parametrize("k", [48, 64])
+@pytest.mark.parametrize("method", METHODS)
+def test_p2_wide_kernels(k, method):
+    """P1 + P2 on the padded widths of the production configs (c3/c4: k = 64,
+    c5: k = 48), reordered graph as in bench.py: one step 1e-12 with identical
+    branch codes, ten steps 1e-10 (north-star tolerance)."""
+    op, g, X0 = setup_wide(k)
+    o1 = run_ofm(op, method, X0, 1, refresh=0)
+    X1, r1 = gpu_run(g, method, X0, 1)
+    assert rel(X1, o1.X) <= 1e-12
+    assert list(r1.codes[0]) == list(o1.codes[0])
+    o = run_ofm(op, method, X0, 10, refresh=0)
+    X, r = gpu_run(g, method, X0, 10)
+    assert rel(X, o.X) <= 1e-10
+    assert np.allclose(r.history[:, :2], o.history[:, :2], rtol=1e-9, atol=0)
+
+
+def test_full_size_c4_two_iterations():
+    """BASELINE c4 at full size (N = 5M, E = 50M, k = 64) in the bench launch
+    configuration (LPA-reordered graph, OFM-f2): two whole iterations (the
+    second with the PR+ beta) against the oracle's Algorithm 2 on all rows."""
+    cfg = CONFIGS["c4"]
+    s, d, _ = config_graph(cfg)
+    op = build_operator(cfg.n, s, d)
+    g = ofsc.Graph(cfg.n, s, d, reorder=True)
+    X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
+    o = run_ofm(op, "ofm_f2", X0, 2, refresh=0)
+    X, r = gpu_run(g, "ofm_f2", X0, 2)
+    assert r.report["iters"] == 2
+    assert [list(c) for c in r.codes] == [list(c) for c in o.codes]
+    assert np.max(np.abs(r.alphas - np.array(o.alphas))) <= 1e-12 * np.max(np.abs(o.alphas))
+    assert rel(X, o.X) <= 1e-12
+    g.close()
