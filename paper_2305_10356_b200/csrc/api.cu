@@ -70,6 +70,8 @@ struct Workspace {
   int KP = 0;
   void *X = nullptr, *AX = nullptr, *G = nullptr, *AV = nullptr, *Vg = nullptr, *Xg = nullptr;
   void* sendbuf = nullptr;  // p > 1: packed rows of the halo exchange
+  cudaStream_t comm_st = nullptr;            // p > 1: halo exchange overlapped with the SpMM
+  cudaEvent_t ev_v = nullptr, ev_x = nullptr;
   double *part_cols = nullptr, *part_g4 = nullptr, *part_g2 = nullptr, *grams = nullptr;
   double* state = nullptr;  // M, W [KP*KP each], alpha, beta, gg_prev [KP], colred [2KP]
   DevCtl* ctl = nullptr;
@@ -81,6 +83,11 @@ struct Workspace {
   void release() {
     if (cap) cudaStreamDestroy(cap);
     cap = nullptr;
+    if (comm_st) cudaStreamDestroy(comm_st);
+    if (ev_v) cudaEventDestroy(ev_v);
+    if (ev_x) cudaEventDestroy(ev_x);
+    comm_st = nullptr;
+    ev_v = ev_x = nullptr;
     if (e_iter) cudaGraphExecDestroy(e_iter);
     if (e_refresh) cudaGraphExecDestroy(e_refresh);
     if (g_iter) cudaGraphDestroy(g_iter);
@@ -122,6 +129,11 @@ struct ofsc_graph_s {
   std::vector<int64_t> recv_cnt, recv_off, send_cnt, send_off;
   int32_t* d_send_idx = nullptr;   // own rows to send, grouped by peer
   int64_t total_send = 0;
+  // the local CSR split per row: own-row columns | halo columns (p > 1, for the overlap)
+  int64_t* row_ptr_loc = nullptr;
+  int32_t* col_loc = nullptr;
+  int64_t* row_ptr_rem = nullptr;
+  int32_t* col_rem = nullptr;
   int32_t* cid = nullptr;          // community of each internal row (reordered graphs)
   int64_t* cstart = nullptr;       // community start rows [n_comm + 1]
   bool reordered = false;
@@ -251,6 +263,10 @@ static void graph_free(ofsc_graph g) {
   dfree(g->cstart);
   dfree(g->d_gid);
   dfree(g->d_send_idx);
+  dfree(g->row_ptr_loc);
+  dfree(g->col_loc);
+  dfree(g->row_ptr_rem);
+  dfree(g->col_rem);
 }
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
@@ -368,6 +384,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       } catch (...) {
         dfree(hl.row_ptr); dfree(hl.col); dfree(hl.s_ext); dfree(hl.s32_ext);
         dfree(hl.d_gid); dfree(hl.d_send_idx);
+        dfree(hl.row_ptr_loc); dfree(hl.col_loc); dfree(hl.row_ptr_rem); dfree(hl.col_rem);
         free_csr();
         throw;
       }
@@ -384,6 +401,10 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       g->send_off = hl.send_off;
       g->d_send_idx = hl.d_send_idx;
       g->total_send = hl.total_send;
+      g->row_ptr_loc = hl.row_ptr_loc;
+      g->col_loc = hl.col_loc;
+      g->row_ptr_rem = hl.row_ptr_rem;
+      g->col_rem = hl.col_rem;
       g->own_off = 0;
       g->slot_rows = hl.ext_rows;
       OFSC_CUDA(cudaStreamSynchronize(s));
@@ -683,8 +704,16 @@ ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const 
         gr((size_t)4 * KP * KP * 8, s);
     const char* zown = (const char*)zs.p + (size_t)g->own_off * KP * es;
     launch_gram_pair(dt, KP, nl, zown, zown, xs.p, p4.as<double>(), nb, s);
-    launch_spmm_gram(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p,
-                     xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s);
+    if (g->p > 1) {   // the iteration's split form: own-row columns, then halo columns
+      launch_spmm(dt, KP, nl, 0, g->row_ptr_loc, g->col_loc, g->s_slot, g->s32_slot, zs.p, ys.p,
+                  nullptr, s, nullptr, nullptr, nullptr, 1);
+      launch_spmm(dt, KP, nl, 0, g->row_ptr_rem, g->col_rem, g->s_slot, g->s32_slot, zs.p, ys.p,
+                  nullptr, s, nullptr, nullptr, nullptr, 2);
+      launch_gram_stream(dt, KP, nl, zown, xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s);
+    } else {
+      launch_spmm_gram(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p,
+                       xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s);
+    }
     launch_reduce_partials(p4.as<double>(), nb, 2 * KP * KP, gr.as<double>(), s);
     launch_reduce_partials(p2.as<double>(), nb2, 2 * KP * KP, gr.as<double>() + 2 * KP * KP, s);
     allreduce_d(g, gr.as<double>(), 4 * KP * KP, s);
@@ -717,7 +746,12 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   OFSC_CUDA(cudaMalloc(&w.AV, blk));
   const size_t vg = g->p == 1 ? blk : (size_t)g->ext_rows * KP * es;
   OFSC_CUDA(cudaMalloc(&w.Vg, vg));
-  if (g->p > 1) OFSC_CUDA(cudaMalloc(&w.sendbuf, (size_t)std::max<int64_t>(g->total_send, 1) * KP * es));
+  if (g->p > 1) {
+    OFSC_CUDA(cudaMalloc(&w.sendbuf, (size_t)std::max<int64_t>(g->total_send, 1) * KP * es));
+    OFSC_CUDA(cudaStreamCreateWithFlags(&w.comm_st, cudaStreamNonBlocking));
+    OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_v, cudaEventDisableTiming));
+    OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_x, cudaEventDisableTiming));
+  }
   const int nbmax = num_sms() * 4;   // grids of the streaming kernels are chosen per run
   w.nb2 = gram_stream_grid(dt, KP, nl);
   OFSC_CUDA(cudaMalloc(&w.part_cols, (size_t)nbmax * 2 * KP * 8));
@@ -842,6 +876,15 @@ static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaSt
   pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, p.M, 2 * (size_t)p.KP * p.KP, s); });
 }
 
+static bool overlap_exchange() {   // OFSC_NO_OVERLAP=1: exchange, then one SpMM pass
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("OFSC_NO_OVERLAP");
+    env = (e && e[0] == '1') ? 0 : 1;
+  }
+  return env == 1;
+}
+
 // One iteration of Algorithm 2 (l.8-12), the R-mode schedule of DESIGN.md:
 // C3 -> beta -> C4 -> [all-gather V] -> C2 -> Gram reduce -> [all-reduce] -> line search.
 static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool refresh,
@@ -862,15 +905,31 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     pr.ph(OFSC_PH_BETA, 1, [&] { launch_beta(p, w.nb3, 1, s); });
   }
   pr.ph(OFSC_PH_DIRECTION_GRAM, 1, [&] { launch_direction_gram(dt, p, w.nb4, s); });
-  if (g->p > 1)
-    pr.ph(OFSC_PH_COMM, 0, [&] {
-      halo_exchange(g, dt, p.KP, w.Vg, w.sendbuf, s);
+  if (g->p > 1 && overlap_exchange() && !pr.timing) {
+    // halo exchange on the comm stream while the SpMM sums the own-row columns;
+    // the halo columns are added once the exchange lands
+    OFSC_CUDA(cudaEventRecord(w.ev_v, s));
+    OFSC_CUDA(cudaStreamWaitEvent(w.comm_st, w.ev_v, 0));
+    halo_exchange(g, dt, p.KP, w.Vg, w.sendbuf, w.comm_st);
+    OFSC_CUDA(cudaEventRecord(w.ev_x, w.comm_st));
+    pr.ph(OFSC_PH_SPMM_GRAM, 2, [&] {
+      launch_spmm(dt, p.KP, g->n_local, 0, g->row_ptr_loc, g->col_loc, g->s_slot, g->s32_slot,
+                  w.Vg, w.AV, &p.ctl->stop, s, nullptr, nullptr, w.ctr, 1);
+      OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_x, 0));
+      launch_spmm(dt, p.KP, g->n_local, 0, g->row_ptr_rem, g->col_rem, g->s_slot, g->s32_slot,
+                  w.Vg, w.AV, &p.ctl->stop, s, nullptr, nullptr, w.ctr, 2);
     });
-  pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
-    launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
-                w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
-                g->p == 1 ? g->cstart : nullptr, w.ctr);
-  });
+  } else {
+    if (g->p > 1)
+      pr.ph(OFSC_PH_COMM, 0, [&] {
+        halo_exchange(g, dt, p.KP, w.Vg, w.sendbuf, s);
+      });
+    pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
+      launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
+                  w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
+                  g->p == 1 ? g->cstart : nullptr, w.ctr);
+    });
+  }
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {
     launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
   });

@@ -568,6 +568,36 @@ __global__ void k_gather_s(int64_t rows, const int32_t* gid, const double* s, do
   }
 }
 
+__global__ void k_local_count(int64_t n_local, const int64_t* row_ptr, const int32_t* col,
+                              int64_t* cnt_loc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_local;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; ++q) c += col[q] < n_local;
+    cnt_loc[i] = c;
+  }
+}
+
+// stable split of every row's columns: local ext ids (< n_local) | halo ext ids
+__global__ void k_split_rows(int64_t n_local, const int64_t* row_ptr, const int32_t* col,
+                             const int64_t* ptr_loc, int32_t* col_loc, int32_t* col_rem) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_local;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = ptr_loc[i], b = row_ptr[i] - ptr_loc[i];   // remote offset = row_ptr - ptr_loc
+    for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; ++q) {
+      const int32_t c = col[q];
+      if (c < n_local) col_loc[a++] = c;
+      else col_rem[b++] = c;
+    }
+  }
+}
+
+__global__ void k_sub_ptr(int64_t n1, const int64_t* a, const int64_t* b, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+
 __global__ void k_iota32(int64_t n, int32_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -640,6 +670,31 @@ void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_
     OFSC_LAUNCH_CHECK();
   }
   out.nnz_local = nnz;
+  // 2b. the same CSR split per row into local columns | halo columns (order kept):
+  //     the local part runs while the halo is exchanged
+  {
+    DevBuf<int64_t> cnt(std::max<int64_t>(nl, 1), st);
+    OFSC_CUDA(cudaMalloc(&out.row_ptr_loc, (nl + 1) * sizeof(int64_t)));
+    OFSC_CUDA(cudaMalloc(&out.row_ptr_rem, (nl + 1) * sizeof(int64_t)));
+    OFSC_CUDA(cudaMalloc(&out.col_loc, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+    OFSC_CUDA(cudaMalloc(&out.col_rem, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+    OFSC_CUDA(cudaMemsetAsync(out.row_ptr_loc, 0, (nl + 1) * sizeof(int64_t), st));
+    if (nl > 0) {
+      k_local_count<<<blocks_for(nl), 256, 0, st>>>(nl, out.row_ptr, out.col, cnt.p);
+      OFSC_LAUNCH_CHECK();
+      size_t tb = 0;
+      OFSC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, cnt.p, out.row_ptr_loc + 1, nl, st));
+      DevBuf<char> tmp(tb, st);
+      OFSC_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, cnt.p, out.row_ptr_loc + 1, nl, st));
+      k_sub_ptr<<<blocks_for(nl + 1), 256, 0, st>>>(nl + 1, out.row_ptr, out.row_ptr_loc,
+                                                     out.row_ptr_rem);
+      k_split_rows<<<blocks_for(nl), 256, 0, st>>>(nl, out.row_ptr, out.col, out.row_ptr_loc,
+                                                  out.col_loc, out.col_rem);
+      OFSC_LAUNCH_CHECK();
+    } else {
+      OFSC_CUDA(cudaMemsetAsync(out.row_ptr_rem, 0, sizeof(int64_t), st));
+    }
+  }
   OFSC_CUDA(cudaMalloc(&out.s_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(double)));
   OFSC_CUDA(cudaMalloc(&out.s32_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(float)));
   k_gather_s<<<blocks_for(std::max<int64_t>(out.ext_rows, 1)), 256, 0, st>>>(

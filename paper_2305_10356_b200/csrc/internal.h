@@ -90,8 +90,8 @@ struct IterParams {
 // ---- launchers (kernels_*.cu) ----
 int grid_rows(int64_t n_rows, int blocks_per_sm);
 int num_sms();
-void keep_pool();
-void trace_point(const char* what, cudaStream_t st);   // OFSC_TRACE=1: phase timestamps   // default mempool keeps freed scratch (no per-build re-mapping)
+void keep_pool();    // default mempool keeps freed scratch (no per-build re-mapping)
+void trace_point(const char* what, cudaStream_t st);   // OFSC_TRACE=1: phase timestamps
 
 // grid sizes of the TMA-pipelined streaming kernels (<= 4 * #SMs)
 int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n);
@@ -114,7 +114,8 @@ void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid = nullptr,
-                 const int64_t* cstart = nullptr, unsigned long long* ctr = nullptr);
+                 const int64_t* cstart = nullptr, unsigned long long* ctr = nullptr,
+                 int phase = 0);   // 1: raw partial sums into Y; 2: continue from Y and finish
 constexpr int kSpmmChunk = 8;  // rows per dynamic work grab of the SpMM
 // C2b: TMA-streamed Gram pair over own rows (mode 0: Z^T Y, X^T Y; mode 1: Z^T Z, Z^T Y)
 int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n);
@@ -203,6 +204,10 @@ struct HaloLayout {
   int64_t n_local = 0, ext_rows = 0, nnz_local = 0, total_send = 0;
   int64_t* row_ptr = nullptr;        // [n_local + 1], from 0
   int32_t* col = nullptr;            // [nnz_local] ext ids
+  int64_t* row_ptr_loc = nullptr;    // the same rows split: columns < n_local (own rows) ...
+  int32_t* col_loc = nullptr;
+  int64_t* row_ptr_rem = nullptr;    // ... and halo columns (>= n_local), each in CSR order
+  int32_t* col_rem = nullptr;
   double* s_ext = nullptr;           // [ext_rows]
   float* s32_ext = nullptr;
   int32_t* d_gid = nullptr;          // [ext_rows] global id of each ext row

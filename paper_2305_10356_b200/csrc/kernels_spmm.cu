@@ -70,7 +70,10 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
        const int* stop, unsigned long long* __restrict__ ctr, int ch, int c0,
-       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart) {
+       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart, int phase) {
+  // phase 0: Y = A Z (whole rows); 1: Y <- raw neighbour sums over this CSR (the
+  // local columns of a multi-GPU rank, while the halo is in flight); 2: continue
+  // the sums from Y over this CSR (the halo columns) and finish Y = -Z_i - s_i sum
   if (stop && *stop) return;
   uint64_t pf = 0, pn = 0;
   if constexpr (HINT) {
@@ -119,6 +122,14 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       hi = (int)cstart[ci + 1];
     }
     T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    if (phase == 2) {
+      const T* yp = Y + i * KP + c0 + 2 * l;
+      const V2 p0 = *reinterpret_cast<const V2*>(yp), p1 = *reinterpret_cast<const V2*>(yp + H2);
+      a0 = p0.x;
+      a1 = p0.y;
+      a2 = p1.x;
+      a3 = p1.y;
+    }
     int64_t e = beg;
     for (; e + 8 <= end; e += 8) {
       int c[8];
@@ -165,16 +176,23 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       a2 = fma(sv, z1.x, a2);
       a3 = fma(sv, z1.y, a3);
     }
-    const T* zo = Zg + (own_off + i) * KP + c0 + 2 * l;
-    const V2 o0 = *reinterpret_cast<const V2*>(zo), o1 = *reinterpret_cast<const V2*>(zo + H2);
-    T si;
-    if constexpr (sizeof(T) == 8) si = (T)s[own_off + i];
-    else si = s32[own_off + i];
     V2 y0, y1;
-    y0.x = -o0.x - si * a0;
-    y0.y = -o0.y - si * a1;
-    y1.x = -o1.x - si * a2;
-    y1.y = -o1.y - si * a3;
+    if (phase == 1) {                              // raw partial sums
+      y0.x = a0;
+      y0.y = a1;
+      y1.x = a2;
+      y1.y = a3;
+    } else {
+      const T* zo = Zg + (own_off + i) * KP + c0 + 2 * l;
+      const V2 o0 = *reinterpret_cast<const V2*>(zo), o1 = *reinterpret_cast<const V2*>(zo + H2);
+      T si;
+      if constexpr (sizeof(T) == 8) si = (T)s[own_off + i];
+      else si = s32[own_off + i];
+      y0.x = -o0.x - si * a0;
+      y0.y = -o0.y - si * a1;
+      y1.x = -o1.x - si * a2;
+      y1.y = -o1.y - si * a3;
+    }
     if constexpr (HINT) {
       stg2h(Y + i * KP + c0 + 2 * l, y0, pf);
       stg2h(Y + i * KP + c0 + 2 * l + H2, y1, pf);
@@ -204,7 +222,7 @@ int spmm_grid(int64_t n_local) {  // resident CTAs (3 per SM) for the chunked sc
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart,
-                 unsigned long long* ctr) {
+                 unsigned long long* ctr, int phase) {
   // cid / cstart: community layout of reordered graphs (p == 1), for the L2 hints.
   const int hint = (cid && cstart && own_off == 0) ? env_int("OFSC_SPMM_HINT", 0) : 0;
   const int nb = spmm_grid(n_local);
@@ -220,10 +238,10 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #define OFSC_SPMM_LAUNCH_H(CWC, H)                                                              \
     if (dt == OFSC_F64)                                                                         \
       k_spmm<double, KPC, CWC, H><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32, \
-          (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart);                         \
+          (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart, phase);                  \
     else                                                                                        \
       k_spmm<float, KPC, CWC, H><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,  \
-          (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart);
+          (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, phase);
 #define OFSC_SPMM_LAUNCH(CWC) \
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
