@@ -64,14 +64,14 @@ __device__ __forceinline__ void stg2h(float* p, float2 v, uint64_t pol) {
                "l"(pol));
 }
 
-template <typename T, int KP, int CW, int HINT>
+template <typename T, int KP, int CW, int HINT, int PHASE>
 __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
        const int* stop, unsigned long long* __restrict__ ctr, int ch, int c0,
-       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart, int phase) {
-  // phase 0: Y = A Z (whole rows); 1: Y <- raw neighbour sums over this CSR (the
+       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart) {
+  // PHASE 0: Y = A Z (whole rows); 1: Y <- raw neighbour sums over this CSR (the
   // local columns of a multi-GPU rank, while the halo is in flight); 2: continue
   // the sums from Y over this CSR (the halo columns) and finish Y = -Z_i - s_i sum
   if (stop && *stop) return;
@@ -122,7 +122,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       hi = (int)cstart[ci + 1];
     }
     T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    if (phase == 2) {
+    if constexpr (PHASE == 2) {
       const T* yp = Y + i * KP + c0 + 2 * l;
       const V2 p0 = *reinterpret_cast<const V2*>(yp), p1 = *reinterpret_cast<const V2*>(yp + H2);
       a0 = p0.x;
@@ -177,7 +177,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       a3 = fma(sv, z1.y, a3);
     }
     V2 y0, y1;
-    if (phase == 1) {                              // raw partial sums
+    if constexpr (PHASE == 1) {                    // raw partial sums
       y0.x = a0;
       y0.y = a1;
       y1.x = a2;
@@ -229,28 +229,33 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   const int ch = env_int("OFSC_SPMM_CHUNK", kSpmmChunk);   // rows per work grab (tuning knob)
   int cw = env_int("OFSC_SPMM_CW", spmm_col_window(dt, KP));  // columns per pass (tuning knob)
   if (cw != 16 && cw != 32) cw = KP;
+  if (phase) cw = KP;                       // split (multi-GPU) passes use whole rows
   if (KP % cw) cw = KP;
   const int passes = KP / cw;
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
     unsigned long long* c = ctr ? ctr + ps : nullptr;
     const int c0 = ps * cw;
-#define OFSC_SPMM_LAUNCH_H(CWC, H)                                                              \
+#define OFSC_SPMM_LAUNCH_P(CWC, H, PH)                                                          \
     if (dt == OFSC_F64)                                                                         \
-      k_spmm<double, KPC, CWC, H><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32, \
-          (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart, phase);                  \
+      k_spmm<double, KPC, CWC, H, PH><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, \
+          s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart);                    \
     else                                                                                        \
-      k_spmm<float, KPC, CWC, H><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, s32,  \
-          (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, phase);
+      k_spmm<float, KPC, CWC, H, PH><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s,  \
+          s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart);
+#define OFSC_SPMM_LAUNCH_H(CWC, H) OFSC_SPMM_LAUNCH_P(CWC, H, 0)
 #define OFSC_SPMM_LAUNCH(CWC) \
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
-      if (cw == KPC) { OFSC_SPMM_LAUNCH(KPC) }
+      if (phase == 1) { OFSC_SPMM_LAUNCH_P(KPC, 0, 1) }
+      else if (phase == 2) { OFSC_SPMM_LAUNCH_P(KPC, 0, 2) }
+      else if (cw == KPC) { OFSC_SPMM_LAUNCH(KPC) }
       else if (cw == 32) { if constexpr (KPC % 32 == 0) { OFSC_SPMM_LAUNCH(32) } }
       else { if constexpr (KPC % 16 == 0) { OFSC_SPMM_LAUNCH(16) } }
     });
 #undef OFSC_SPMM_LAUNCH
 #undef OFSC_SPMM_LAUNCH_H
+#undef OFSC_SPMM_LAUNCH_P
     OFSC_LAUNCH_CHECK();
   }
 }
