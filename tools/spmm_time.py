@@ -15,6 +15,8 @@ for name in (sys.argv[1:] or ["c4"]):
     X = torch.from_numpy(x0_block(cfg.n, cfg.k, cfg.seed_x0)).cuda()
     r = ofsc.run(g, "ofm_f2", X, 12, timing_skip=2, profile=True)
     km = r.report["kernel_ms"]
-    print(json.dumps({"config": name, "spmm_ms": km[3] / 10, "iter_ms": sum(km) / 10,
+    print(json.dumps({"config": name, "spmm_ms": km[3] / 10, "gram_stream_ms": km[8] / 10,
+                      "update_direction_ms": km[0] / 10, "direction_gram_ms": km[2] / 10,
+                      "iter_ms": sum(km) / 10,
                       "checksum": float(X.double().sum())}), flush=True)
     g.close()
