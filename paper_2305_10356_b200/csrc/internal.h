@@ -50,6 +50,7 @@ struct DevCtl {
   int n_three;   // line searches that chose among three real roots
   int n_zero;    // degenerate cubics
   double gnorm0, gnorm, obj;
+  int limit;     // device-side loop (CUDA graph while node): run while iter < limit && !stop
 };
 
 // Everything the per-iteration kernels need, passed by value.
