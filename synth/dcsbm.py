@@ -41,6 +41,9 @@ CONFIGS = {
     "c3hi": Config("c3hi", 200_000, 71, 1_600_000, 2.5, 64, 5.0, 311, 302, 303, 200),
     "c4": Config("c4", 5_000_000, 64, 50_000_000, 3.0, 64, 5.0, 401, 402, 403, 50),
     "c5": Config("c5", 1_000_000, 48, 8_000_000, 3.0, 48, 5.0, 501, 502, 503, 500),
+    # optional, paper-shaped: the Graph Challenge graphs' nnz(A)/N ~ 48
+    # (Table 2) at 1M nodes, equal blocks
+    "c6": Config("c6", 1_000_000, 64, 23_700_000, 3.0, 64, None, 601, 602, 603, 50),
 }
 
 
