@@ -156,6 +156,31 @@ def load_traffic():
     return None
 
 
+def kp_of(k):
+    return 16 if k <= 16 else 32 if k <= 32 else 48 if k <= 48 else 64
+
+
+def nvlink_stats(info, kern, K, kp, es, world, max_over_ranks):
+    """p > 1: halo exchange volume per rank per iteration (rows received / sent,
+    DESIGN.md sec. 8) and the profiled (non-overlapped) communication time, as a
+    fraction of 900 GB/s per direction per GPU (NVLink 5)."""
+    if world == 1:
+        return None
+    recv_b = info["halo_rows"] * kp * es
+    send_b = info["send_rows"] * kp * es
+    comm_ms = kern.get("comm", {}).get("ms_total", 0.0) / max(K, 1)
+    comm_ms = max_over_ranks(comm_ms)
+    gbs = max(recv_b, send_b) / (comm_ms / 1e3) / 1e9 if comm_ms > 0 else None
+    return {"halo_rows": info["halo_rows"], "send_rows": info["send_rows"],
+            "recv_bytes_per_iter": recv_b, "send_bytes_per_iter": send_b,
+            "allgather_bytes_per_iter": int((world - 1) * info["n"] / world * kp * es),
+            "comm_ms_per_iter_profiled": round(comm_ms, 4),
+            "achieved_gbs": round(gbs, 1) if gbs else None,
+            "frac_of_900": round(gbs / 900.0, 4) if gbs else None,
+            "note": "profiled pass runs exchange and SpMM back to back; the timed pass overlaps "
+                    "the exchange with the own-column part of the SpMM"}
+
+
 def load_gather_peak():
     """Measured L2-resident random-row gather bandwidth (tools/l2_bw_probe.cu)."""
     p = os.path.join(ROOT, "profiles", "measured_l2.json")
@@ -300,6 +325,7 @@ def run_ours(args):
                           "achieved_gbs_per_gpu": round(it_bytes * (K / (ms / 1e3)) / 1e9, 1),
                           "frac": round(it_bytes * (K / (ms / 1e3)) / 1e9 / hbm_peak, 4)},
         "kernels": kern,
+        "nvlink": nvlink_stats(info, kern, K, kp_of(k), es, world, max_over_ranks),
         "gpu_launches": rep["launches"],
         "clocks": clocks,
     }

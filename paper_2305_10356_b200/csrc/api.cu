@@ -1037,7 +1037,9 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
                  "ofsc_run needs an NCCL communicator when p > 1 (local test communicator given)");
     cudaStream_t s = (cudaStream_t)stream;
     const int KP = padded_k(o.k);
+    trace_point("run: start", s);
     ensure_workspace(g, dt, KP, s);
+    trace_point("run: workspace", s);
     Workspace& w = g->ws;
     const int T = o.max_iters;
     const size_t es = esize(dt);
@@ -1062,6 +1064,7 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
       Prof init;
       refresh_ops(g, dt, p, s, init);
     }
+    trace_point("run: init refresh", s);
     // The iteration is captured once per call as CUDA graphs (plain and refresh
     // iteration); they bake in this call's history buffers.  Profiling runs
     // eager launches bracketed by events instead.
@@ -1097,6 +1100,7 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
         n_launch_refresh = c2.total();
       }
     }
+    trace_point("run: graphs captured", s);
     int* h_stop = nullptr;
     OFSC_CUDA(cudaMallocHost(&h_stop, sizeof(int)));
     struct HostFree {
@@ -1515,8 +1519,10 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     // (~0.2 s at 5M nodes vs ~2 ms saved per iteration there)
     ofsc_build_opts bo{opts->max_iters >= 100 ? 1 : 0, 30};
     if (bopts) bo = *bopts;
+    trace_point("spectral_cluster: start", s);
     ofsc_status b = ofsc_graph_build_ex(comm, n, m, h_src, h_dst, 0, &bo, stream, &g);
     if (b != OFSC_OK) throw Error{b, g_last_error};
+    trace_point("spectral_cluster: graph built", s);
     const int64_t nl = g->n_local;
     const int32_t* perm = g->reordered ? g->perm : nullptr;
     DBuf dX(g->p > 1 ? (size_t)std::max<int64_t>(nl, 1) * k * es : 0, s),
@@ -1534,7 +1540,9 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
                      perm ? perm + g->row_begin : nullptr, s);
       Xrun = dX.p;
     }
+    trace_point("spectral_cluster: X0 on device", s);
     run_st = ofsc_run(g, method, dt, opts, Xrun, k, nullptr, rep, stream);
+    trace_point("spectral_cluster: run done", s);
     if (run_st != OFSC_OK && run_st != OFSC_ERR_DIVERGED) throw Error{run_st, g_last_error};
     // features back to the caller's full array (rows this rank owns)
     if (g->p == 1) {
@@ -1563,8 +1571,10 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     OFSC_LAUNCH_CHECK();
     if (comm && comm->nranks > 1)
       OFSC_NCCL(ncclAllReduce(dC.p, dC.p, (size_t)n_clusters * k, ncclFloat64, ncclSum, comm->nccl, s));
+    trace_point("spectral_cluster: normalised", s);
     r = ofsc_kmeans(comm, dt, nl, k, dY.p, k, n_clusters, dC.as<double>(), km_max_iters,
                     dL.as<int32_t>(), nullptr, nullptr, stream);
+    trace_point("spectral_cluster: kmeans done", s);
     if (r != OFSC_OK) throw Error{r, g_last_error};
     if (g->p == 1) {
       OFSC_CUDA(cudaMemcpyAsync(h_labels, dL.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
