@@ -355,16 +355,14 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     g->row_begin = g->begins[g->rank];
     g->row_end = g->begins[g->rank + 1];
     g->n_local = g->row_end - g->row_begin;
-    int64_t slot = 0, max_nnz = 0;
+    int64_t max_nnz = 0;
     for (int r = 0; r < p; ++r) {
-      slot = std::max(slot, g->begins[r + 1] - g->begins[r]);
       const int64_t nz = rp_at(g->begins[r + 1]) - rp_at(g->begins[r]) + (g->begins[r + 1] - g->begins[r]);
       max_nnz = std::max(max_nnz, nz);
     }
     g->slot_rows = n;     // p == 1: the gather buffer is the whole X (p > 1: set below)
     g->own_off = 0;
     g->ext_rows = n;
-    (void)slot;
     const int64_t e0 = rp_at(g->row_begin), e1 = rp_at(g->row_end);
     g->nnz_local = e1 - e0;
     if (p == 1) {
@@ -581,7 +579,7 @@ ofsc_status ofsc_graph_destroy(ofsc_graph g) {
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// helpers for the hooks: user layout (global rows, ld) -> slot layout (KP)
+// helpers for the hooks: user layout (global rows, ld) -> gather-buffer layout (KP)
 // ---------------------------------------------------------------------------
 namespace ofsc {
 

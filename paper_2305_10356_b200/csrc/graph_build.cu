@@ -468,25 +468,6 @@ void append_csr(CsrDevice& csr, int64_t m, const int64_t* d_src, const int64_t* 
 }
 
 // ---- multi-GPU layout helpers ----------------------------------------------
-// global id g (owned by rank r, rows [b_r, b_{r+1})) -> slot id r*slot_rows + (g - b_r)
-__global__ void k_remap(const int32_t* in, int64_t nnz, int32_t* out, const int64_t* begins, int p,
-                        int64_t slot_rows) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = in[e];
-    int r = 0;
-    while (r + 1 < p && begins[r + 1] <= g) ++r;
-    out[e] = (int32_t)(r * slot_rows + (g - begins[r]));
-  }
-}
-
-void remap_columns(const int32_t* col_in, int64_t nnz, int32_t* col_out, const int64_t* d_begins,
-                   int p, int64_t slot_rows, cudaStream_t st) {
-  if (nnz <= 0) return;
-  k_remap<<<blocks_for(nnz), 256, 0, st>>>(col_in, nnz, col_out, d_begins, p, slot_rows);
-  OFSC_LAUNCH_CHECK();
-}
-
 __global__ void k_scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
                                 const int64_t* begins, int p, int64_t slot_rows) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;

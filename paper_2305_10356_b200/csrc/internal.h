@@ -195,8 +195,6 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
                double* intra_frac, int32_t* d_cid, int64_t** d_cstart, cudaStream_t st);
 void relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
                    int64_t* s2, int64_t* d2, cudaStream_t st);
-void remap_columns(const int32_t* col_in, int64_t nnz, int32_t* col_out, const int64_t* d_begins,
-                   int p, int64_t slot_rows, cudaStream_t st);
 void scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
                    const int64_t* d_begins, int p, int64_t slot_rows, cudaStream_t st);
 void rebase_row_ptr(const int64_t* in, int64_t rows, int64_t base, int64_t* out, cudaStream_t st);
