@@ -6,8 +6,8 @@ the paper's workloads (DCSBM graphs standing in for the IEEE HPEC Graph
 Challenge SBM graphs), the initial feature block X0 and the K-means
 initial-centroid row indices.  Both sides receive these arrays as inputs.
 """
-from .dcsbm import (CONFIGS, Config, dcsbm_graph, stream_parts, snowball_parts, x0_block,
+from .dcsbm import (CONFIGS, Config, dcsbm_graph, rmat_graph, stream_parts, snowball_parts, x0_block,
                     kmeans_init_rows, config_graph)
 
-__all__ = ["CONFIGS", "Config", "dcsbm_graph", "stream_parts", "snowball_parts", "x0_block",
+__all__ = ["CONFIGS", "Config", "dcsbm_graph", "rmat_graph", "stream_parts", "snowball_parts", "x0_block",
            "kmeans_init_rows", "config_graph"]

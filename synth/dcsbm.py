@@ -31,6 +31,7 @@ class Config:
     seed_x0: int
     seed_km: int
     iters: int              # iteration budget of the config
+    kind: str = "dcsbm"     # "dcsbm" or "rmat" (NEXT-3 stress graphs; blocks = K-means clusters)
 
 
 # BASELINE.json "configs" (c1..c5); seeds from SURVEY 8(d).1.
@@ -44,6 +45,10 @@ CONFIGS = {
     # optional, paper-shaped: the Graph Challenge graphs' nnz(A)/N ~ 48
     # (Table 2) at 1M nodes, equal blocks
     "c6": Config("c6", 1_000_000, 64, 23_700_000, 3.0, 64, None, 601, 602, 603, 50),
+    # NEXT-3 stress graph shaped like the paper's Graph500 scaling input (P:510-511,
+    # Graph500 R-MAT a,b,c = 0.57, 0.19, 0.19, edge factor 16; k = 8 as in P:642),
+    # at scale 22 (4.2M nodes): heavy-tailed degrees, high partition imbalance
+    "r22": Config("r22", 1 << 22, 8, 16 << 22, 0.0, 8, None, 701, 702, 703, 50, "rmat"),
 }
 
 
@@ -160,6 +165,26 @@ def dcsbm_graph(n, blocks, edges, ratio, seed, dirichlet=None, gamma=2.1,
     return src, dst, labels
 
 
+def rmat_graph(scale, edges, seed, a=0.57, b=0.19, c=0.19):
+    """Graph500-style R-MAT edge list (Chakrabarti et al.; Graph500 spec
+    parameters): each edge picks one quadrant per level with probabilities
+    (a, b, c, 1-a-b-c); node ids are then randomly permuted so the high-degree
+    nodes carry no locality.  Self-loops and duplicates are left in (the graph
+    build drops / collapses them, R13).  Labels are all zero (no planted blocks)."""
+    rng = _rng(seed)
+    n = 1 << scale
+    u = np.zeros(edges, dtype=np.int64)
+    v = np.zeros(edges, dtype=np.int64)
+    for lvl in range(scale):
+        r = rng.random(edges)
+        bit_u = r >= a + b                     # quadrants c, d: lower half for u
+        bit_v = ((r >= a) & (r < a + b)) | (r >= a + b + c)
+        u |= bit_u.astype(np.int64) << lvl
+        v |= bit_v.astype(np.int64) << lvl
+    perm = rng.permutation(n).astype(np.int64)
+    return perm[u], perm[v], np.zeros(n, dtype=np.int32)
+
+
 def stream_parts(src, dst, parts, seed):
     """Random permutation of the edges split into `parts` nearly equal parts
     (sizes differ by <= 1), for the edge-sampling streaming protocol."""
@@ -227,7 +252,7 @@ def config_graph(cfg: Config):
     path = None
     if cfg.edges >= 1_000_000:
         d = os.environ.get("OFSC_SYNTH_CACHE", "/tmp/ofsc_synth")
-        tag = f"{cfg.name}_{cfg.n}_{cfg.blocks}_{cfg.edges}_{cfg.ratio}_{cfg.dirichlet}_{cfg.seed_graph}_v1"
+        tag = f"{cfg.name}_{cfg.kind}_{cfg.n}_{cfg.blocks}_{cfg.edges}_{cfg.ratio}_{cfg.dirichlet}_{cfg.seed_graph}_v1"
         path = os.path.join(d, tag + ".npz")
         if os.path.exists(path):
             try:
@@ -236,7 +261,10 @@ def config_graph(cfg: Config):
                 return _CACHE[key]
             except Exception:
                 pass
-    out = dcsbm_graph(cfg.n, cfg.blocks, cfg.edges, cfg.ratio, cfg.seed_graph, cfg.dirichlet)
+    if cfg.kind == "rmat":
+        out = rmat_graph(int(cfg.n).bit_length() - 1, cfg.edges, cfg.seed_graph)
+    else:
+        out = dcsbm_graph(cfg.n, cfg.blocks, cfg.edges, cfg.ratio, cfg.seed_graph, cfg.dirichlet)
     if path is not None:
         try:
             os.makedirs(os.path.dirname(path), exist_ok=True)

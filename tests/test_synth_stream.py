@@ -44,3 +44,16 @@ def test_snowball_is_bfs_ordered_on_a_path():
         seen |= set(ps.tolist()) | set(pd.tolist())
         lo, hi = min(seen), max(seen)
         assert seen == set(range(lo, hi + 1))
+
+
+def test_rmat_degree_skew_and_shape():
+    """R-MAT (NEXT-3 stress input): ids in range, heavy-tailed degrees (max degree
+    far above the mean, as in Graph500), deterministic from the seed."""
+    from synth import rmat_graph
+    s, d, lab = rmat_graph(12, 16 << 12, 3)
+    n = 1 << 12
+    assert s.min() >= 0 and d.max() < n and lab.shape == (n,)
+    deg = np.bincount(np.concatenate([s, d]), minlength=n)
+    assert deg.max() > 20 * deg.mean()
+    s2, d2, _ = rmat_graph(12, 16 << 12, 3)
+    assert np.array_equal(s, s2) and np.array_equal(d, d2)
