@@ -138,6 +138,7 @@ struct ofsc_graph_s {
   int32_t* col_rem = nullptr;
   int32_t* cid = nullptr;          // community of each internal row (reordered graphs)
   int64_t* cstart = nullptr;       // community start rows [n_comm + 1]
+  HeavyRows heavy, heavy_loc, heavy_rem;  // power-law rows split into chunks (SpMM binning)
   bool reordered = false;
   ofsc_graph_info info{};
   Workspace ws;
@@ -269,6 +270,9 @@ static void graph_free(ofsc_graph g) {
   dfree(g->col_loc);
   dfree(g->row_ptr_rem);
   dfree(g->col_rem);
+  g->heavy.release();
+  g->heavy_loc.release();
+  g->heavy_rem.release();
 }
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
@@ -408,6 +412,8 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       g->own_off = 0;
       g->slot_rows = hl.ext_rows;
       OFSC_CUDA(cudaStreamSynchronize(s));
+      build_heavy(g->row_ptr_loc, g->n_local, g->heavy_loc, s);
+      build_heavy(g->row_ptr_rem, g->n_local, g->heavy_rem, s);
       dfree(csr.row_ptr);
       dfree(csr.col);
       dfree(csr.s);
@@ -429,6 +435,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     in.reordered = g->reordered ? 1 : 0;
     in.n_communities = n_comm;
     in.intra_edge_fraction = intra;
+    build_heavy(g->row_ptr, g->n_local, g->heavy, s);
     in.halo_rows = g->ext_rows - g->n_local;
     in.send_rows = g->total_send;
     trace_point("graph_build: done", s);
@@ -491,6 +498,7 @@ ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const
     g->row_ptr = csr.row_ptr;
     g->col = csr.col;
     scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, 1, n, s);
+    build_heavy(g->row_ptr, n, g->heavy, s);
     OFSC_CUDA(cudaStreamSynchronize(s));
     g->nnz_local = csr.nnz;
     ofsc_graph_info& in = g->info;
@@ -706,13 +714,13 @@ ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const 
     launch_gram_pair(dt, KP, nl, zown, zown, xs.p, p4.as<double>(), nb, s);
     if (g->p > 1) {   // the iteration's split form: own-row columns, then halo columns
       launch_spmm(dt, KP, nl, 0, g->row_ptr_loc, g->col_loc, g->s_slot, g->s32_slot, zs.p, ys.p,
-                  nullptr, s, nullptr, nullptr, nullptr, 1);
+                  nullptr, s, nullptr, nullptr, nullptr, 1, &g->heavy_loc);
       launch_spmm(dt, KP, nl, 0, g->row_ptr_rem, g->col_rem, g->s_slot, g->s32_slot, zs.p, ys.p,
-                  nullptr, s, nullptr, nullptr, nullptr, 2);
+                  nullptr, s, nullptr, nullptr, nullptr, 2, &g->heavy_rem);
       launch_gram_stream(dt, KP, nl, zown, xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s);
     } else {
       launch_spmm_gram(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p,
-                       xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s);
+                       xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s, &g->heavy);
     }
     launch_reduce_partials(p4.as<double>(), nb, 2 * KP * KP, gr.as<double>(), s);
     launch_reduce_partials(p2.as<double>(), nb2, 2 * KP * KP, gr.as<double>() + 2 * KP * KP, s);
@@ -870,7 +878,8 @@ static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaSt
   }
   pr.ph(OFSC_PH_REFRESH, 3, [&] {
     launch_spmm_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
-                     g->s32_slot, Zg, nullptr, w.AX, w.part_g2, 1, &p.ctl->stop, w.nb2, s);
+                     g->s32_slot, Zg, nullptr, w.AX, w.part_g2, 1, &p.ctl->stop, w.nb2, s,
+                     &g->heavy);
     launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, p.M, s);  // M, W contiguous
   });
   pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, p.M, 2 * (size_t)p.KP * p.KP, s); });
@@ -914,10 +923,10 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     OFSC_CUDA(cudaEventRecord(w.ev_x, w.comm_st));
     pr.ph(OFSC_PH_SPMM_GRAM, 2, [&] {
       launch_spmm(dt, p.KP, g->n_local, 0, g->row_ptr_loc, g->col_loc, g->s_slot, g->s32_slot,
-                  w.Vg, w.AV, &p.ctl->stop, s, nullptr, nullptr, w.ctr, 1);
+                  w.Vg, w.AV, &p.ctl->stop, s, nullptr, nullptr, w.ctr, 1, &g->heavy_loc);
       OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_x, 0));
       launch_spmm(dt, p.KP, g->n_local, 0, g->row_ptr_rem, g->col_rem, g->s_slot, g->s32_slot,
-                  w.Vg, w.AV, &p.ctl->stop, s, nullptr, nullptr, w.ctr, 2);
+                  w.Vg, w.AV, &p.ctl->stop, s, nullptr, nullptr, w.ctr, 2, &g->heavy_rem);
     });
   } else {
     if (g->p > 1)
@@ -927,7 +936,7 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
       launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
                   w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
-                  g->p == 1 ? g->cstart : nullptr, w.ctr);
+                  g->p == 1 ? g->cstart : nullptr, w.ctr, 0, &g->heavy);
     });
   }
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {

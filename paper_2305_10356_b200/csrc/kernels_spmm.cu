@@ -10,7 +10,11 @@
 // runs are bitwise reproducible.
 //   mode 0 (iteration):  T = Z^T Y, R' = X^T Y    (Z = V)
 //   mode 1 (refresh):    M = Z^T Z, W = Z^T Y     (Z = X)
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
+
+#include <cub/cub.cuh>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -70,7 +74,8 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
        const int* stop, unsigned long long* __restrict__ ctr, int ch, int c0,
-       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart) {
+       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart, int64_t heavy) {
+  // rows with more than `heavy` neighbours are left to the chunked heavy-row pass
   // PHASE 0: Y = A Z (whole rows); 1: Y <- raw neighbour sums over this CSR (the
   // local columns of a multi-GPU rank, while the halo is in flight); 2: continue
   // the sums from Y over this CSR (the halo columns) and finish Y = -Z_i - s_i sum
@@ -115,6 +120,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     const int64_t i = base + q + sub;
     if (!active || i >= n_local) continue;
     const int64_t beg = row_ptr[i], end = row_ptr[i + 1];
+    if (end - beg > heavy) continue;               // uniform within the row group
     int lo = 0, hi = 0;                            // community row range of row i (HINT)
     if constexpr (HINT) {
       const int ci = cid[i];
@@ -209,6 +215,236 @@ static int env_int(const char* name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
+// ---- degree-aware row binning (power-law rows) ------------------------------
+// Chunk pass: one LPR-lane group per chunk of <= kHeavyChunk neighbours of a
+// heavy row (same lane mapping and 8-in-flight loop as k_spmm); raw partial
+// sums go to scratch[chunk].  Finalize: per (heavy row, column), the chunk
+// partials summed in chunk order (deterministic), then the row finished as in
+// k_spmm (PHASE 1 stores the raw sum, PHASE 2 adds the stored partial first).
+template <typename T, int KP>
+__global__ void __launch_bounds__(kThreads)
+k_spmm_chunks(int64_t n_chunks, const int64_t* __restrict__ cbeg, const int64_t* __restrict__ cend,
+              const int32_t* __restrict__ col, const double* __restrict__ s,
+              const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ scratch,
+              const int* stop) {
+  if (stop && *stop) return;
+  using V2 = typename Vec2<T>::type;
+  constexpr int LPR = KP / 4;
+  constexpr int RPW = 32 / LPR;
+  constexpr int H2 = KP / 2;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR, l = lane % LPR;
+  if (sub >= RPW) return;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T* zc = Zg + 2 * l;
+  for (int64_t q = gw * RPW + sub; q < n_chunks; q += nw * RPW) {
+    const int64_t beg = cbeg[q], end = cend[q];
+    T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    int64_t e = beg;
+    for (; e + 8 <= end; e += 8) {
+      int c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = __ldg(col + e + u);
+      V2 z0[8], z1[8];
+      T sv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const T* zr = zc + (int64_t)c[u] * KP;
+        z0[u] = __ldg(reinterpret_cast<const V2*>(zr));
+        z1[u] = __ldg(reinterpret_cast<const V2*>(zr + H2));
+        if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
+        else sv[u] = (T)__ldg(s32 + c[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a0 = fma(sv[u], z0[u].x, a0);
+        a1 = fma(sv[u], z0[u].y, a1);
+        a2 = fma(sv[u], z1[u].x, a2);
+        a3 = fma(sv[u], z1[u].y, a3);
+      }
+    }
+    for (; e < end; ++e) {
+      const int c = __ldg(col + e);
+      const T* zr = zc + (int64_t)c * KP;
+      const V2 z0 = __ldg(reinterpret_cast<const V2*>(zr));
+      const V2 z1 = __ldg(reinterpret_cast<const V2*>(zr + H2));
+      T sv;
+      if constexpr (sizeof(T) == 8) sv = (T)__ldg(s + c);
+      else sv = (T)__ldg(s32 + c);
+      a0 = fma(sv, z0.x, a0);
+      a1 = fma(sv, z0.y, a1);
+      a2 = fma(sv, z1.x, a2);
+      a3 = fma(sv, z1.y, a3);
+    }
+    T* o = scratch + q * 64 + 2 * l;
+    o[0] = a0;
+    o[1] = a1;
+    o[H2] = a2;
+    o[H2 + 1] = a3;
+  }
+}
+
+template <typename T, int PHASE>
+__global__ void k_heavy_finish(int64_t n_heavy, int KP, const int32_t* __restrict__ rows,
+                               const int32_t* __restrict__ first, const T* __restrict__ scratch,
+                               int64_t own_off, const double* __restrict__ s,
+                               const float* __restrict__ s32, const T* __restrict__ Zg,
+                               T* __restrict__ Y, const int* stop) {
+  if (stop && *stop) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_heavy * KP;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = e / KP;
+    const int c = (int)(e % KP);
+    const int64_t i = rows[h];
+    T acc = 0;
+    if constexpr (PHASE == 2) acc = Y[i * KP + c];
+    for (int q = first[h]; q < first[h + 1]; ++q) acc = acc + scratch[(int64_t)q * 64 + c];
+    if constexpr (PHASE == 1) {
+      Y[i * KP + c] = acc;
+    } else {
+      T si;
+      if constexpr (sizeof(T) == 8) si = (T)s[own_off + i];
+      else si = s32[own_off + i];
+      Y[i * KP + c] = -Zg[(own_off + i) * KP + c] - si * acc;
+    }
+  }
+}
+
+static void launch_heavy(ofsc_dtype dt, int KP, int64_t own_off, const int64_t* row_ptr,
+                         const int32_t* col, const double* s, const float* s32, const void* Zg,
+                         void* Y, const int* stop, cudaStream_t st, int phase, const HeavyRows& hr) {
+  (void)row_ptr;
+  const int nbc = (int)std::min<int64_t>((hr.n_chunks * 32 + kThreads - 1) / kThreads,
+                                         (int64_t)num_sms() * 8);
+  const int nbf = (int)std::min<int64_t>((hr.n_rows * KP + 255) / 256, (int64_t)num_sms() * 8);
+  OFSC_DISPATCH_KP(KP, {
+    if (dt == OFSC_F64) {
+      k_spmm_chunks<double, KPC><<<std::max(nbc, 1), kThreads, 0, st>>>(
+          hr.n_chunks, hr.chunk_beg, hr.chunk_end, col, s, s32, (const double*)Zg,
+          (double*)hr.scratch, stop);
+    } else {
+      k_spmm_chunks<float, KPC><<<std::max(nbc, 1), kThreads, 0, st>>>(
+          hr.n_chunks, hr.chunk_beg, hr.chunk_end, col, s, s32, (const float*)Zg,
+          (float*)hr.scratch, stop);
+    }
+  });
+  OFSC_LAUNCH_CHECK();
+#define OFSC_HF(TT, PH)                                                                           \
+  k_heavy_finish<TT, PH><<<std::max(nbf, 1), 256, 0, st>>>(hr.n_rows, KP, hr.rows, hr.chunk_first, \
+      (const TT*)hr.scratch, own_off, s, s32, (const TT*)Zg, (TT*)Y, stop)
+  if (dt == OFSC_F64) {
+    if (phase == 1) OFSC_HF(double, 1); else if (phase == 2) OFSC_HF(double, 2); else OFSC_HF(double, 0);
+  } else {
+    if (phase == 1) OFSC_HF(float, 1); else if (phase == 2) OFSC_HF(float, 2); else OFSC_HF(float, 0);
+  }
+#undef OFSC_HF
+  OFSC_LAUNCH_CHECK();
+}
+
+__global__ void k_heavy_flags(int64_t n, const int64_t* row_ptr, int64_t thresh, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (row_ptr[i + 1] - row_ptr[i]) > thresh ? 1 : 0;
+}
+
+__global__ void k_iota_rows(int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+__global__ void k_row_bounds(int64_t nh, const int32_t* rows, const int64_t* row_ptr, int64_t* b,
+                             int64_t* e) {
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nh;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    b[h] = row_ptr[rows[h]];
+    e[h] = row_ptr[rows[h] + 1];
+  }
+}
+
+void HeavyRows::release() {
+  for (void* q : {(void*)rows, (void*)chunk_first, (void*)chunk_beg, (void*)chunk_end, scratch})
+    if (q) cudaFree(q);
+  rows = nullptr;
+  chunk_first = nullptr;
+  chunk_beg = chunk_end = nullptr;
+  scratch = nullptr;
+  n_rows = n_chunks = 0;
+  thresh = INT64_MAX;
+}
+
+void build_heavy(const int64_t* d_row_ptr, int64_t n_rows, HeavyRows& out, cudaStream_t st) {
+  out.release();
+  if (n_rows <= 0) return;
+  const int64_t thresh = env_int("OFSC_HEAVY_THRESH", (int)kHeavyThresh);
+  int* flag = nullptr;
+  int32_t *iota = nullptr, *sel = nullptr;
+  int64_t* nsel = nullptr;
+  OFSC_CUDA(cudaMallocAsync(&flag, n_rows * sizeof(int), st));
+  OFSC_CUDA(cudaMallocAsync(&iota, n_rows * sizeof(int32_t), st));
+  OFSC_CUDA(cudaMallocAsync(&sel, n_rows * sizeof(int32_t), st));
+  OFSC_CUDA(cudaMallocAsync(&nsel, sizeof(int64_t), st));
+  const int nb = (int)std::min<int64_t>((n_rows + 255) / 256, (int64_t)num_sms() * 16);
+  k_heavy_flags<<<nb, 256, 0, st>>>(n_rows, d_row_ptr, thresh, flag);
+  k_iota_rows<<<nb, 256, 0, st>>>(n_rows, iota);
+  OFSC_LAUNCH_CHECK();
+  size_t tb = 0;
+  OFSC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota, flag, sel, nsel, n_rows, st));
+  void* tmp = nullptr;
+  OFSC_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), st));
+  OFSC_CUDA(cub::DeviceSelect::Flagged(tmp, tb, iota, flag, sel, nsel, n_rows, st));
+  int64_t nh = 0;
+  OFSC_CUDA(cudaMemcpyAsync(&nh, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  OFSC_CUDA(cudaStreamSynchronize(st));
+  if (nh > 0) {
+    std::vector<int32_t> rows(nh);
+    std::vector<int64_t> b(nh), e(nh);
+    int64_t *db = nullptr, *de = nullptr;
+    OFSC_CUDA(cudaMallocAsync(&db, nh * sizeof(int64_t), st));
+    OFSC_CUDA(cudaMallocAsync(&de, nh * sizeof(int64_t), st));
+    k_row_bounds<<<(int)std::min<int64_t>((nh + 255) / 256, 1024), 256, 0, st>>>(nh, sel, d_row_ptr,
+                                                                               db, de);
+    OFSC_LAUNCH_CHECK();
+    OFSC_CUDA(cudaMemcpyAsync(rows.data(), sel, nh * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaMemcpyAsync(b.data(), db, nh * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaMemcpyAsync(e.data(), de, nh * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    OFSC_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(db, st);
+    cudaFreeAsync(de, st);
+    std::vector<int32_t> first(nh + 1, 0);
+    std::vector<int64_t> cb, ce;
+    for (int64_t h = 0; h < nh; ++h) {
+      first[h] = (int32_t)cb.size();
+      for (int64_t x = b[h]; x < e[h]; x += kHeavyChunk) {
+        cb.push_back(x);
+        ce.push_back(std::min(e[h], x + kHeavyChunk));
+      }
+    }
+    first[nh] = (int32_t)cb.size();
+    out.thresh = thresh;
+    out.n_rows = nh;
+    out.n_chunks = (int64_t)cb.size();
+    OFSC_CUDA(cudaMalloc(&out.rows, nh * sizeof(int32_t)));
+    OFSC_CUDA(cudaMalloc(&out.chunk_first, (nh + 1) * sizeof(int32_t)));
+    OFSC_CUDA(cudaMalloc(&out.chunk_beg, out.n_chunks * sizeof(int64_t)));
+    OFSC_CUDA(cudaMalloc(&out.chunk_end, out.n_chunks * sizeof(int64_t)));
+    OFSC_CUDA(cudaMalloc(&out.scratch, out.n_chunks * 64 * sizeof(double)));
+    OFSC_CUDA(cudaMemcpy(out.rows, rows.data(), nh * sizeof(int32_t), cudaMemcpyHostToDevice));
+    OFSC_CUDA(cudaMemcpy(out.chunk_first, first.data(), (nh + 1) * sizeof(int32_t),
+                         cudaMemcpyHostToDevice));
+    OFSC_CUDA(cudaMemcpy(out.chunk_beg, cb.data(), out.n_chunks * sizeof(int64_t),
+                         cudaMemcpyHostToDevice));
+    OFSC_CUDA(cudaMemcpy(out.chunk_end, ce.data(), out.n_chunks * sizeof(int64_t),
+                         cudaMemcpyHostToDevice));
+  }
+  cudaFreeAsync(flag, st);
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(sel, st);
+  cudaFreeAsync(nsel, st);
+  cudaFreeAsync(tmp, st);
+}
+
 // Default column window of the SpMM passes (see k_spmm).
 int spmm_col_window(ofsc_dtype, int KP) { return KP; }
 
@@ -222,7 +458,9 @@ int spmm_grid(int64_t n_local) {  // resident CTAs (3 per SM) for the chunked sc
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart,
-                 unsigned long long* ctr, int phase) {
+                 unsigned long long* ctr, int phase, const HeavyRows* heavy) {
+  const bool hv = heavy && heavy->n_rows > 0;
+  const int64_t hth = hv ? heavy->thresh : INT64_MAX;
   // cid / cstart: community layout of reordered graphs (p == 1), for the L2 hints.
   const int hint = (cid && cstart && own_off == 0) ? env_int("OFSC_SPMM_HINT", 0) : 0;
   const int nb = spmm_grid(n_local);
@@ -239,10 +477,10 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #define OFSC_SPMM_LAUNCH_P(CWC, H, PH)                                                          \
     if (dt == OFSC_F64)                                                                         \
       k_spmm<double, KPC, CWC, H, PH><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, \
-          s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart);                    \
+          s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart, hth);               \
     else                                                                                        \
       k_spmm<float, KPC, CWC, H, PH><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s,  \
-          s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart);
+          s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth);
 #define OFSC_SPMM_LAUNCH_H(CWC, H) OFSC_SPMM_LAUNCH_P(CWC, H, 0)
 #define OFSC_SPMM_LAUNCH(CWC) \
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
@@ -258,13 +496,16 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #undef OFSC_SPMM_LAUNCH_P
     OFSC_LAUNCH_CHECK();
   }
+  if (hv) launch_heavy(dt, KP, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, phase, *heavy);
 }
 
 void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       const int64_t* row_ptr, const int32_t* col, const double* s,
                       const float* s32, const void* Zg, const void* Xown, void* Y, double* part,
-                      int mode, const int* stop, int nblk, cudaStream_t st) {
-  launch_spmm(dt, KP, n_local, own_off, row_ptr, col, s, s32, Zg, Y, stop, st);
+                      int mode, const int* stop, int nblk, cudaStream_t st,
+                      const HeavyRows* heavy) {
+  launch_spmm(dt, KP, n_local, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, nullptr, nullptr,
+              nullptr, 0, heavy);
   if (part) {
     const size_t es = dt == OFSC_F64 ? 8 : 4;
     const void* Zown = (const char*)Zg + (size_t)own_off * KP * es;

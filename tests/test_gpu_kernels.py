@@ -9,7 +9,7 @@ pytestmark = pytest.mark.gpu
 
 import paper_2305_10356_b200 as ofsc  # noqa: E402
 from oracle import (build_operator, apply_A, grams, cubic_coefficients, select_step,  # noqa: E402
-                    fro2_A, METHODS)
+                    fro2_A, METHODS, run_ofm)
 from synth import CONFIGS, config_graph, dcsbm_graph, x0_block  # noqa: E402
 from tests import graphs as G  # noqa: E402
 
@@ -257,3 +257,62 @@ def test_halo_exchange_plan_is_consistent(p, reorder):
             assert np.array_equal(sg[so[r]:so[r + 1]], rg[ro[q]:ro[q + 1]]), (q, r)
     if reorder:
         assert sum(halos.values()) < 0.9 * (p - 1) * n     # far below an all-gather
+
+
+def _heavy_graph():
+    """A power-law stress graph: a hub of degree 9,000 (> kHeavyThresh = 256,
+    so it is split into 512-neighbour chunks), two hubs of ~5,000 and an R-MAT
+    background."""
+    from synth import rmat_graph
+    rs, rd, _ = rmat_graph(13, 6 << 13, 5)
+    n = 1 << 13
+    hub = [np.zeros(9000, np.int64), np.arange(1, 9001) % n]
+    hub2 = [np.full(5000, 17, np.int64), (np.arange(5000) * 7 + 3) % n]
+    hub3 = [np.full(5000, 4242, np.int64), (np.arange(5000) * 11 + 5) % n]
+    s = np.concatenate([rs, hub[0], hub2[0], hub3[0]])
+    d = np.concatenate([rd, hub[1], hub2[1], hub3[1]])
+    return s, d, n
+
+
+@pytest.mark.parametrize("thresh", [None, 8])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_heavy_rows_split_spmm(thresh, dtype, monkeypatch):
+    """Degree-aware row binning: rows above the threshold are summed in chunks
+    (fixed chunk order) -- SpMM + Grams match the oracle; thresh = 8 forces most
+    rows of the graph through the chunked path."""
+    if thresh is not None:
+        monkeypatch.setenv("OFSC_HEAVY_THRESH", str(thresh))
+    s, d, n = _heavy_graph()
+    op = build_operator(n, s, d)
+    assert op.deg.max() > 4096
+    g = ofsc.Graph(n, s, d)
+    k = 32
+    rng = np.random.default_rng(3)
+    Z = rng.standard_normal((n, k)) / np.sqrt(n)
+    X = rng.standard_normal((n, k)) / np.sqrt(n)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    Y, Gm = g.apply_gram(torch.from_numpy(Z).to(tdt).cuda(), torch.from_numpy(X).to(tdt).cuda())
+    if dtype == "f64":
+        Yo = apply_A(op, Z)
+        assert np.max(np.abs(Y.cpu().numpy() - Yo)) <= 4e-14 * np.max(np.abs(Yo))
+        assert rel(Gm.cpu().numpy()[2], (Z.T @ Yo)) <= 1e-13
+    else:
+        Z32 = Z.astype(np.float32).astype(np.float64)
+        Yo = apply_A(op, Z32, "f32")
+        assert np.max(np.abs(Y.cpu().double().numpy() - Yo)) <= 1e-5 * np.max(np.abs(Yo))
+    g.close()
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_heavy_rows_iteration(method):
+    """P2 on the power-law stress graph (hub rows split): 10 iterations vs the oracle."""
+    s, d, n = _heavy_graph()
+    op = build_operator(n, s, d)
+    g = ofsc.Graph(n, s, d, reorder=True)
+    X0 = x0_block(n, 8, 31)
+    o = run_ofm(op, method, X0, 10, refresh=0)
+    X = torch.from_numpy(X0.copy()).cuda()
+    r = ofsc.run(g, method, X, 10)
+    assert r.report["iters"] == o.iters
+    assert rel(X.cpu().numpy(), o.X) <= 1e-10
+    g.close()
