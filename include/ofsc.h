@@ -11,6 +11,10 @@
  *   Alg. 1 l.5   Euclidean K-means (Lloyd) ........................... ofsc_kmeans
  *   P:587               ARI / NMI of two labelings (host) .................. ofsc_scores
  *   Alg. 1 end to end   host buffers in, labels out ........................ ofsc_spectral_cluster
+ *   P:589, P:596        orthogonalisation + Rayleigh-Ritz, relerr ........... ofsc_rayleigh_ritz
+ *   P:584, P:609        streaming: add an edge part to a built graph ........ ofsc_graph_append
+ *   kernel-level hooks  SpMM, SpMM + Grams, line search, exchange plan ...... ofsc_graph_apply,
+ *                       ofsc_graph_apply_gram, ofsc_line_search, ofsc_graph_exchange_plan
  *
  * Conventions
  *  - Pointers named d_* are CUDA device pointers, h_* are host pointers.  The
@@ -33,7 +37,10 @@
  *  - Multi-GPU: one process per GPU.  Rows are partitioned contiguously,
  *    balanced by nnz; a rank's row range is ofsc_graph_info.row_begin/row_end
  *    and every d_X / d_Y / d_labels argument is that rank's local row block.
- *    comm == NULL means a single GPU.
+ *    comm == NULL means a single GPU.  Per iteration each rank exchanges only
+ *    the rows its peers reference (halo, grouped ncclSend/ncclRecv, overlapped
+ *    with the SpMM's own-column part) and all-reduces the k x k Grams and the
+ *    column dots.
  *  - No CPU fallback: every numerical step runs in this library's sm_100a kernels.
  */
 #ifndef OFSC_H
