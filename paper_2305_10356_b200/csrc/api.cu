@@ -139,6 +139,8 @@ struct ofsc_graph_s {
   int32_t* cid = nullptr;          // community of each internal row (reordered graphs)
   int64_t* cstart = nullptr;       // community start rows [n_comm + 1]
   HeavyRows heavy, heavy_loc, heavy_rem;  // power-law rows split into chunks (SpMM binning)
+  double* sval = nullptr;          // per-nonzero s_j (p == 1, large graphs; build_sval)
+  float* sval32 = nullptr;
   bool reordered = false;
   ofsc_graph_info info{};
   Workspace ws;
@@ -273,6 +275,8 @@ static void graph_free(ofsc_graph g) {
   g->heavy.release();
   g->heavy_loc.release();
   g->heavy_rem.release();
+  dfree(g->sval);
+  dfree(g->sval32);
 }
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
@@ -436,6 +440,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     in.n_communities = n_comm;
     in.intra_edge_fraction = intra;
     build_heavy(g->row_ptr, g->n_local, g->heavy, s);
+    if (p == 1) build_sval(g->nnz_local, g->col, g->s_slot, g->s32_slot, &g->sval, &g->sval32, s);
     in.halo_rows = g->ext_rows - g->n_local;
     in.send_rows = g->total_send;
     trace_point("graph_build: done", s);
@@ -499,6 +504,7 @@ ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const
     g->col = csr.col;
     scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, 1, n, s);
     build_heavy(g->row_ptr, n, g->heavy, s);
+    build_sval(csr.nnz, g->col, g->s_slot, g->s32_slot, &g->sval, &g->sval32, s);
     OFSC_CUDA(cudaStreamSynchronize(s));
     g->nnz_local = csr.nnz;
     ofsc_graph_info& in = g->info;
@@ -936,7 +942,9 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     pr.ph(OFSC_PH_SPMM_GRAM, 1, [&] {
       launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
                   w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
-                  g->p == 1 ? g->cstart : nullptr, w.ctr, 0, &g->heavy);
+                  g->p == 1 ? g->cstart : nullptr, w.ctr, 0, &g->heavy,
+                  g->p == 1 ? (dt == OFSC_F64 ? (const void*)g->sval : (const void*)g->sval32)
+                            : nullptr);
     });
   }
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {

@@ -137,7 +137,12 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
                  const int* stop, cudaStream_t st, const int32_t* cid = nullptr,
                  const int64_t* cstart = nullptr, unsigned long long* ctr = nullptr,
                  int phase = 0,    // 1: raw partial sums into Y; 2: continue from Y and finish
-                 const HeavyRows* heavy = nullptr);
+                 const HeavyRows* heavy = nullptr,
+                 const void* sval = nullptr);   // per-nonzero s_j (type of the run), or NULL
+// per-nonzero neighbour scales s_j = s[col[e]] (streamed with the column ids by the
+// SpMM of large graphs instead of a random 8-byte gather per neighbour)
+void build_sval(int64_t nnz, const int32_t* col, const double* s, const float* s32, double** sval,
+                float** sval32, cudaStream_t st);
 constexpr int kSpmmChunk = 8;  // rows per dynamic work grab of the SpMM
 // C2b: TMA-streamed Gram pair over own rows (mode 0: Z^T Y, X^T Y; mode 1: Z^T Z, Z^T Y)
 int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n);

@@ -68,13 +68,16 @@ __device__ __forceinline__ void stg2h(float* p, float2 v, uint64_t pol) {
                "l"(pol));
 }
 
-template <typename T, int KP, int CW, int HINT, int PHASE>
+template <typename T, int KP, int CW, int HINT, int PHASE, int SV = 0>
 __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
        const int* stop, unsigned long long* __restrict__ ctr, int ch, int c0,
-       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart, int64_t heavy) {
+       const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart, int64_t heavy,
+       const T* __restrict__ sval) {
+  // SV = 1: the neighbour scale s_j is read from the per-nonzero array sval (streamed
+  // with the column ids) instead of gathered from s by column id
   // rows with more than `heavy` neighbours are left to the chunked heavy-row pass
   // PHASE 0: Y = A Z (whole rows); 1: Y <- raw neighbour sums over this CSR (the
   // local columns of a multi-GPU rank, while the halo is in flight); 2: continue
@@ -158,7 +161,8 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
           z0[u] = __ldg(reinterpret_cast<const V2*>(zr));
           z1[u] = __ldg(reinterpret_cast<const V2*>(zr + H2));
         }
-        if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
+        if constexpr (SV) sv[u] = __ldg(sval + e + u);
+        else if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
         else sv[u] = (T)__ldg(s32 + c[u]);
       }
 #pragma unroll
@@ -175,7 +179,8 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       const V2 z0 = __ldg(reinterpret_cast<const V2*>(zr));
       const V2 z1 = __ldg(reinterpret_cast<const V2*>(zr + H2));
       T sv;
-      if constexpr (sizeof(T) == 8) sv = (T)__ldg(s + c);
+      if constexpr (SV) sv = __ldg(sval + e);
+      else if constexpr (sizeof(T) == 8) sv = (T)__ldg(s + c);
       else sv = (T)__ldg(s32 + c);
       a0 = fma(sv, z0.x, a0);
       a1 = fma(sv, z0.y, a1);
@@ -445,6 +450,31 @@ void build_heavy(const int64_t* d_row_ptr, int64_t n_rows, HeavyRows& out, cudaS
   cudaFreeAsync(tmp, st);
 }
 
+__global__ void k_gather_sval(int64_t nnz, const int32_t* col, const double* s, const float* s32,
+                              double* sval, float* sval32) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    sval[e] = s[col[e]];
+    sval32[e] = s32[col[e]];
+  }
+}
+
+void build_sval(int64_t nnz, const int32_t* col, const double* s, const float* s32, double** sval,
+                float** sval32, cudaStream_t st) {
+  if (*sval) cudaFree(*sval);
+  if (*sval32) cudaFree(*sval32);
+  *sval = nullptr;
+  *sval32 = nullptr;
+  // auto: graphs whose gathers mostly miss L2 (measured c4: SpMM 5.6 -> 5.3 ms; on
+  // L2-resident c3 the extra stream costs 3 %): OFSC_SPMM_SVAL=1 forces it, 0 disables
+  const int mode = env_int("OFSC_SPMM_SVAL", -1);
+  if (nnz <= 0 || mode == 0 || (mode < 0 && nnz < 20000000)) return;
+  OFSC_CUDA(cudaMalloc(sval, nnz * sizeof(double)));
+  OFSC_CUDA(cudaMalloc(sval32, nnz * sizeof(float)));
+  k_gather_sval<<<num_sms() * 16, 256, 0, st>>>(nnz, col, s, s32, *sval, *sval32);
+  OFSC_LAUNCH_CHECK();
+}
+
 // Default column window of the SpMM passes (see k_spmm).
 int spmm_col_window(ofsc_dtype, int KP) { return KP; }
 
@@ -458,7 +488,8 @@ int spmm_grid(int64_t n_local) {  // resident CTAs (3 per SM) for the chunked sc
 void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const int64_t* row_ptr,
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart,
-                 unsigned long long* ctr, int phase, const HeavyRows* heavy) {
+                 unsigned long long* ctr, int phase, const HeavyRows* heavy,
+                 const void* sval) {
   const bool hv = heavy && heavy->n_rows > 0;
   const int64_t hth = hv ? heavy->thresh : INT64_MAX;
   // cid / cstart: community layout of reordered graphs (p == 1), for the L2 hints.
@@ -474,18 +505,22 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   for (int ps = 0; ps < passes; ++ps) {
     unsigned long long* c = ctr ? ctr + ps : nullptr;
     const int c0 = ps * cw;
-#define OFSC_SPMM_LAUNCH_P(CWC, H, PH)                                                          \
+#define OFSC_SPMM_LAUNCH_S(CWC, H, PH, SVV)                                                     \
     if (dt == OFSC_F64)                                                                         \
-      k_spmm<double, KPC, CWC, H, PH><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s, \
-          s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart, hth);               \
+      k_spmm<double, KPC, CWC, H, PH, SVV><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr,  \
+          col, s, s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart, hth,        \
+          (const double*)sval);                                                                 \
     else                                                                                        \
-      k_spmm<float, KPC, CWC, H, PH><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr, col, s,  \
-          s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth);
+      k_spmm<float, KPC, CWC, H, PH, SVV><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr,   \
+          col, s, s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth,          \
+          (const float*)sval);
+#define OFSC_SPMM_LAUNCH_P(CWC, H, PH) OFSC_SPMM_LAUNCH_S(CWC, H, PH, 0)
 #define OFSC_SPMM_LAUNCH_H(CWC, H) OFSC_SPMM_LAUNCH_P(CWC, H, 0)
 #define OFSC_SPMM_LAUNCH(CWC) \
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
-      if (phase == 1) { OFSC_SPMM_LAUNCH_P(KPC, 0, 1) }
+      if (sval && phase == 0 && cw == KPC && !hint) { OFSC_SPMM_LAUNCH_S(KPC, 0, 0, 1) }
+      else if (phase == 1) { OFSC_SPMM_LAUNCH_P(KPC, 0, 1) }
       else if (phase == 2) { OFSC_SPMM_LAUNCH_P(KPC, 0, 2) }
       else if (cw == KPC) { OFSC_SPMM_LAUNCH(KPC) }
       else if (cw == 32) { if constexpr (KPC % 32 == 0) { OFSC_SPMM_LAUNCH(32) } }
@@ -494,6 +529,7 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #undef OFSC_SPMM_LAUNCH
 #undef OFSC_SPMM_LAUNCH_H
 #undef OFSC_SPMM_LAUNCH_P
+#undef OFSC_SPMM_LAUNCH_S
     OFSC_LAUNCH_CHECK();
   }
   if (hv) launch_heavy(dt, KP, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, phase, *heavy);

@@ -306,3 +306,19 @@ def test_degenerate_graphs(case, method):
         assert any(8 <= c <= 10 for c in o.codes[t]), o.codes[t]
         assert abs(r.history[-1, 0] - o.history[-1, 0]) <= 1e-8 * abs(o.history[-1, 0])
     g.close()
+
+
+@pytest.mark.parametrize("method", ["ofm_f2", "triofm_f1"])
+def test_streamed_neighbour_scales_bitwise(method, monkeypatch):
+    """The per-nonzero s_j stream (on by default for graphs with > 2e7 nonzeros,
+    forced here on c2) computes exactly the same sums as the gathered s_j."""
+    cfg, op, g, X0, _ = setup("c2")
+    X_a, _ = gpu_run(g, method, X0, 10)
+    monkeypatch.setenv("OFSC_SPMM_SVAL", "1")
+    s, d, _ = config_graph(cfg)
+    g2 = ofsc.Graph(cfg.n, s, d)
+    X_b, _ = gpu_run(g2, method, X0, 10)
+    assert np.array_equal(X_a, X_b)
+    o = run_ofm(op, method, X0, 10, refresh=0)
+    assert rel(X_b, o.X) <= 1e-10
+    g2.close()
