@@ -467,6 +467,137 @@ k_gram_stream(int64_t n_local, const T* __restrict__ gZ, const T* __restrict__ g
   acc.store(part + (int64_t)blockIdx.x * 2 * KP * KP, warp, lane);
 }
 
+// C2b, warp-specialised: warps 0-7 run the DMMA Gram products, warps 8-11
+// (producers) wait for each TMA stage, convert it into one of two padded fp64
+// tiles and hand it over on an mbarrier, so the tensor-pipe warps never wait
+// for the staging copy.  Same products and summation order as k_gram_stream.
+constexpr int kGWS_NS = 3;          // TMA stages
+constexpr int kGWS_NP = 2;          // padded tiles
+constexpr int kGWS_THREADS = 384;   // 8 consumer + 4 producer warps
+
+template <typename T, int KP>
+struct GSmemWS {
+  static constexpr int LD = KP + 4;
+  static constexpr size_t pad = (size_t)kSTR * LD * 8;               // one padded array
+  static constexpr size_t arr = (size_t)kSTR * KP * sizeof(T);
+  static constexpr size_t stage = 3 * arr;                            // Z, X, Y
+  static constexpr size_t bytes = kGWS_NP * 3 * pad + kGWS_NS * stage + (kGWS_NS + 2 * kGWS_NP) * 8;
+};
+
+template <typename T, int KP, int MODE>
+__global__ void __launch_bounds__(kGWS_THREADS, 1)
+k_gram_stream_ws(int64_t n_local, const T* __restrict__ gZ, const T* __restrict__ gX,
+                 const T* __restrict__ gY, double* __restrict__ part, const int* stop) {
+  using S = GSmemWS<T, KP>;
+  constexpr int LD = S::LD;
+  if (stop && *stop) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* pads = (double*)smraw;                                       // [NP][3][kSTR][LD]
+  unsigned char* stg = smraw + kGWS_NP * 3 * S::pad;
+  uint64_t* full = (uint64_t*)(stg + kGWS_NS * S::stage);
+  uint64_t* pfull = full + kGWS_NS;
+  uint64_t* pempty = pfull + kGWS_NP;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (n_local + kSTR - 1) / kSTR;
+  auto arr = [&](int st, int a) { return (const T*)(stg + st * S::stage + a * S::arr); };
+  auto pad = [&](int pb, int a) { return pads + ((size_t)pb * 3 + a) * kSTR * LD; };
+  auto issue = [&](int st, int64_t tile) {
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, n_local - row0);
+    const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+    mbar_arrive_expect_tx(&full[st], (MODE == 0 ? 3u : 2u) * b);
+    bulk_g2s((void*)arr(st, 0), gZ + row0 * KP, b, &full[st]);
+    if (MODE == 0) bulk_g2s((void*)arr(st, 1), gX + row0 * KP, b, &full[st]);
+    bulk_g2s((void*)arr(st, 2), gY + row0 * KP, b, &full[st]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kGWS_NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kGWS_NP; ++s) {
+      mbar_init(&pfull[s], 1);
+      mbar_init(&pempty[s], 8);                 // one arrival per consumer warp
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp >= 8) {
+    // ---- producers: TMA stage -> padded fp64 tile
+    const int ptid = tid - 256;
+    if (ptid == 0)
+      for (int s = 0; s < kGWS_NS; ++s) {
+        const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+        if (tile < ntiles) issue(s, tile);
+      }
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = it % kGWS_NS, pb = it % kGWS_NP;
+      const int rows = (int)imin64(kSTR, n_local - tile * kSTR);
+      mbar_wait(&full[st], (uint32_t)((it / kGWS_NS) & 1));
+      if (it >= kGWS_NP) mbar_wait(&pempty[pb], (uint32_t)(((it / kGWS_NP) - 1) & 1));
+      double* Zd = pad(pb, 0);
+      double* Xd = pad(pb, 1);
+      double* Yd = pad(pb, 2);
+      const T* sZ = arr(st, 0);
+      const T* sX = arr(st, 1);
+      const T* sY = arr(st, 2);
+      for (int e = ptid; e < kSTR * KP; e += 128) {
+        const int r = e / KP, c = e % KP;
+        const bool ok = r < rows;
+        Zd[r * LD + c] = ok ? (double)sZ[e] : 0.0;
+        if (MODE == 0) Xd[r * LD + c] = ok ? (double)sX[e] : 0.0;
+        Yd[r * LD + c] = ok ? (double)sY[e] : 0.0;
+      }
+      named_bar_sync(1, 128);                  // stage st consumed, tile pb written
+      if (ptid == 0) {
+        mbar_arrive(&pfull[pb]);
+        const int64_t nxt = tile + (int64_t)kGWS_NS * gridDim.x;
+        if (nxt < ntiles) issue(st, nxt);
+      }
+    }
+  } else {
+    // ---- consumers: DMMA Gram products on the padded tiles
+    typename GramSel<KP>::type acc;
+    acc.zero();
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int pb = it % kGWS_NP;
+      const int rows = (int)imin64(kSTR, n_local - tile * kSTR);
+      mbar_wait(&pfull[pb], (uint32_t)((it / kGWS_NP) & 1));
+      const double* Zd = pad(pb, 0);
+      const double* Xd = pad(pb, 1);
+      const double* Yd = pad(pb, 2);
+      const int r4 = (rows + 3) & ~3;
+      if (MODE == 0) acc.accumulate(Zd, Yd, Xd, Yd, r4, warp, lane);
+      else acc.accumulate(Zd, Zd, Zd, Yd, r4, warp, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pempty[pb]);
+    }
+    acc.store(part + (int64_t)blockIdx.x * 2 * KP * KP, warp, lane);
+  }
+}
+
+template <typename T, int KP, int MODE>
+static void launch_gs_ws(int64_t n, const void* Z, const void* X, const void* Y, double* part,
+                         const int* stop, int nblk, cudaStream_t st) {
+  const size_t smem = GSmemWS<T, KP>::bytes;
+  auto kern = k_gram_stream_ws<T, KP, MODE>;
+  static bool set = false;
+  if (!set) {
+    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = true;
+  }
+  kern<<<nblk, kGWS_THREADS, smem, st>>>(n, (const T*)Z, (const T*)X, (const T*)Y, part, stop);
+  OFSC_LAUNCH_CHECK();
+}
+
+static int gs_ws() {   // warp-specialised C2b (default; OFSC_GS_WS=0: staging-copy kernel)
+  static int v = -1;     // measured: c4 2.30 -> 2.27 ms, c3 0.0987 -> 0.0952 ms
+  if (v < 0) {
+    const char* e = getenv("OFSC_GS_WS");
+    v = (e && *e) ? atoi(e) : 1;
+  }
+  return v;
+}
+
 template <typename T, int KP, int MODE>
 static void launch_gs(int64_t n, const void* Z, const void* X, const void* Y, double* part,
                       const int* stop, int nblk, cudaStream_t st) {
@@ -484,7 +615,8 @@ static void launch_gs(int64_t n, const void* Z, const void* X, const void* Y, do
 int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n) {
   size_t b = 0;
   OFSC_DISPATCH_KP(KP, {
-    b = dt == OFSC_F64 ? GSmem<double, KPC>::bytes : GSmem<float, KPC>::bytes;
+    if (gs_ws()) b = dt == OFSC_F64 ? GSmemWS<double, KPC>::bytes : GSmemWS<float, KPC>::bytes;
+    else b = dt == OFSC_F64 ? GSmem<double, KPC>::bytes : GSmem<float, KPC>::bytes;
   });
   return stream_grid(n, b);
 }
@@ -493,6 +625,16 @@ void launch_gram_stream(ofsc_dtype dt, int KP, int64_t n, const void* Zown, cons
                         const void* Y, double* part, int mode, const int* stop, int nblk,
                         cudaStream_t st) {
   OFSC_DISPATCH_KP(KP, {
+    if (gs_ws()) {
+      if (dt == OFSC_F64) {
+        if (mode == 0) launch_gs_ws<double, KPC, 0>(n, Zown, Xown, Y, part, stop, nblk, st);
+        else launch_gs_ws<double, KPC, 1>(n, Zown, Xown, Y, part, stop, nblk, st);
+      } else {
+        if (mode == 0) launch_gs_ws<float, KPC, 0>(n, Zown, Xown, Y, part, stop, nblk, st);
+        else launch_gs_ws<float, KPC, 1>(n, Zown, Xown, Y, part, stop, nblk, st);
+      }
+      return;
+    }
     if (dt == OFSC_F64) {
       if (mode == 0) launch_gs<double, KPC, 0>(n, Zown, Xown, Y, part, stop, nblk, st);
       else launch_gs<double, KPC, 1>(n, Zown, Xown, Y, part, stop, nblk, st);

@@ -2,7 +2,7 @@
 # Bench lines for the other BASELINE configs / options (no e2e, no cpu baseline)
 out=gpurun_out/sweep
 mkdir -p $out
-for spec in "c1 f64 0" "c2 f64 0" "c2 f32 0" "c3 f64 0" "c3hi f64 0" "c5 f64 0" "c6 f64 0" "c4 f32 0" "c4 f64 1"; do
+for spec in "c1 f64 0" "c2 f64 0" "c2 f32 0" "c3 f64 0" "c3hi f64 0" "c5 f64 0" "c6 f64 0" "r22 f64 0" "c4 f32 0" "c4 f64 1"; do
   set -- $spec
   python bench.py --config $1 --dtype $2 --refresh $3 --no-e2e --no-cpu --steps 30 --warmup 3 \
     > $out/$1_$2_r$3.json 2> $out/$1_$2_r$3.err
