@@ -1324,11 +1324,14 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                          : kmeans_blocks(std::max<int64_t>(n_local, 1));
     const int nbp = fused ? nb : kmeans_partial_blocks(std::max<int64_t>(n_local, 1));
     const int W = dim + 1;
-    DBuf chg(8, s), pin((size_t)nb * 8, s), part((size_t)nbp * K * W * 8, s),
-        red((size_t)K * W * 8, s), tot(8, s);
+    DBuf chg(3 * 8, s), pin((size_t)nb * 8, s), part((size_t)nbp * K * W * 8, s),
+        red((size_t)K * W * 8, s), tot(8, s),
+        lbd(fused ? (size_t)std::max<int64_t>(n_local, 1) * 8 : 8, s), dlt((size_t)K * 8, s);
     OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
     unsigned long long* h_chg = nullptr;
-    OFSC_CUDA(cudaMallocHost(&h_chg, 8));
+    OFSC_CUDA(cudaMallocHost(&h_chg, 3 * 8));
+    const bool stats = getenv("OFSC_KMEANS_STATS") != nullptr;   // per-step skip statistics
+    const bool noskip = getenv("OFSC_KMEANS_NOSKIP") != nullptr; // A/B: no bound test
     struct HostFree {
       void* q;
       ~HostFree() { cudaFreeHost(q); }
@@ -1336,22 +1339,38 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
     int it = 0;
     double inertia = 0.0;
     for (it = 1; it <= max_iters; ++it) {
-      OFSC_CUDA(cudaMemsetAsync(chg.p, 0, 8, s));
+      OFSC_CUDA(cudaMemsetAsync(chg.p, 0, 3 * 8, s));
       OFSC_CUDA(cudaMemsetAsync(pin.p, 0, (size_t)nb * 8, s));
+      cudaEvent_t ea = nullptr, eb = nullptr;
+      if (stats) {
+        OFSC_CUDA(cudaEventCreate(&ea));
+        OFSC_CUDA(cudaEventCreate(&eb));
+        OFSC_CUDA(cudaEventRecord(ea, s));
+      }
       if (n_local > 0 && fused)
         launch_kmeans_step(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
-                           chg.as<unsigned long long>(), pin.as<double>(), part.as<double>(), nb, s);
+                           chg.as<unsigned long long>(), pin.as<double>(), part.as<double>(),
+                           lbd.as<double>(), it > 1 && !noskip ? dlt.as<double>() : nullptr, nb, s);
       else if (n_local > 0)
         launch_kmeans_assign(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
                              chg.as<unsigned long long>(), pin.as<double>(), nb, s);
+      if (stats) OFSC_CUDA(cudaEventRecord(eb, s));
       launch_reduce_partials(pin.as<double>(), nb, 1, tot.as<double>(), s);
       if (comm && comm->nranks > 1) {
         OFSC_NCCL(ncclAllReduce(chg.p, chg.p, 1, ncclUint64, ncclSum, comm->nccl, s));
         OFSC_NCCL(ncclAllReduce(tot.p, tot.p, 1, ncclFloat64, ncclSum, comm->nccl, s));
       }
-      OFSC_CUDA(cudaMemcpyAsync(h_chg, chg.p, 8, cudaMemcpyDeviceToHost, s));
+      OFSC_CUDA(cudaMemcpyAsync(h_chg, chg.p, 3 * 8, cudaMemcpyDeviceToHost, s));
       OFSC_CUDA(cudaMemcpyAsync(&inertia, tot.p, 8, cudaMemcpyDeviceToHost, s));
       OFSC_CUDA(cudaStreamSynchronize(s));
+      if (stats) {
+        float ms = 0.f;
+        OFSC_CUDA(cudaEventElapsedTime(&ms, ea, eb));
+        cudaEventDestroy(ea);
+        cudaEventDestroy(eb);
+        fprintf(stderr, "[ofsc kmeans] step %d changes %llu skipped %llu product_blocks %llu ms %.3f\n",
+                it, h_chg[0], h_chg[1], h_chg[2], ms);
+      }
       if (it > 1 && *h_chg == 0) break;
       if (n_local > 0 && !fused)
         launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nbp, s);
@@ -1360,7 +1379,8 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
       launch_reduce_partials(part.as<double>(), nbp, K * W, red.as<double>(), s);
       if (comm && comm->nranks > 1)
         OFSC_NCCL(ncclAllReduce(red.p, red.p, (size_t)K * W, ncclFloat64, ncclSum, comm->nccl, s));
-      launch_kmeans_finish(K, dim, red.as<double>(), d_centroids, s);
+      if (fused) launch_kmeans_finish_delta(K, dim, red.as<double>(), d_centroids, dlt.as<double>(), s);
+      else launch_kmeans_finish(K, dim, red.as<double>(), d_centroids, s);
     }
     OFSC_CUDA(cudaStreamSynchronize(s));
     if (iters_out) *iters_out = std::min(it, max_iters);

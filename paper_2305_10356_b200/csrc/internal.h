@@ -196,9 +196,16 @@ int kmeans_blocks(int64_t n);
 // Fused Lloyd step (assign + per-CTA partial sums, part[nblk][K][dim + 1]); dim <= 64, K <= 128.
 bool kmeans_step_supported(int dim, int K);
 int kmeans_step_blocks(int64_t n);
+// lbound[n]: per-row lower bound on the distance to the nearest other centroid
+// (written every step); delta[K]: centroid moves of the last update, NULL on the
+// first step (no bounds yet: every row is assigned by the products).
 void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                         const double* C, int* labels, unsigned long long* changes,
-                        double* part_inertia, double* part, int nblk, cudaStream_t st);
+                        double* part_inertia, double* part, double* lbound, const double* delta,
+                        int nblk, cudaStream_t st);
+// fused path: C = means (empty keeps), delta[c] = ||C_new - C_old|| (dim <= 64)
+void launch_kmeans_finish_delta(int K, int dim, const double* red, double* C, double* delta,
+                                cudaStream_t st);
 int kmeans_partial_blocks(int64_t n);
 
 // graph build (graph_build.cu)

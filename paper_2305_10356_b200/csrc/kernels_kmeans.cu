@@ -370,51 +370,158 @@ void launch_kmeans_assign(ofsc_dtype dt, int64_t n, int dim, const void* Y, int6
 // Fused Lloyd step (dim <= 64, K <= 128): assignment + per-CTA partial sums in
 // one pass over Y.  A CTA walks 32-row tiles (static stride, so the summation
 // order is fixed); the tile is staged in padded smem (next tile prefetched into
-// registers).  Warp w owns centroid blocks w (and w + 8):
-//   assign: its DMMA B fragments (C^T, DP/4 k-steps) stay in registers; the 4
-//           row blocks of the tile are 4 independent accumulation chains;
-//           scores ||c||^2 - 2 y.c; best / runner-up merged across lanes and
-//           warps (8 threads per row, butterfly; the merge is the lexicographic
-//           (score, index) minimum, so ties go to the lowest index); the same
-//           exactness guard as k_kmeans_assign_mma (direct form in d order when
-//           the margin is below tau);
-//   sums:   S[c][d] += sum_r [label_r = c] Y[r][d] on DMMA with the one-hot
-//           matrix as the A operand (products are exact, accumulation order is
-//           fixed by the tiling -> deterministic); accumulators stay in
-//           registers across tiles; a warp skips k-steps whose 4 rows carry
-//           none of its centroids.  Counts: integer smem atomics (exact).
+// registers).
+//   skip test (steps >= 2; Hamerly's bounds, exact decisions): every row keeps a
+//           lower bound lb_r <= min_{c != a} ||y_r - c|| for its label a.  After
+//           the centroids moved by delta_c (triangle inequality) it becomes
+//           lb_r - max_{c != a} delta_c; the distance to the own centroid is
+//           recomputed directly (d order, 8 lanes).  If sqrt(D_a) (1 + rel) <
+//           lb (rel = 1e-12 >> the (dim + 2) u rounding of either side's
+//           distances), every other centroid is strictly farther in the
+//           oracle's arithmetic too, so its argmin is a: the row keeps its
+//           label and its distance, and needs no assignment products.
+//   assign: only for 8-row blocks holding a row that failed the test.  Warp w
+//           owns centroid blocks w (and w + 8); its DMMA B fragments (C^T, DP/4
+//           k-steps) stay in registers; scores ||c||^2 - 2 y.c; best /
+//           runner-up merged across lanes and warps (8 threads per row,
+//           butterfly; the merge is the lexicographic (score, index) minimum,
+//           so ties go to the lowest index); the same exactness guard as
+//           k_kmeans_assign_mma (direct form in d order when the margin is
+//           below tau).  The runner-up score gives the row's new lower bound.
+//   sums:   S[c][d] += Y[r][d] for label_r = c, by the warp owning c (lane l:
+//           columns 2l, 2l + 1), rows in tile order: fixed order, no atomics,
+//           deterministic.  Counts: integer smem atomics (exact).
 // part[b] = (sums, count) per centroid feeds the fixed-order reduction.
 // ---------------------------------------------------------------------------
 constexpr int kKsRows = 32;
+constexpr int kKsStages = 3;
+static_assert(kKsRows == 32, "the row-mask logic maps tile rows to lanes");
+constexpr double kKmRel = 1e-12;   // relative margin of the bound tests
+
+// Scores of NBLK compacted 8-row blocks against this warp's centroid blocks:
+// best / runner-up (score, index) per row slot, merged over the row's 4 lanes.
+template <int NBLK, int NBW, int DP>
+__device__ __forceinline__ void km_assign_blocks(const double* Ys, const int (&rowA)[4],
+                                                 const double (&bf)[NBW][DP / 4],
+                                                 const double* cn, int warp, int KB, int tig,
+                                                 double (&b1)[4], double (&b2)[4], int (&c1)[4]) {
+  constexpr int LDY = DP + 4;
+  // CH independent accumulation chains per block (k-steps kk = ch mod CH), so a
+  // single block is not one 16-deep dependent DMMA chain
+  constexpr int CH = NBLK >= 4 ? 1 : (NBLK == 3 ? 1 : 4 / NBLK);
+#pragma unroll
+  for (int q = 0; q < NBW; ++q) {
+    const int cb = warp + 8 * q;
+    if (cb < KB) {
+      double a[NBLK][CH][2];
+#pragma unroll
+      for (int rb = 0; rb < NBLK; ++rb)
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) a[rb][ch][0] = a[rb][ch][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < DP / 4; ++kk)
+#pragma unroll
+        for (int rb = 0; rb < NBLK; ++rb)
+          dmma(a[rb][kk % CH][0], a[rb][kk % CH][1], Ys[rowA[rb] * LDY + 4 * kk + tig], bf[q][kk]);
+#pragma unroll
+      for (int rb = 0; rb < NBLK; ++rb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = cb * 8 + 2 * tig + h;
+          double dot = a[rb][0][h];
+#pragma unroll
+          for (int ch = 1; ch < CH; ++ch) dot += a[rb][ch][h];
+          const double sc = cn[c] - 2.0 * dot;
+          if (sc < b1[rb] || (sc == b1[rb] && c < c1[rb])) {
+            b2[rb] = b1[rb];
+            b1[rb] = sc;
+            c1[rb] = c;
+          } else if (sc < b2[rb]) {
+            b2[rb] = sc;
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int rb = 0; rb < NBLK; ++rb)
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {             // merge the 4 lanes of the row
+      const double ob1 = __shfl_xor_sync(0xffffffffu, b1[rb], o);
+      const double ob2 = __shfl_xor_sync(0xffffffffu, b2[rb], o);
+      const int oc1 = __shfl_xor_sync(0xffffffffu, c1[rb], o);
+      if (ob1 < b1[rb] || (ob1 == b1[rb] && oc1 < c1[rb])) {
+        b2[rb] = fmin(b1[rb], ob2);
+        b1[rb] = ob1;
+        c1[rb] = oc1;
+      } else {
+        b2[rb] = fmin(b2[rb], ob1);
+      }
+    }
+}
 
 template <typename T, int NBW, int DP>
 __global__ void __launch_bounds__(kKmThreads, NBW == 1 ? 2 : 1)
 k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
               const double* __restrict__ C, int* __restrict__ labels,
-              unsigned long long* changes, double* part_inertia, double* part) {
+              unsigned long long* changes, double* part_inertia, double* part,
+              double* __restrict__ lbound, const double* __restrict__ delta) {
   // DP: dim rounded up to a multiple of 16 (padding columns are zero)
   constexpr int TR = kKsRows;
-  constexpr int PRE = TR * DP / kKmThreads;       // prefetched doubles per thread
+  constexpr int PRE = TR * DP / kKmThreads;       // tile elements per thread
   constexpr int LDY = DP + 4;
+  constexpr int KPW = 64 * NBW;
+  constexpr int NST = kKsStages;                   // tile ring: 2 tiles in flight
   extern __shared__ double sm[];
   const int W = dim + 1;
   const int KB = (K + 7) / 8;
-  double* Ys = sm;                                 // [TR][LDY]
-  double* cn = Ys + TR * LDY;                      // [64 * NBW] ||c||^2 (inf for padding)
-  double* mb1 = cn + 64 * NBW;                     // [TR][8 warps]
+  double* Ysr = sm;                                // [NST][TR][LDY]
+  double* s_lb = Ysr + NST * TR * LDY;             // [NST][TR] lower bounds of the tile rows
+  double* cn = s_lb + NST * TR;                    // [KPW] ||c||^2 (inf for padding)
+  double* Cs = cn + KPW;                           // [KPW][DP] centroids (direct distances)
+  double* mb1 = Cs + KPW * DP;                     // [TR][8 warps]
   double* mb2 = mb1 + 8 * TR;
   int* mc1 = (int*)(mb2 + 8 * TR);                 // [TR][8 warps]
   int* tl = mc1 + 8 * TR;                          // [TR] tile labels (-1: padding row)
-  int* cnt = tl + TR;                              // [64 * NBW]
+  int* cnt = tl + TR;                              // [KPW]
+  int* fl = cnt + KPW;                             // [TR] row failed the bound test
+  int* s_lab = fl + TR;                            // [NST][TR] labels of the tile rows
   __shared__ double s_in[kKmThreads / 32];
+  __shared__ double s_m1, s_m2, s_cnmax;
+  __shared__ int s_i1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
-  for (int c = tid; c < 64 * NBW; c += kKmThreads) {
+  for (int c = tid; c < KPW; c += kKmThreads) {
     double a = 0.0;
     if (c < K)
       for (int d = 0; d < dim; ++d) a = a + C[c * dim + d] * C[c * dim + d];
     cn[c] = c < K ? a : CUDART_INF;
     cnt[c] = 0;
+  }
+  for (int e = tid; e < KPW * DP; e += kKmThreads) {
+    const int c = e / DP, d = e % DP;
+    Cs[e] = (c < K && d < dim) ? C[c * dim + d] : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // largest and second largest centroid move (excluding-own maximum), max ||c||^2
+    double m1 = 0.0, m2 = 0.0, cm = 0.0;
+    int i1 = -1;
+    for (int c = 0; c < K; ++c) {
+      cm = fmax(cm, cn[c]);
+      if (!delta) continue;
+      const double v = delta[c];
+      if (v > m1) {
+        m2 = m1;
+        m1 = v;
+        i1 = c;
+      } else if (v > m2) {
+        m2 = v;
+      }
+    }
+    s_m1 = m1;
+    s_m2 = m2;
+    s_i1 = i1;
+    s_cnmax = cm;
   }
   // register-resident B fragments: B[k = d][n = c] = C[c][d], d = 4 kk + tig, c = cb*8 + gid
   double bf[NBW][DP / 4];
@@ -427,187 +534,243 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
       bf[q][kk] = (c < K && d < dim) ? C[c * dim + d] : 0.0;
     }
   }
-  double sacc[NBW][DP / 8][2];                     // sums S[cb*8 + gid][db*8 + 2 tig + h]
+  double sacc[NBW][8][2];                          // sums S[cb*8 + j][2 lane + h]
 #pragma unroll
   for (int q = 0; q < NBW; ++q)
 #pragma unroll
-    for (int db = 0; db < DP / 8; ++db) sacc[q][db][0] = sacc[q][db][1] = 0.0;
+    for (int j = 0; j < 8; ++j) sacc[q][j][0] = sacc[q][j][1] = 0.0;
   const int64_t ntiles = (n + TR - 1) / TR;
-  double pre[PRE];
-  int old_pre = 0;                                 // previous label of row (tid >> 3), w == 0 lanes
-  auto fetch = [&](int64_t tile) {
+  const int rrow = tid >> 3, rw = tid & 7;         // row phases: 8 threads per row
+  // tile `tile` -> ring slot: Y rows (fp64 padded; cp.async, zero-filled outside
+  // [0, n) x [0, dim)), their labels and lower bounds; one commit group per call
+  auto issue = [&](int64_t tile, int slot) {
     const int64_t r0 = tile * TR;
+    double* Yd = Ysr + slot * TR * LDY;
 #pragma unroll
     for (int j = 0; j < PRE; ++j) {
       const int e = tid + kKmThreads * j;         // e < TR * DP
       const int q = e / DP, d = e % DP;
-      pre[j] = (d < dim && r0 + q < n) ? ld1(Y + (r0 + q) * ldy + d) : 0.0;
+      const bool ok = d < dim && r0 + q < n;
+      const T* src = ok ? Y + (r0 + q) * ldy + d : Y;
+      if constexpr (sizeof(T) == 8) cp_async<8>(&Yd[q * LDY + d], src, ok ? 8 : 0);
+      else Yd[q * LDY + d] = ok ? (double)*src : 0.0;
     }
-    if ((tid & 7) == 0 && r0 + (tid >> 3) < n) old_pre = labels[r0 + (tid >> 3)];
+    if (tid < TR) {
+      const bool ok = r0 + tid < n;
+      cp_async<4>(&s_lab[slot * TR + tid], ok ? labels + r0 + tid : labels, ok ? 4 : 0);
+    } else if (tid < 2 * TR && delta) {
+      const bool ok = r0 + tid - TR < n;
+      cp_async<8>(&s_lb[slot * TR + tid - TR], ok ? lbound + r0 + tid - TR : lbound, ok ? 8 : 0);
+    }
+    cp_async_commit();
   };
-  if ((int64_t)blockIdx.x < ntiles) fetch(blockIdx.x);
+#pragma unroll
+  for (int s0 = 0; s0 < NST - 1; ++s0) {
+    const int64_t t0 = blockIdx.x + (int64_t)s0 * gridDim.x;
+    if (t0 < ntiles) issue(t0, s0);
+    else cp_async_commit();
+  }
+  __syncthreads();
+  const double tau_c = s_cnmax;
   double inertia = 0.0;
-  unsigned long long nchg = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  unsigned int nchg = 0, nskip = 0, ntile = 0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int64_t r0 = tile * TR;
     const int rows = (int)imin64(TR, n - r0);
-    __syncthreads();                               // previous tile fully consumed
-#pragma unroll
-    for (int j = 0; j < PRE; ++j) {
-      const int e = tid + kKmThreads * j;
-      Ys[(e / DP) * LDY + e % DP] = pre[j];
+    const int slot = it % NST;
+    cp_async_wait<NST - 2>();                      // this thread's copies of `tile` landed
+    __syncthreads();                               // all copies visible; previous tile consumed
+    {
+      const int64_t nxt = tile + (int64_t)(NST - 1) * gridDim.x;
+      if (nxt < ntiles) issue(nxt, (it + NST - 1) % NST);
+      else cp_async_commit();
     }
-    const int old_lab = old_pre;
-    __syncthreads();
-    if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
-    // ---- assign: this warp's centroid blocks x the 4 row blocks
-    double b1[TR / 8], b2[TR / 8];
-    int c1[TR / 8];
+    const double* Ys = Ysr + slot * TR * LDY;
+    const int old_lab = rrow < rows ? s_lab[slot * TR + rrow] : -1;
+    const double old_lb = delta ? s_lb[slot * TR + rrow] : 0.0;
+    // ---- skip test (8 threads per row; all lanes take the shuffles)
+    const bool vrow = rrow < rows;
+    bool skip = false;
+    double Da = 0.0, lnew = 0.0, yn;
+    {
+      const int a = old_lab >= 0 ? old_lab : 0;
+      double sd = 0.0;                             // ||y - c_a||^2 and ||y||^2 (padding
+      yn = 0.0;                                    // columns are zero on both sides)
 #pragma unroll
-    for (int rb = 0; rb < TR / 8; ++rb) {
-      b1[rb] = CUDART_INF;
-      b2[rb] = CUDART_INF;
-      c1[rb] = 0x7fffffff;
-    }
-#pragma unroll
-    for (int q = 0; q < NBW; ++q) {
-      const int cb = warp + 8 * q;
-      if (cb < KB) {
-        double a[TR / 8][2];
-#pragma unroll
-        for (int rb = 0; rb < TR / 8; ++rb) a[rb][0] = a[rb][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < DP / 4; ++kk)
-#pragma unroll
-            for (int rb = 0; rb < TR / 8; ++rb)
-              dmma(a[rb][0], a[rb][1], Ys[(rb * 8 + gid) * LDY + 4 * kk + tig], bf[q][kk]);
-#pragma unroll
-        for (int rb = 0; rb < TR / 8; ++rb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = cb * 8 + 2 * tig + h;
-            const double sc = cn[c] - 2.0 * a[rb][h];
-            if (sc < b1[rb] || (sc == b1[rb] && c < c1[rb])) {
-              b2[rb] = b1[rb];
-              b1[rb] = sc;
-              c1[rb] = c;
-            } else if (sc < b2[rb]) {
-              b2[rb] = sc;
-            }
-          }
+      for (int i = 0; i < DP / 8; ++i) {
+        const int d = rw + 8 * i;
+        const double y = Ys[rrow * LDY + d];
+        const double df = y - Cs[a * DP + d];
+        sd = fma(df, df, sd);
+        yn = fma(y, y, yn);
       }
+#pragma unroll
+      for (int o = 1; o <= 4; o <<= 1) {
+        sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        yn += __shfl_xor_sync(0xffffffffu, yn, o);
+      }
+      if (delta && vrow && old_lab >= 0) {
+        const double dm = old_lab == s_i1 ? s_m2 : s_m1;
+        Da = sd;
+        lnew = old_lb - dm - kKmRel * (old_lb + dm);
+        skip = sqrt(Da) * (1.0 + kKmRel) < lnew;
+      }
+      if (rw == 0) fl[rrow] = (vrow && !skip) ? 1 : 0;
+      if (rw == 0 && skip) ++nskip;
     }
+    __syncthreads();
+    // products only for the rows that failed, compacted into ceil(nf / 8) blocks
+    const unsigned fmask = __ballot_sync(0xffffffffu, fl[lane] != 0);   // TR == 32 rows
+    const int nf = __popc(fmask);
+    const int nblk = (nf + 7) >> 3;
+    if (tid == 0) ntile += nblk;
+    if (nblk) {
+      int rowA[4];
+      double b1[4], b2[4];
+      int c1[4];
 #pragma unroll
-    for (int rb = 0; rb < TR / 8; ++rb) {
-#pragma unroll
-      for (int o = 1; o <= 2; o <<= 1) {           // merge the 4 lanes of the row
-        const double ob1 = __shfl_xor_sync(0xffffffffu, b1[rb], o);
-        const double ob2 = __shfl_xor_sync(0xffffffffu, b2[rb], o);
-        const int oc1 = __shfl_xor_sync(0xffffffffu, c1[rb], o);
-        if (ob1 < b1[rb] || (ob1 == b1[rb] && oc1 < c1[rb])) {
-          b2[rb] = fmin(b1[rb], ob2);
-          b1[rb] = ob1;
-          c1[rb] = oc1;
-        } else {
-          b2[rb] = fmin(b2[rb], ob1);
-        }
+      for (int rb = 0; rb < 4; ++rb) {
+        const int sl = rb * 8 + gid;                 // compact slot -> tile row
+        const int rr = sl < nf ? (int)__fns(fmask, 0, sl + 1) : 0;
+        rowA[rb] = rr;
+        b1[rb] = CUDART_INF;
+        b2[rb] = CUDART_INF;
+        c1[rb] = 0x7fffffff;
+      }
+      switch (nblk) {
+        case 1: km_assign_blocks<1, NBW, DP>(Ys, rowA, bf, cn, warp, KB, tig, b1, b2, c1); break;
+        case 2: km_assign_blocks<2, NBW, DP>(Ys, rowA, bf, cn, warp, KB, tig, b1, b2, c1); break;
+        case 3: km_assign_blocks<3, NBW, DP>(Ys, rowA, bf, cn, warp, KB, tig, b1, b2, c1); break;
+        default: km_assign_blocks<4, NBW, DP>(Ys, rowA, bf, cn, warp, KB, tig, b1, b2, c1); break;
       }
       if (tig == 0) {
-        const int r = rb * 8 + gid;
-        mb1[r * 8 + warp] = b1[rb];
-        mb2[r * 8 + warp] = b2[rb];
-        mc1[r * 8 + warp] = c1[rb];
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          if (rb < nblk) {
+            const int sl = rb * 8 + gid;
+            mb1[sl * 8 + warp] = b1[rb];
+            mb2[sl * 8 + warp] = b2[rb];
+            mc1[sl * 8 + warp] = c1[rb];
+          }
+        }
       }
     }
     __syncthreads();
     {
-      // merge across warps: 8 threads per row (thread = (row, warp slot))
-      const int r = tid >> 3, w = tid & 7;
-      double x1 = mb1[r * 8 + w], x2 = mb2[r * 8 + w];
-      int xc = mc1[r * 8 + w];
-      double yn = 0.0;                             // ||y||^2: 8 partial sums, butterfly
-      for (int d = w; d < dim; d += 8) yn = fma(Ys[r * LDY + d], Ys[r * LDY + d], yn);
-#pragma unroll
-      for (int o = 1; o <= 4; o <<= 1) {
-        const double ob1 = __shfl_xor_sync(0xffffffffu, x1, o);
-        const double ob2 = __shfl_xor_sync(0xffffffffu, x2, o);
-        const int oc1 = __shfl_xor_sync(0xffffffffu, xc, o);
-        if (ob1 < x1 || (ob1 == x1 && oc1 < xc)) {
-          x2 = fmin(x1, ob2);
-          x1 = ob1;
-          xc = oc1;
-        } else {
-          x2 = fmin(x2, ob1);
-        }
-        yn += __shfl_xor_sync(0xffffffffu, yn, o);
-      }
-      int lab = xc;
-      double dist = yn + x1;
-      if (!(x2 - x1 > 1e-12 * (1.0 + yn))) {       // direct form, exactly as the oracle
-        double best = CUDART_INF;                  // centroids c = w, w + 8, ... then merged
-        int bc = 0x7fffffff;
-        for (int c = w; c < K; c += 8) {
-          double a = 0.0;
-          for (int d = 0; d < dim; ++d) {
-            const double diff = Ys[r * LDY + d] - C[c * dim + d];
-            a = a + diff * diff;
-          }
-          if (a < best) {                          // c increases: lowest index wins ties
-            best = a;
-            bc = c;
-          }
-        }
-        const unsigned gmask = 0xffu << (lane & 24);   // the row's 8 lanes (all take this branch)
+      // merge across warps: 8 threads per row (thread = (row, warp slot)); when any
+      // row of the tile ran the products every lane runs the butterflies, rows
+      // that skipped ignore the result
+      const int r = rrow, w = rw;
+      int lab = old_lab;
+      double dist = Da;
+      if (fmask) {
+        const bool blk = (fmask >> r) & 1u;
+        const int sl = __popc(fmask & ((1u << r) - 1u));   // compact slot of row r
+        double x1 = blk ? mb1[sl * 8 + w] : CUDART_INF, x2 = blk ? mb2[sl * 8 + w] : CUDART_INF;
+        int xc = blk ? mc1[sl * 8 + w] : 0;
 #pragma unroll
         for (int o = 1; o <= 4; o <<= 1) {
-          const double ob = __shfl_xor_sync(gmask, best, o);
-          const int oc = __shfl_xor_sync(gmask, bc, o);
-          if (ob < best || (ob == best && oc < bc)) {
-            best = ob;
-            bc = oc;
+          const double ob1 = __shfl_xor_sync(0xffffffffu, x1, o);
+          const double ob2 = __shfl_xor_sync(0xffffffffu, x2, o);
+          const int oc1 = __shfl_xor_sync(0xffffffffu, xc, o);
+          if (ob1 < x1 || (ob1 == x1 && oc1 < xc)) {
+            x2 = fmin(x1, ob2);
+            x1 = ob1;
+            xc = oc1;
+          } else {
+            x2 = fmin(x2, ob1);
           }
         }
-        lab = bc;
-        dist = best;
+        if (!skip && vrow) {
+          // score error bound: (dim + 2) u (||y||^2 + ||c||^2) per score, dim <= 64
+          const double tau = 1e-12 * (1.0 + yn + tau_c);
+          lab = xc;
+          dist = yn + x1;
+          lnew = sqrt(fmax(yn + x2 - 2.0 * tau, 0.0));
+          if (!(x2 - x1 > tau)) {                  // direct form, exactly as the oracle
+            double best = CUDART_INF;              // centroids c = w, w + 8, ... then merged
+            int bc = 0x7fffffff;
+            for (int c = w; c < K; c += 8) {
+              double a = 0.0;
+              for (int d = 0; d < dim; ++d) {
+                const double diff = Ys[r * LDY + d] - C[c * dim + d];
+                a = a + diff * diff;
+              }
+              if (a < best) {                      // c increases: lowest index wins ties
+                best = a;
+                bc = c;
+              }
+            }
+            const unsigned gmask = 0xffu << (lane & 24);   // the row's 8 lanes (all take this branch)
+#pragma unroll
+            for (int o = 1; o <= 4; o <<= 1) {
+              const double ob = __shfl_xor_sync(gmask, best, o);
+              const int oc = __shfl_xor_sync(gmask, bc, o);
+              if (ob < best || (ob == best && oc < bc)) {
+                best = ob;
+                bc = oc;
+              }
+            }
+            lab = bc;
+            dist = best;
+            lnew = 0.0;                            // near tie: recompute next step
+          }
+        }
       }
       if (w == 0) {
         tl[r] = r < rows ? lab : -1;
         if (r < rows) {
           if (old_lab != lab) ++nchg;
           labels[r0 + r] = lab;
+          lbound[r0 + r] = lnew;
           inertia += dist;
           atomicAdd(&cnt[lab], 1);                 // integer: exact
         }
       }
     }
     __syncthreads();
-    // ---- sums on DMMA: S(cb block x d) += onehot(cb block x 4 rows) Y(4 rows x d)
+    // ---- sums: the warp owning the label adds the row (lane: columns 2 lane, 2 lane + 1),
+    // rows in tile order
+    {
+      const int labl = tl[lane];                     // TR == 32: lane = tile row
 #pragma unroll
-    for (int q = 0; q < NBW; ++q) {
-      const int cb = warp + 8 * q;
-      if (cb < KB) {
-        const int cl = cb * 8;
-#pragma unroll
-        for (int k0 = 0; k0 < TR; k0 += 4) {
-          const int l4 = tl[k0 + tig];
-          const bool any = __any_sync(0xffffffffu, l4 >= cl && l4 < cl + 8);
-          if (!any) continue;
-          const double a = (l4 == cl + gid) ? 1.0 : 0.0;
-          const double* yb = Ys + (k0 + tig) * LDY + gid;
-#pragma unroll
-          for (int db = 0; db < DP / 8; ++db) dmma(sacc[q][db][0], sacc[q][db][1], a, yb[db * 8]);
+      for (int q = 0; q < NBW; ++q) {
+        const int cb = warp + 8 * q;
+        unsigned mk = __ballot_sync(0xffffffffu, (labl >> 3) == cb);
+        while (mk) {
+          const int r = __ffs(mk) - 1;
+          mk &= mk - 1u;
+          const int lab = __shfl_sync(0xffffffffu, labl, r);
+          if (2 * lane < DP) {
+            const double y0 = Ys[r * LDY + 2 * lane], y1 = Ys[r * LDY + 2 * lane + 1];
+            switch (lab & 7) {
+#define OFSC_KS_ADD(J)          \
+  case J:                       \
+    sacc[q][J][0] += y0;        \
+    sacc[q][J][1] += y1;        \
+    break;
+              OFSC_KS_ADD(0) OFSC_KS_ADD(1) OFSC_KS_ADD(2) OFSC_KS_ADD(3)
+              OFSC_KS_ADD(4) OFSC_KS_ADD(5) OFSC_KS_ADD(6) OFSC_KS_ADD(7)
+#undef OFSC_KS_ADD
+            }
+          }
         }
       }
     }
   }
+  cp_async_wait<0>();
   for (int o = 16; o; o >>= 1) {
     inertia += __shfl_xor_sync(0xffffffffu, inertia, o);
     nchg += __shfl_xor_sync(0xffffffffu, nchg, o);
+    nskip += __shfl_xor_sync(0xffffffffu, nskip, o);
   }
   if (lane == 0) {
     s_in[warp] = inertia;
-    if (nchg) atomicAdd(changes, nchg);            // integer: order-independent
+    if (nchg) atomicAdd(changes, (unsigned long long)nchg);        // integer: order-independent
+    if (nskip) atomicAdd(changes + 1, (unsigned long long)nskip);  // statistics: rows that skipped
   }
+  if (tid == 0 && ntile) atomicAdd(changes + 2, (unsigned long long)ntile);   // 8-row product blocks
   __syncthreads();
   if (tid == 0) {
     double a = 0.0;
@@ -616,30 +779,31 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
   }
   double* pb = part + (int64_t)blockIdx.x * K * W;
 #pragma unroll
-  for (int q = 0; q < NBW; ++q) {
-    const int c = (warp + 8 * q) * 8 + gid;
-    if (c < K) {
+  for (int q = 0; q < NBW; ++q)
 #pragma unroll
-      for (int db = 0; db < DP / 8; ++db)
+    for (int j = 0; j < 8; ++j) {
+      const int c = (warp + 8 * q) * 8 + j;
+      if (c < K) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int d = db * 8 + 2 * tig + h;
-          if (d < dim) pb[c * W + d] = sacc[q][db][h];
+          const int d = 2 * lane + h;
+          if (d < dim) pb[c * W + d] = sacc[q][j][h];
         }
+      }
     }
-  }
   for (int c = tid; c < K; c += kKmThreads) pb[c * W + dim] = (double)cnt[c];
 }
 
 size_t kmeans_step_smem(int dim, int K) {
   const int DP = (dim + 15) & ~15;
-  const int nbw = K > 64 ? 2 : 1;
-  return ((size_t)kKsRows * (DP + 4) + 64 * nbw + 16 * kKsRows) * 8 +
-         ((size_t)9 * kKsRows + 64 * nbw) * 4;
+  const int kpw = K > 64 ? 128 : 64;
+  return ((size_t)kKsStages * kKsRows * (DP + 4) + kKsStages * kKsRows + kpw + (size_t)kpw * DP +
+          16 * kKsRows) * 8 +
+         ((size_t)10 * kKsRows + kpw + kKsStages * kKsRows) * 4;
 }
 
 bool kmeans_step_supported(int dim, int K) {
-  return dim <= 64 && K <= 128 && kmeans_step_smem(dim, K) <= 100 * 1024 &&
+  return dim <= 64 && K <= 128 && kmeans_step_smem(dim, K) <= 200 * 1024 &&
          getenv("OFSC_KMEANS_DIRECT") == nullptr && getenv("OFSC_KMEANS_UNFUSED") == nullptr;
 }
 
@@ -651,14 +815,15 @@ int kmeans_step_blocks(int64_t n) {
 
 void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                         const double* C, int* labels, unsigned long long* changes,
-                        double* part_inertia, double* part, int nblk, cudaStream_t st) {
+                        double* part_inertia, double* part, double* lbound, const double* delta,
+                        int nblk, cudaStream_t st) {
   const size_t smem = kmeans_step_smem(dim, K);
 #define OFSC_KS3(TT, NB, DPC)                                                                    \
   {                                                                                              \
     OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_step<TT, NB, DPC>,                                   \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
-    k_kmeans_step<TT, NB, DPC><<<nblk, kKmThreads, smem, st>>>(n, dim, (const TT*)Y, ldy, K, C,  \
-                                                               labels, changes, part_inertia, part); \
+    k_kmeans_step<TT, NB, DPC><<<nblk, kKmThreads, smem, st>>>(                                  \
+        n, dim, (const TT*)Y, ldy, K, C, labels, changes, part_inertia, part, lbound, delta);   \
   }
 #define OFSC_KS(TT, NB)                                                                          \
   switch ((dim + 15) / 16) {                                                                     \
@@ -674,6 +839,37 @@ void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_
   }
 #undef OFSC_KS
 #undef OFSC_KS3
+  OFSC_LAUNCH_CHECK();
+}
+
+// New centroids of the fused path and their moves: one CTA per centroid,
+// thread d < dim: C[c][d] = mean (empty keeps it); delta[c] = ||C_new - C_old||
+// (fixed-order sum, inflated by 1e-12 so it bounds the exact move).
+__global__ void k_kmeans_finish_delta(int K, int dim, const double* red, double* C,
+                                      double* delta) {
+  __shared__ double s[64];
+  const int c = blockIdx.x, d = threadIdx.x;
+  double df2 = 0.0;
+  if (d < dim) {
+    const double cntv = red[c * (dim + 1) + dim];
+    const double old = C[c * dim + d];
+    const double nw = cntv > 0.0 ? red[c * (dim + 1) + d] / cntv : old;
+    C[c * dim + d] = nw;
+    const double df = nw - old;
+    df2 = df * df;
+  }
+  s[d] = df2;
+  __syncthreads();
+  if (d == 0) {
+    double a = 0.0;
+    for (int e = 0; e < dim; ++e) a += s[e];
+    delta[c] = sqrt(a) * (1.0 + 1e-12);
+  }
+}
+
+void launch_kmeans_finish_delta(int K, int dim, const double* red, double* C, double* delta,
+                                cudaStream_t st) {
+  k_kmeans_finish_delta<<<K, 64, 0, st>>>(K, dim, red, C, delta);
   OFSC_LAUNCH_CHECK();
 }
 

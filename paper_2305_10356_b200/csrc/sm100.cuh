@@ -67,6 +67,21 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- cp.async (LDGSTS): per-thread global -> shared copies, zero-filled
+// beyond src_bytes; completion by commit / wait groups --------------------------
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, int src_bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(gsrc), "n"(BYTES),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---- fp64 MMA: D(8x8) += A(8x4) B(4x8) --------------------------------------
 // Fragments (PTX ISA, m8n8k4 .f64): gid = lane >> 2, tig = lane & 3;
 //   a = A[gid][tig], b = B[tig][gid], d0 = D[gid][2 tig], d1 = D[gid][2 tig + 1].
