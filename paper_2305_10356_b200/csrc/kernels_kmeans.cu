@@ -543,9 +543,21 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
   const int rrow = tid >> 3, rw = tid & 7;         // row phases: 8 threads per row
   // tile `tile` -> ring slot: Y rows (fp64 padded; cp.async, zero-filled outside
   // [0, n) x [0, dim)), their labels and lower bounds; one commit group per call
+  // full-width fp64 rows, 16-byte aligned: 16-byte copies from one base pointer
+  const bool vec16 = sizeof(T) == 8 && kKmThreads % (DP / 2) == 0 && dim == DP && (ldy & 1) == 0 &&
+                     (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
   auto issue = [&](int64_t tile, int slot) {
     const int64_t r0 = tile * TR;
     double* Yd = Ysr + slot * TR * LDY;
+    if (vec16 && r0 + TR <= n) {
+      constexpr int H = DP / 2;                   // 16-byte chunks per row
+      constexpr int RS = kKmThreads / H;          // rows advanced per j
+      const int q0 = tid / H, c2 = 2 * (tid % H);
+      const T* src = Y + (r0 + q0) * ldy + c2;
+      double* dst = Yd + q0 * LDY + c2;
+#pragma unroll
+      for (int j = 0; j < PRE / 2; ++j) cp_async<16>(dst + j * RS * LDY, src + (int64_t)(j * RS) * ldy, 16);
+    } else {
 #pragma unroll
     for (int j = 0; j < PRE; ++j) {
       const int e = tid + kKmThreads * j;         // e < TR * DP
@@ -554,6 +566,7 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
       const T* src = ok ? Y + (r0 + q) * ldy + d : Y;
       if constexpr (sizeof(T) == 8) cp_async<8>(&Yd[q * LDY + d], src, ok ? 8 : 0);
       else Yd[q * LDY + d] = ok ? (double)*src : 0.0;
+    }
     }
     if (tid < TR) {
       const bool ok = r0 + tid < n;
