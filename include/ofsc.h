@@ -305,7 +305,7 @@ ofsc_status ofsc_scores(int64_t n, const int32_t* h_a, const int32_t* h_b, doubl
                         double* nmi);
 
 /* Algorithm 1 end to end from HOST buffers: edges (m, full list) -> build A
- * (bopts NULL: LPA locality reordering iff opts->max_iters >= 100) -> run `method` from h_X
+ * (bopts NULL: LPA locality reordering iff opts->max_iters >= 32) -> run `method` from h_X
  * (ALL n rows x k in original node order, dense ld = k, dtype dt; in: X0, out:
  * features before normalisation for the nodes this rank owns) -> row-normalise
  * -> K-means with centroids initialised at the original node ids

@@ -48,8 +48,10 @@ struct DBuf {
   DBuf(size_t bytes, cudaStream_t st) : s(st) {
     if (bytes) OFSC_CUDA(cudaMallocAsync(&p, bytes, st));
   }
-  ~DBuf() {
+  ~DBuf() { release(); }
+  void release() {
     if (p) cudaFreeAsync(p, s);
+    p = nullptr;
   }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
@@ -305,10 +307,10 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     CsrDevice csr;
     int64_t n_comm = 0;
     double intra = 0.0;
-    auto free_csr = [&] {
-      dfree(csr.row_ptr);
-      dfree(csr.col);
-      dfree(csr.s);
+    auto free_csr = [&] {   // stream-ordered pool frees: no device-wide synchronisation
+      if (csr.row_ptr) cudaFreeAsync(csr.row_ptr, s);
+      if (csr.col) cudaFreeAsync(csr.col, s);
+      if (csr.s) cudaFreeAsync(csr.s, s);
       csr.row_ptr = nullptr;
       csr.col = nullptr;
       csr.s = nullptr;
@@ -418,9 +420,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       OFSC_CUDA(cudaStreamSynchronize(s));
       build_heavy(g->row_ptr_loc, g->n_local, g->heavy_loc, s);
       build_heavy(g->row_ptr_rem, g->n_local, g->heavy_rem, s);
-      dfree(csr.row_ptr);
-      dfree(csr.col);
-      dfree(csr.s);
+      free_csr();
     }
     OFSC_CUDA(cudaStreamSynchronize(s));
     ofsc_graph_info& in = g->info;
@@ -1328,14 +1328,12 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
         red((size_t)K * W * 8, s), tot(8, s),
         lbd(fused ? (size_t)std::max<int64_t>(n_local, 1) * 8 : 8, s), dlt((size_t)K * 8, s);
     OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
-    unsigned long long* h_chg = nullptr;
-    OFSC_CUDA(cudaMallocHost(&h_chg, 3 * 8));
+    // pinned counter readback, allocated once per host thread (cudaFreeHost would
+    // synchronise the whole device, e.g. the feature download of spectral_cluster)
+    static thread_local unsigned long long* h_chg = nullptr;
+    if (!h_chg) OFSC_CUDA(cudaMallocHost(&h_chg, 3 * 8));
     const bool stats = getenv("OFSC_KMEANS_STATS") != nullptr;   // per-step skip statistics
     const bool noskip = getenv("OFSC_KMEANS_NOSKIP") != nullptr; // A/B: no bound test
-    struct HostFree {
-      void* q;
-      ~HostFree() { cudaFreeHost(q); }
-    } hf{h_chg};
     int it = 0;
     double inertia = 0.0;
     for (it = 1; it <= max_iters; ++it) {
@@ -1546,16 +1544,28 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     OFSC_CUDA(cudaStreamCreateWithFlags(&side.st, cudaStreamNonBlocking));
     OFSC_CUDA(cudaEventCreateWithFlags(&side.a, cudaEventDisableTiming));
     OFSC_CUDA(cudaEventCreateWithFlags(&side.b, cudaEventDisableTiming));
-    OFSC_CUDA(cudaEventRecord(side.b, s));                 // dXf allocated
+    // the edges go first (the build needs them), X0 follows on the side stream
+    // while the graph is built (the run needs it only after the build)
+    DBuf de(m > 0 ? (size_t)m * 2 * sizeof(int64_t) : 0, s);
+    if (m > 0) {
+      OFSC_CUDA(cudaMemcpyAsync(de.p, h_src, (size_t)m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      OFSC_CUDA(cudaMemcpyAsync(de.as<int64_t>() + m, h_dst, (size_t)m * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+    }
+    OFSC_CUDA(cudaEventRecord(side.b, s));                 // dXf allocated, edges uploaded
     OFSC_CUDA(cudaStreamWaitEvent(side.st, side.b, 0));
     OFSC_CUDA(cudaMemcpyAsync(dXf.p, h_X, (size_t)n * k * es, cudaMemcpyHostToDevice, side.st));
     OFSC_CUDA(cudaEventRecord(side.a, side.st));
-    // default: reorder only when the run is long enough to repay the LPA pass
-    // (~0.2 s at 5M nodes vs ~2 ms saved per iteration there)
-    ofsc_build_opts bo{opts->max_iters >= 100 ? 1 : 0, 30};
+    // default: reorder when the run is long enough to repay the LPA pass
+    // (c4: ~60 ms for LPA + second CSR build vs ~3 ms saved per iteration;
+    // profiles/r01/SUMMARY.md, tools/build_probe.py)
+    ofsc_build_opts bo{opts->max_iters >= 32 ? 1 : 0, 30};
     if (bopts) bo = *bopts;
     trace_point("spectral_cluster: start", s);
-    ofsc_status b = ofsc_graph_build_ex(comm, n, m, h_src, h_dst, 0, &bo, stream, &g);
+    ofsc_status b = ofsc_graph_build_ex(comm, n, m, m > 0 ? de.as<int64_t>() : h_src,
+                                        m > 0 ? de.as<int64_t>() + m : h_dst, m > 0 ? 1 : 0, &bo,
+                                        stream, &g);
+    de.release();
     if (b != OFSC_OK) throw Error{b, g_last_error};
     trace_point("spectral_cluster: graph built", s);
     const int64_t nl = g->n_local;

@@ -912,8 +912,7 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
   int* nxt = lb.p;
   const int nb = num_sms() * 8;
   // sweeps until fewer than n/1000 labels change (at least 6, at most `sweeps`)
-  unsigned long long* h_chg = nullptr;
-  OFSC_CUDA(cudaMallocHost(&h_chg, sizeof(unsigned long long)));
+  unsigned long long chg = 0, *h_chg = &chg;   // pageable: no pinned alloc / free (device syncs)
   for (int sw = 0; sw < sweeps; ++sw) {
     OFSC_CUDA(cudaMemsetAsync(ic.p, 0, sizeof(unsigned long long), st));
     for (int colour = 0; colour < 2; ++colour) {
@@ -928,7 +927,6 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
       if (*h_chg * 1000ull < (unsigned long long)n) break;
     }
   }
-  cudaFreeHost(h_chg);
   k_lpa_keys<<<blocks_for(n), 256, 0, st>>>(n, cur, keys.p);
   OFSC_LAUNCH_CHECK();
   size_t tmp_bytes = 0;

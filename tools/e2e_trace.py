@@ -15,10 +15,23 @@ X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
 rows = kmeans_init_rows(cfg.n, cfg.blocks, cfg.seed_km)
 hs, hd = torch.from_numpy(s).pin_memory(), torch.from_numpy(d).pin_memory()
 hx = torch.from_numpy(X0).pin_memory()
+import ctypes as C  # noqa: E402
+L = ofsc.lib()
+h_lab = torch.empty(cfg.n, dtype=torch.int32).pin_memory()
+h_rows = torch.from_numpy(rows).pin_memory()
+o = ofsc.make_opts(cfg.k, cfg.iters)
+stream = torch.cuda.current_stream()
 for rep in range(3):
-    x = hx.clone().pin_memory()
+    x = hx.clone().pin_memory()                  # pinned in/out feature buffer (as bench.py)
+    rpt = ofsc.Report()
     torch.cuda.synchronize()
     t = time.perf_counter()
-    labels, feats, report = ofsc.spectral_cluster(cfg.n, hs.numpy(), hd.numpy(), "ofm_f2", x.numpy(),
-                                                  cfg.blocks, rows, max_iters=cfg.iters)
+    st = L.ofsc_spectral_cluster(None, cfg.n, s.size, C.c_void_p(hs.data_ptr()),
+                                 C.c_void_p(hd.data_ptr()), ofsc.METHODS["ofm_f2"],
+                                 ofsc.DTYPES["f64"], C.byref(o), None, C.c_void_p(x.data_ptr()),
+                                 cfg.blocks, C.c_void_p(h_rows.data_ptr()), 100,
+                                 C.c_void_p(h_lab.data_ptr()), C.byref(rpt),
+                                 C.c_void_p(stream.cuda_stream))
+    torch.cuda.synchronize()
+    ofsc._check(st)
     print(f"call {rep}: {1e3 * (time.perf_counter() - t):.1f} ms", file=sys.stderr, flush=True)
