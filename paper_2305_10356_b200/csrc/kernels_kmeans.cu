@@ -605,29 +605,27 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
     // ---- skip test (8 threads per row; all lanes take the shuffles)
     const bool vrow = rrow < rows;
     bool skip = false;
-    double Da = 0.0, lnew = 0.0, yn;
+    double Da = 0.0, lnew = 0.0;
     {
       const int a = old_lab >= 0 ? old_lab : 0;
-      double sd = 0.0;                             // ||y - c_a||^2 and ||y||^2 (padding
-      yn = 0.0;                                    // columns are zero on both sides)
-#pragma unroll
-      for (int i = 0; i < DP / 8; ++i) {
+      double sd0 = 0.0, sd1 = 0.0;                 // ||y - c_a||^2 (padding columns are
+#pragma unroll                                      // zero on both sides), two chains
+      for (int i = 0; i < DP / 8; i += 2) {
         const int d = rw + 8 * i;
-        const double y = Ys[rrow * LDY + d];
-        const double df = y - Cs[a * DP + d];
-        sd = fma(df, df, sd);
-        yn = fma(y, y, yn);
+        const double df0 = Ys[rrow * LDY + d] - Cs[a * DP + d];
+        const double df1 = Ys[rrow * LDY + d + 8] - Cs[a * DP + d + 8];
+        sd0 = fma(df0, df0, sd0);
+        sd1 = fma(df1, df1, sd1);
       }
+      double sd = sd0 + sd1;
 #pragma unroll
-      for (int o = 1; o <= 4; o <<= 1) {
-        sd += __shfl_xor_sync(0xffffffffu, sd, o);
-        yn += __shfl_xor_sync(0xffffffffu, yn, o);
-      }
+      for (int o = 1; o <= 4; o <<= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
       if (delta && vrow && old_lab >= 0) {
         const double dm = old_lab == s_i1 ? s_m2 : s_m1;
         Da = sd;
         lnew = old_lb - dm - kKmRel * (old_lb + dm);
-        skip = sqrt(Da) * (1.0 + kKmRel) < lnew;
+        // sqrt(Da) (1 + rel) < lnew, compared in squares (Da >= 0)
+        skip = lnew > 0.0 && Da * ((1.0 + kKmRel) * (1.0 + kKmRel)) < lnew * lnew;
       }
       if (rw == 0) fl[rrow] = (vrow && !skip) ? 1 : 0;
       if (rw == 0 && skip) ++nskip;
@@ -682,8 +680,12 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
         const int sl = __popc(fmask & ((1u << r) - 1u));   // compact slot of row r
         double x1 = blk ? mb1[sl * 8 + w] : CUDART_INF, x2 = blk ? mb2[sl * 8 + w] : CUDART_INF;
         int xc = blk ? mc1[sl * 8 + w] : 0;
+        double yn = 0.0;                           // ||y||^2: 8 partial sums, butterfly
+#pragma unroll
+        for (int i = 0; i < DP / 8; ++i) yn = fma(Ys[r * LDY + w + 8 * i], Ys[r * LDY + w + 8 * i], yn);
 #pragma unroll
         for (int o = 1; o <= 4; o <<= 1) {
+          yn += __shfl_xor_sync(0xffffffffu, yn, o);
           const double ob1 = __shfl_xor_sync(0xffffffffu, x1, o);
           const double ob2 = __shfl_xor_sync(0xffffffffu, x2, o);
           const int oc1 = __shfl_xor_sync(0xffffffffu, xc, o);
