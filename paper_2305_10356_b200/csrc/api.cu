@@ -59,9 +59,7 @@ struct DBuf {
   T* as() const { return (T*)p; }
 };
 
-static void dfree(void* p) {
-  if (p) cudaFree(p);
-}
+static void dfree(void* p) { dev_free(p); }
 
 static ncclDataType_t nccl_type(ofsc_dtype dt) { return dt == OFSC_F64 ? ncclFloat64 : ncclFloat32; }
 
@@ -83,6 +81,7 @@ struct Workspace {
   cudaGraphExec_t e_iter = nullptr, e_refresh = nullptr, e_loop = nullptr;
   cudaStream_t cap = nullptr;  // private stream used only for graph capture
   void release() {
+    if (have) cudaDeviceSynchronize();   // pool frees below: no queued user left
     if (cap) cudaStreamDestroy(cap);
     cap = nullptr;
     if (comm_st) cudaStreamDestroy(comm_st);
@@ -259,6 +258,7 @@ ofsc_status ofsc_comm_create_local(int nranks, int rank, ofsc_comm* out) {
 }
 
 static void graph_free(ofsc_graph g) {
+  cudaDeviceSynchronize();   // nothing queued may still use the buffers (pool frees follow)
   g->ws.release();
   dfree(g->d_begins);
   dfree(g->row_ptr);
@@ -331,8 +331,8 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
         build_csr(n, m, psrc, pdst, csr, s);
         if (reorder) {
           // locality reordering derived from the graph: communities -> contiguous rows
-          OFSC_CUDA(cudaMalloc(&g->perm, n * sizeof(int32_t)));
-          OFSC_CUDA(cudaMalloc(&g->cid, n * sizeof(int32_t)));
+          dev_alloc((void**)&g->perm, n * sizeof(int32_t), s);
+          dev_alloc((void**)&g->cid, n * sizeof(int32_t), s);
           DBuf inv(n * sizeof(int32_t), s);
           lpa_order(csr, sweeps, g->perm, inv.as<int32_t>(), &n_comm, &intra, g->cid, &g->cstart, s);
           DBuf s2(m * sizeof(int64_t), s), d2(m * sizeof(int64_t), s);
@@ -379,13 +379,13 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       g->row_ptr = csr.row_ptr;
       g->col = csr.col;
       g->s_slot = csr.s;
-      OFSC_CUDA(cudaMalloc(&g->s32_slot, n * sizeof(float)));
-      OFSC_CUDA(cudaMalloc(&g->d_begins, 2 * sizeof(int64_t)));
+      dev_alloc((void**)&g->s32_slot, n * sizeof(float), s);
+      dev_alloc((void**)&g->d_begins, 2 * sizeof(int64_t), s);
       OFSC_CUDA(cudaMemcpyAsync(g->d_begins, g->begins.data(), 2 * sizeof(int64_t),
                                 cudaMemcpyHostToDevice, s));
       scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, 1, n, s);
     } else {
-      OFSC_CUDA(cudaMalloc(&g->d_begins, (p + 1) * sizeof(int64_t)));
+      dev_alloc((void**)&g->d_begins, (p + 1) * sizeof(int64_t), s);
       OFSC_CUDA(cudaMemcpyAsync(g->d_begins, g->begins.data(), (p + 1) * sizeof(int64_t),
                                 cudaMemcpyHostToDevice, s));
       HaloLayout hl;
@@ -754,27 +754,27 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   const size_t es = esize(dt);
   const int64_t nl = std::max<int64_t>(g->n_local, 1);
   const size_t blk = (size_t)nl * KP * es;
-  OFSC_CUDA(cudaMalloc(&w.X, blk));
-  OFSC_CUDA(cudaMalloc(&w.AX, blk));
-  OFSC_CUDA(cudaMalloc(&w.G, blk));
-  OFSC_CUDA(cudaMalloc(&w.AV, blk));
+  dev_alloc((void**)&w.X, blk, s);
+  dev_alloc((void**)&w.AX, blk, s);
+  dev_alloc((void**)&w.G, blk, s);
+  dev_alloc((void**)&w.AV, blk, s);
   const size_t vg = g->p == 1 ? blk : (size_t)g->ext_rows * KP * es;
-  OFSC_CUDA(cudaMalloc(&w.Vg, vg));
+  dev_alloc((void**)&w.Vg, vg, s);
   if (g->p > 1) {
-    OFSC_CUDA(cudaMalloc(&w.sendbuf, (size_t)std::max<int64_t>(g->total_send, 1) * KP * es));
+    dev_alloc((void**)&w.sendbuf, (size_t)std::max<int64_t>(g->total_send, 1) * KP * es, s);
     OFSC_CUDA(cudaStreamCreateWithFlags(&w.comm_st, cudaStreamNonBlocking));
     OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_v, cudaEventDisableTiming));
     OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_x, cudaEventDisableTiming));
   }
   const int nbmax = num_sms() * 4;   // grids of the streaming kernels are chosen per run
   w.nb2 = gram_stream_grid(dt, KP, nl);
-  OFSC_CUDA(cudaMalloc(&w.part_cols, (size_t)nbmax * 2 * KP * 8));
-  OFSC_CUDA(cudaMalloc(&w.part_g4, (size_t)nbmax * 2 * KP * KP * 8));
-  OFSC_CUDA(cudaMalloc(&w.part_g2, (size_t)w.nb2 * 2 * KP * KP * 8));
-  OFSC_CUDA(cudaMalloc(&w.grams, (size_t)4 * KP * KP * 8));
-  OFSC_CUDA(cudaMalloc(&w.state, (size_t)(2 * KP * KP + 5 * KP) * 8));
-  OFSC_CUDA(cudaMalloc(&w.ctl, sizeof(DevCtl)));
-  OFSC_CUDA(cudaMalloc(&w.ctr, 4 * sizeof(unsigned long long)));  // one per SpMM column pass
+  dev_alloc((void**)&w.part_cols, (size_t)nbmax * 2 * KP * 8, s);
+  dev_alloc((void**)&w.part_g4, (size_t)nbmax * 2 * KP * KP * 8, s);
+  dev_alloc((void**)&w.part_g2, (size_t)w.nb2 * 2 * KP * KP * 8, s);
+  dev_alloc((void**)&w.grams, (size_t)4 * KP * KP * 8, s);
+  dev_alloc((void**)&w.state, (size_t)(2 * KP * KP + 5 * KP) * 8, s);
+  dev_alloc((void**)&w.ctl, sizeof(DevCtl), s);
+  dev_alloc((void**)&w.ctr, 4 * sizeof(unsigned long long), s);  // one per SpMM column pass
   w.dt = dt;
   w.KP = KP;
   w.have = true;
@@ -874,7 +874,7 @@ static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaSt
   const size_t es = esize(dt);
   const void* Zg = w.X;
   if (g->p > 1) {
-    if (!w.Xg) OFSC_CUDA(cudaMalloc(&w.Xg, (size_t)g->ext_rows * p.KP * es));
+    if (!w.Xg) dev_alloc((void**)&w.Xg, (size_t)g->ext_rows * p.KP * es, s);
     pr.ph(OFSC_PH_COMM, 0, [&] {
       OFSC_CUDA(cudaMemcpyAsync(w.Xg, w.X, (size_t)g->n_local * p.KP * es,
                                 cudaMemcpyDeviceToDevice, s));
@@ -1306,6 +1306,16 @@ ofsc_status ofsc_row_normalize(ofsc_dtype dt, int64_t n_local, int32_t k, const 
   });
 }
 
+namespace ofsc {
+// K-means step counters (changes, skipped, product blocks) and inertia -> mapped host memory
+__global__ void k_publish_counters(const unsigned long long* chg, const double* tot,
+                                   unsigned long long* h) {
+  if (threadIdx.x < 3) ((volatile unsigned long long*)h)[threadIdx.x] = chg[threadIdx.x];
+  if (threadIdx.x == 3) ((volatile unsigned long long*)h)[3] = __double_as_longlong(*tot);
+  __threadfence_system();
+}
+}  // namespace ofsc
+
 ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t dim,
                         const void* d_Y, int64_t ldy, int32_t n_clusters, double* d_centroids,
                         int32_t max_iters, int32_t* d_labels, int32_t* iters_out,
@@ -1330,8 +1340,15 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
     OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
     // pinned counter readback, allocated once per host thread (cudaFreeHost would
     // synchronise the whole device, e.g. the feature download of spectral_cluster)
+    // published by a kernel into mapped host memory: no copy-engine transfer, so the
+    // per-step readback never queues behind a large download (spectral_cluster's
+    // features overlap K-means on a side stream)
     static thread_local unsigned long long* h_chg = nullptr;
-    if (!h_chg) OFSC_CUDA(cudaMallocHost(&h_chg, 3 * 8));
+    static thread_local unsigned long long* d_hchg = nullptr;
+    if (!h_chg) {
+      OFSC_CUDA(cudaHostAlloc((void**)&h_chg, 4 * 8, cudaHostAllocMapped));
+      OFSC_CUDA(cudaHostGetDevicePointer((void**)&d_hchg, h_chg, 0));
+    }
     const bool stats = getenv("OFSC_KMEANS_STATS") != nullptr;   // per-step skip statistics
     const bool noskip = getenv("OFSC_KMEANS_NOSKIP") != nullptr; // A/B: no bound test
     int it = 0;
@@ -1358,8 +1375,8 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
         OFSC_NCCL(ncclAllReduce(chg.p, chg.p, 1, ncclUint64, ncclSum, comm->nccl, s));
         OFSC_NCCL(ncclAllReduce(tot.p, tot.p, 1, ncclFloat64, ncclSum, comm->nccl, s));
       }
-      OFSC_CUDA(cudaMemcpyAsync(h_chg, chg.p, 3 * 8, cudaMemcpyDeviceToHost, s));
-      OFSC_CUDA(cudaMemcpyAsync(&inertia, tot.p, 8, cudaMemcpyDeviceToHost, s));
+      k_publish_counters<<<1, 32, 0, s>>>(chg.as<unsigned long long>(), tot.as<double>(), d_hchg);
+      OFSC_LAUNCH_CHECK();
       OFSC_CUDA(cudaStreamSynchronize(s));
       if (stats) {
         float ms = 0.f;
@@ -1369,7 +1386,12 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
         fprintf(stderr, "[ofsc kmeans] step %d changes %llu skipped %llu product_blocks %llu ms %.3f\n",
                 it, h_chg[0], h_chg[1], h_chg[2], ms);
       }
-      if (it > 1 && *h_chg == 0) break;
+      {
+        double v;
+        memcpy(&v, (const void*)&((volatile unsigned long long*)h_chg)[3], 8);
+        inertia = v;
+      }
+      if (it > 1 && ((volatile unsigned long long*)h_chg)[0] == 0) break;
       if (n_local > 0 && !fused)
         launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nbp, s);
       else if (n_local == 0)
@@ -1524,6 +1546,7 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     OFSC_REQUIRE(opts && h_X && h_init_rows && h_labels && n_clusters >= 1 && opts->k >= 1,
                  OFSC_ERR_ARG, "bad spectral_cluster args");
     cudaStream_t s = (cudaStream_t)stream;
+    trace_point("spectral_cluster: enter", s);
     // copies overlap compute on a side stream: X0 upload || graph build,
     // feature download || normalise + K-means (pinned host buffers make them async)
     // (declared after dXf: destroyed first, so the side stream is drained before
@@ -1634,10 +1657,13 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
       for (int64_t i = 0; i < n; ++i)
         if (tmp[i] >= 0) h_labels[i] = tmp[i];
     }
+    trace_point("spectral_cluster: labels queued", s);
     OFSC_CUDA(cudaStreamSynchronize(side.st));
+    trace_point("spectral_cluster: features downloaded", s);
     OFSC_CUDA(cudaStreamSynchronize(s));
   });
   if (g) ofsc_graph_destroy(g);
+  trace_point("spectral_cluster: end", (cudaStream_t)stream);
   if (st == OFSC_OK && run_st == OFSC_ERR_DIVERGED) return OFSC_ERR_DIVERGED;
   return st;
 }

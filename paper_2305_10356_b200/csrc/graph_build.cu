@@ -439,8 +439,8 @@ void append_csr(CsrDevice& csr, int64_t m, const int64_t* d_src, const int64_t* 
     OFSC_LAUNCH_CHECK();
     OFSC_CUDA(cudaStreamSynchronize(st));
   }
-  cudaFree(csr.row_ptr);
-  cudaFree(csr.col);
+  dev_free(csr.row_ptr);   // stream synchronised above
+  dev_free(csr.col);
   csr.row_ptr = new_ptr;
   csr.col = new_col;
   csr.nnz = nnz_new;
@@ -639,12 +639,12 @@ void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_
   for (int64_t i = 0; i < nl; ++i) out.h_gid[i] = (int32_t)(rb + i);
   if (h > 0)
     OFSC_CUDA(cudaMemcpy(out.h_gid.data() + nl, halo.p, h * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  OFSC_CUDA(cudaMalloc(&out.d_gid, std::max<int64_t>(out.ext_rows, 1) * sizeof(int32_t)));
+  dev_alloc((void**)&out.d_gid, std::max<int64_t>(out.ext_rows, 1) * sizeof(int32_t), st);
   OFSC_CUDA(cudaMemcpy(out.d_gid, out.h_gid.data(), out.ext_rows * sizeof(int32_t),
                        cudaMemcpyHostToDevice));
   // 2. local CSR: rebased row pointers, columns -> ext ids; s on the ext rows
-  OFSC_CUDA(cudaMalloc(&out.row_ptr, (nl + 1) * sizeof(int64_t)));
-  OFSC_CUDA(cudaMalloc(&out.col, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+  dev_alloc((void**)&out.row_ptr, (nl + 1) * sizeof(int64_t), st);
+  dev_alloc((void**)&out.col, std::max<int64_t>(nnz, 1) * sizeof(int32_t), st);
   rebase_row_ptr(csr.row_ptr + rb, nl, e0, out.row_ptr, st);
   if (nnz > 0) {
     k_remap_ext<<<blocks_for(nnz), 256, 0, st>>>(nnz, gcol, rb, re, nl, halo.p, h, out.col);
@@ -655,10 +655,10 @@ void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_
   //     the local part runs while the halo is exchanged
   {
     DevBuf<int64_t> cnt(std::max<int64_t>(nl, 1), st);
-    OFSC_CUDA(cudaMalloc(&out.row_ptr_loc, (nl + 1) * sizeof(int64_t)));
-    OFSC_CUDA(cudaMalloc(&out.row_ptr_rem, (nl + 1) * sizeof(int64_t)));
-    OFSC_CUDA(cudaMalloc(&out.col_loc, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
-    OFSC_CUDA(cudaMalloc(&out.col_rem, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+    dev_alloc((void**)&out.row_ptr_loc, (nl + 1) * sizeof(int64_t), st);
+    dev_alloc((void**)&out.row_ptr_rem, (nl + 1) * sizeof(int64_t), st);
+    dev_alloc((void**)&out.col_loc, std::max<int64_t>(nnz, 1) * sizeof(int32_t), st);
+    dev_alloc((void**)&out.col_rem, std::max<int64_t>(nnz, 1) * sizeof(int32_t), st);
     OFSC_CUDA(cudaMemsetAsync(out.row_ptr_loc, 0, (nl + 1) * sizeof(int64_t), st));
     if (nl > 0) {
       k_local_count<<<blocks_for(nl), 256, 0, st>>>(nl, out.row_ptr, out.col, cnt.p);
@@ -676,8 +676,8 @@ void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_
       OFSC_CUDA(cudaMemsetAsync(out.row_ptr_rem, 0, sizeof(int64_t), st));
     }
   }
-  OFSC_CUDA(cudaMalloc(&out.s_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(double)));
-  OFSC_CUDA(cudaMalloc(&out.s32_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(float)));
+  dev_alloc((void**)&out.s_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(double), st);
+  dev_alloc((void**)&out.s32_ext, std::max<int64_t>(out.ext_rows, 1) * sizeof(float), st);
   k_gather_s<<<blocks_for(std::max<int64_t>(out.ext_rows, 1)), 256, 0, st>>>(
       out.ext_rows, out.d_gid, csr.s, out.s_ext, out.s32_ext);
   OFSC_LAUNCH_CHECK();
@@ -730,7 +730,7 @@ void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_
     }
   }
   out.total_send = (int64_t)send_idx.size();
-  OFSC_CUDA(cudaMalloc(&out.d_send_idx, std::max<int64_t>(out.total_send, 1) * sizeof(int32_t)));
+  dev_alloc((void**)&out.d_send_idx, std::max<int64_t>(out.total_send, 1) * sizeof(int32_t), st);
   if (out.total_send > 0)
     OFSC_CUDA(cudaMemcpy(out.d_send_idx, send_idx.data(), out.total_send * sizeof(int32_t),
                          cudaMemcpyHostToDevice));
@@ -955,7 +955,7 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
   OFSC_CUDA(cudaStreamSynchronize(st));
   *n_comm = h_cnt;
   *intra_frac = csr.nnz > 0 ? (double)h_ic / (double)csr.nnz : 1.0;
-  OFSC_CUDA(cudaMalloc(d_cstart, (h_cnt + 1) * sizeof(int64_t)));
+  dev_alloc((void**)d_cstart, (h_cnt + 1) * sizeof(int64_t), st);
   k_comm_index<<<blocks_for(n), 256, 0, st>>>(n, flag.p, scan.p, d_cid, *d_cstart);
   OFSC_LAUNCH_CHECK();
   OFSC_CUDA(cudaMemcpyAsync(*d_cstart + h_cnt, &n, sizeof(int64_t), cudaMemcpyHostToDevice, st));

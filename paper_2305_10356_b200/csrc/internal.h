@@ -93,6 +93,12 @@ struct IterParams {
 int grid_rows(int64_t n_rows, int blocks_per_sm);
 int num_sms();
 void keep_pool();    // default mempool keeps freed scratch (no per-build re-mapping)
+// Every long-lived device buffer comes from the device's stream-ordered pool (kept
+// mapped by keep_pool): freeing a multi-GB workspace then costs no unmapping and no
+// device-wide synchronisation.  dev_free releases on the legacy stream: callers
+// guarantee that no queued work still uses the buffer.
+void dev_alloc(void** p, size_t bytes, cudaStream_t st);
+void dev_free(void* p);
 void trace_point(const char* what, cudaStream_t st);   // OFSC_TRACE=1: phase timestamps
 
 // grid sizes of the TMA-pipelined streaming kernels (<= 4 * #SMs)

@@ -10,6 +10,8 @@
 #include "sm100.cuh"
 
 #include <chrono>
+#include <cstring>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
@@ -28,18 +30,45 @@ int num_sms() {
   return n;
 }
 
-// OFSC_TRACE=1: host-side phase timestamps of the graph build to stderr.
+// OFSC_TRACE=1: host-side phase timestamps (stream synchronised at each point)
+// to stderr.  OFSC_TRACE=2: no synchronisation; each point records the host
+// time and a CUDA event on `st`, and a point named "...: end" prints the list
+// (host ms and device ms since the first point of the list).
 void trace_point(const char* what, cudaStream_t st) {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("OFSC_TRACE");
-    on = (e && e[0] == '1') ? 1 : 0;
+    on = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
   }
   if (!on) return;
   static std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  cudaStreamSynchronize(st);
-  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  fprintf(stderr, "[ofsc trace] %10.2f ms  %s\n", ms, what);
+  if (on == 1) {
+    cudaStreamSynchronize(st);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[ofsc trace] %10.2f ms  %s\n", ms, what);
+    return;
+  }
+  struct Pt {
+    const char* what;
+    double host_ms;
+    cudaEvent_t ev;
+  };
+  static std::vector<Pt> pts;
+  cudaEvent_t ev;
+  cudaEventCreate(&ev);
+  cudaEventRecord(ev, st);
+  pts.push_back({what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), ev});
+  const size_t L = strlen(what);
+  if (L >= 5 && strcmp(what + L - 5, ": end") == 0) {
+    cudaEventSynchronize(ev);
+    for (auto& p : pts) {
+      float d = 0.f;
+      cudaEventElapsedTime(&d, pts[0].ev, p.ev);
+      fprintf(stderr, "[ofsc trace2] host %9.2f  device %9.2f ms  %s\n", p.host_ms - pts[0].host_ms, d, p.what);
+    }
+    for (auto& p : pts) cudaEventDestroy(p.ev);
+    pts.clear();
+  }
 }
 
 // The graph build allocates its sort / scan scratch from the device's default
@@ -56,6 +85,15 @@ void keep_pool() {
   uint64_t thr = ~0ull;
   OFSC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   if (dev < 64) done |= 1ull << dev;
+}
+
+void dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+  keep_pool();
+  OFSC_CUDA(cudaMallocAsync(p, bytes, st));
+}
+
+void dev_free(void* p) {
+  if (p) cudaFreeAsync(p, 0);
 }
 
 int grid_rows(int64_t n_rows, int blocks_per_sm) {

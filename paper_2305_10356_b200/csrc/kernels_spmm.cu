@@ -369,8 +369,9 @@ __global__ void k_row_bounds(int64_t nh, const int32_t* rows, const int64_t* row
 }
 
 void HeavyRows::release() {
+  if (rows) cudaDeviceSynchronize();   // pool frees below: no queued user left
   for (void* q : {(void*)rows, (void*)chunk_first, (void*)chunk_beg, (void*)chunk_end, scratch})
-    if (q) cudaFree(q);
+    dev_free(q);
   rows = nullptr;
   chunk_first = nullptr;
   chunk_beg = chunk_end = nullptr;
@@ -430,11 +431,11 @@ void build_heavy(const int64_t* d_row_ptr, int64_t n_rows, HeavyRows& out, cudaS
     out.thresh = thresh;
     out.n_rows = nh;
     out.n_chunks = (int64_t)cb.size();
-    OFSC_CUDA(cudaMalloc(&out.rows, nh * sizeof(int32_t)));
-    OFSC_CUDA(cudaMalloc(&out.chunk_first, (nh + 1) * sizeof(int32_t)));
-    OFSC_CUDA(cudaMalloc(&out.chunk_beg, out.n_chunks * sizeof(int64_t)));
-    OFSC_CUDA(cudaMalloc(&out.chunk_end, out.n_chunks * sizeof(int64_t)));
-    OFSC_CUDA(cudaMalloc(&out.scratch, out.n_chunks * 64 * sizeof(double)));
+    dev_alloc((void**)&out.rows, nh * sizeof(int32_t), st);
+    dev_alloc((void**)&out.chunk_first, (nh + 1) * sizeof(int32_t), st);
+    dev_alloc((void**)&out.chunk_beg, out.n_chunks * sizeof(int64_t), st);
+    dev_alloc((void**)&out.chunk_end, out.n_chunks * sizeof(int64_t), st);
+    dev_alloc((void**)&out.scratch, out.n_chunks * 64 * sizeof(double), st);
     OFSC_CUDA(cudaMemcpy(out.rows, rows.data(), nh * sizeof(int32_t), cudaMemcpyHostToDevice));
     OFSC_CUDA(cudaMemcpy(out.chunk_first, first.data(), (nh + 1) * sizeof(int32_t),
                          cudaMemcpyHostToDevice));
@@ -461,16 +462,17 @@ __global__ void k_gather_sval(int64_t nnz, const int32_t* col, const double* s, 
 
 void build_sval(int64_t nnz, const int32_t* col, const double* s, const float* s32, double** sval,
                 float** sval32, cudaStream_t st) {
-  if (*sval) cudaFree(*sval);
-  if (*sval32) cudaFree(*sval32);
+  if (*sval || *sval32) cudaDeviceSynchronize();   // pool frees below: no queued user left
+  dev_free(*sval);
+  dev_free(*sval32);
   *sval = nullptr;
   *sval32 = nullptr;
   // auto: graphs whose gathers mostly miss L2 (measured c4: SpMM 5.6 -> 5.3 ms; on
   // L2-resident c3 the extra stream costs 3 %): OFSC_SPMM_SVAL=1 forces it, 0 disables
   const int mode = env_int("OFSC_SPMM_SVAL", -1);
   if (nnz <= 0 || mode == 0 || (mode < 0 && nnz < 20000000)) return;
-  OFSC_CUDA(cudaMalloc(sval, nnz * sizeof(double)));
-  OFSC_CUDA(cudaMalloc(sval32, nnz * sizeof(float)));
+  dev_alloc((void**)sval, nnz * sizeof(double), st);
+  dev_alloc((void**)sval32, nnz * sizeof(float), st);
   k_gather_sval<<<num_sms() * 16, 256, 0, st>>>(nnz, col, s, s32, *sval, *sval32);
   OFSC_LAUNCH_CHECK();
 }

@@ -21,7 +21,7 @@ h_lab = torch.empty(cfg.n, dtype=torch.int32).pin_memory()
 h_rows = torch.from_numpy(rows).pin_memory()
 o = ofsc.make_opts(cfg.k, cfg.iters)
 stream = torch.cuda.current_stream()
-for rep in range(3):
+for rep in range(int(os.environ.get("E2E_REPS", "3"))):
     x = hx.clone().pin_memory()                  # pinned in/out feature buffer (as bench.py)
     rpt = ofsc.Report()
     torch.cuda.synchronize()
