@@ -162,3 +162,50 @@ def test_algorithm1_reorder_equivalent():
     l0, _, _ = ofsc.spectral_cluster(cfg.n, s, d, "ofm_f2", X0, cfg.blocks, rows, max_iters=200,
                                      reorder=False)
     assert ari(l1, l0) >= 0.97
+
+
+def _blobs(n, dim, K, seed, spread=0.15):
+    rng = np.random.default_rng(seed)
+    centres = row_normalize(rng.standard_normal((K, dim)))
+    lab = rng.integers(0, K, n)
+    return row_normalize(centres[lab] + spread * rng.standard_normal((n, dim))), lab
+
+
+@pytest.mark.parametrize("n,dim,K", [(20011, 16, 10), (30001, 64, 64), (9001, 48, 100)])
+def test_kmeans_bound_pruning_exact(n, dim, K, capfd, monkeypatch):
+    """Steps >= 2 skip the products for rows whose lower bound proves the label
+    (R28): labels, step count and centroids equal the oracle's Lloyd
+    run and the unpruned kernel's; the statistics show rows were skipped."""
+    Y, _ = _blobs(n, dim, K, n + K)
+    rng = np.random.default_rng(7)
+    C0 = Y[rng.choice(n, K, replace=False)].copy()
+    lo, Co, ito, ino = kmeans_lloyd(Y, C0, max_iters=40)
+    Yd = torch.from_numpy(Y).cuda()
+    monkeypatch.setenv("OFSC_KMEANS_STATS", "1")
+    C = torch.from_numpy(C0.copy()).cuda()
+    lg, itg, ing = ofsc.kmeans(Yd, C, max_iters=40)
+    err = capfd.readouterr().err
+    skipped = [int(l.split("skipped")[1].split()[0]) for l in err.splitlines() if "[ofsc kmeans]" in l]
+    monkeypatch.delenv("OFSC_KMEANS_STATS")
+    assert len(skipped) == itg and skipped[0] == 0 and max(skipped) > n // 2
+    assert np.array_equal(lg.cpu().numpy(), lo) and itg == ito
+    assert np.allclose(C.cpu().numpy(), Co, atol=1e-13, rtol=0)
+    assert abs(ing - ino) <= 1e-12 * ino
+    monkeypatch.setenv("OFSC_KMEANS_NOSKIP", "1")
+    C2 = torch.from_numpy(C0.copy()).cuda()
+    l2, it2, in2 = ofsc.kmeans(Yd, C2, max_iters=40)
+    assert torch.equal(l2, lg) and it2 == itg
+    assert torch.equal(C2, C)                     # same labels -> bit-identical sums
+    assert abs(in2 - ing) <= 1e-12 * ing
+
+
+def test_kmeans_pruning_single_cluster_and_duplicates():
+    """K = 1 (no other centroid: infinite lower bound) and duplicated centroids
+    (exact ties every step: never skipped, lowest index)."""
+    Y, _ = _blobs(5003, 8, 3, 1)
+    for C0 in (Y[:1].copy(), np.concatenate([Y[:3], Y[:3]])):
+        lo, Co, ito, _ = kmeans_lloyd(Y, C0, max_iters=15)
+        C = torch.from_numpy(C0.copy()).cuda()
+        lg, itg, _ = ofsc.kmeans(torch.from_numpy(Y).cuda(), C, max_iters=15)
+        assert np.array_equal(lg.cpu().numpy(), lo) and itg == ito
+        assert np.allclose(C.cpu().numpy(), Co, atol=1e-13, rtol=0)
