@@ -19,6 +19,10 @@ __device__ __forceinline__ double rndT(double v) { return (double)(T)v; }
 
 constexpr int kSTR = 16;   // rows per streamed tile
 constexpr int kSST = 3;    // pipeline stages
+// warp-specialised Gram kernels (C4, C2b)
+constexpr int kGWS_NS = 3;          // TMA stages
+constexpr int kGWS_NP = 2;          // padded tiles
+constexpr int kGWS_THREADS = 384;   // 8 consumer + 4 producer warps
 
 template <typename T, int KP>
 struct StreamTile {
@@ -373,18 +377,168 @@ static void launch_c4(const IterParams& p, int nblk, cudaStream_t s) {
   OFSC_LAUNCH_CHECK();
 }
 
+// C4, warp-specialised (KP = 48 by default, see c4_ws):
+// warps 8-11 (producers) wait for each TMA stage (G, Vp, X), form
+// V = -G + beta Vp in place (the stage is then stored back as V by one bulk
+// copy) and into a padded fp64 tile together with X, and hand the tile over on
+// an mbarrier; warps 0-7 run the DMMA Grams Q = V^T V (upper blocks) and
+// P = V^T X on it.  Same products and summation order as k_direction_gram.
+template <typename T, int KP>
+struct C4SmemWS {
+  static constexpr int LD = KP + 4;
+  static constexpr size_t pad = (size_t)kSTR * LD * 8;
+  static constexpr size_t arr = (size_t)kSTR * KP * sizeof(T);
+  static constexpr size_t stage = 3 * arr;                            // G, Vp (-> V), X
+  static constexpr size_t bytes =
+      kGWS_NP * 2 * pad + kGWS_NS * stage + KP * 8 + (kGWS_NS + 2 * kGWS_NP) * 8;
+};
+
+template <typename T, int KP>
+__global__ void __launch_bounds__(kGWS_THREADS, 1) k_direction_gram_ws(IterParams p) {
+  using S = C4SmemWS<T, KP>;
+  constexpr int LD = S::LD;
+  if (p.ctl->stop) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* pads = (double*)smraw;                                       // [NP][2][kSTR][LD]
+  unsigned char* stg = smraw + kGWS_NP * 2 * S::pad;
+  double* s_beta = (double*)(stg + kGWS_NS * S::stage);
+  uint64_t* full = (uint64_t*)(s_beta + KP);
+  uint64_t* pfull = full + kGWS_NS;
+  uint64_t* pempty = pfull + kGWS_NP;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (p.n_local + kSTR - 1) / kSTR;
+  const T* gG = (const T*)p.G;
+  T* gV = (T*)p.V;
+  const T* gX = (const T*)p.X;
+  auto arr = [&](int st, int a) { return (T*)(stg + st * S::stage + a * S::arr); };  // 0 G, 1 V, 2 X
+  auto pad = [&](int pb, int a) { return pads + ((size_t)pb * 2 + a) * kSTR * LD; };
+  auto issue = [&](int st, int64_t tile) {
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, p.n_local - row0);
+    const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+    mbar_arrive_expect_tx(&full[st], 3u * b);
+    bulk_g2s(arr(st, 0), gG + row0 * KP, b, &full[st]);
+    bulk_g2s(arr(st, 1), gV + row0 * KP, b, &full[st]);
+    bulk_g2s(arr(st, 2), gX + row0 * KP, b, &full[st]);
+  };
+  if (tid == 0) {
+    for (int s0 = 0; s0 < kGWS_NS; ++s0) mbar_init(&full[s0], 1);
+    for (int s0 = 0; s0 < kGWS_NP; ++s0) {
+      mbar_init(&pfull[s0], 1);
+      mbar_init(&pempty[s0], 8);                 // one arrival per consumer warp
+    }
+    fence_barrier_init();
+  }
+  if (tid < KP) s_beta[tid] = p.beta[tid];
+  __syncthreads();
+  if (warp >= 8) {
+    // ---- producers: V = -G + beta Vp (stage, in place, and padded), X padded
+    const int ptid = tid - 256;
+    if (ptid == 0)
+      for (int s0 = 0; s0 < kGWS_NS; ++s0) {
+        const int64_t tile = blockIdx.x + (int64_t)s0 * gridDim.x;
+        if (tile < ntiles) issue(s0, tile);
+      }
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = it % kGWS_NS, pb = it % kGWS_NP;
+      const int64_t row0 = tile * kSTR;
+      const int rows = (int)imin64(kSTR, p.n_local - row0);
+      mbar_wait(&full[st], (uint32_t)((it / kGWS_NS) & 1));
+      if (it >= kGWS_NP) mbar_wait(&pempty[pb], (uint32_t)(((it / kGWS_NP) - 1) & 1));
+      double* Vd = pad(pb, 0);
+      double* Xd = pad(pb, 1);
+      const T* sG = arr(st, 0);
+      T* sV = arr(st, 1);
+      const T* sX = arr(st, 2);
+      for (int e = ptid; e < kSTR * KP; e += 128) {
+        const int r = e / KP, c = e % KP;
+        double v = 0.0, x = 0.0;
+        if (r < rows) {
+          v = rndT<T>(-(double)sG[e] + s_beta[c] * (double)sV[e]);
+          x = (double)sX[e];
+          sV[e] = (T)v;
+        }
+        Vd[r * LD + c] = v;
+        Xd[r * LD + c] = x;
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);                  // stage st transformed, tile pb written
+      if (ptid == 0) {
+        mbar_arrive(&pfull[pb]);
+        bulk_s2g(gV + row0 * KP, sV, (uint32_t)rows * KP * sizeof(T));
+        bulk_commit();
+        const int64_t nxt = tile + (int64_t)kGWS_NS * gridDim.x;
+        if (nxt < ntiles) {
+          bulk_wait_read_all();                  // the V store has read stage st
+          issue(st, nxt);
+        }
+      }
+    }
+    if (ptid == 0) bulk_wait_all();
+  } else {
+    // ---- consumers: Q = V^T V (upper blocks), P = V^T X on DMMA
+    typename GramSel<KP>::type acc;
+    acc.zero();
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int pb = it % kGWS_NP;
+      const int rows = (int)imin64(kSTR, p.n_local - tile * kSTR);
+      mbar_wait(&pfull[pb], (uint32_t)((it / kGWS_NP) & 1));
+      const double* Vd = pad(pb, 0);
+      const double* Xd = pad(pb, 1);
+      acc.accumulate(Vd, Vd, Vd, Xd, (rows + 3) & ~3, warp, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pempty[pb]);
+    }
+    acc.store(p.part_g4 + (int64_t)blockIdx.x * 2 * KP * KP, warp, lane);
+  }
+}
+
+// warp-specialised C4 where it measured faster: KP = 48 (c5: 0.526 -> 0.453 ms);
+// at KP = 64 the one 384-thread CTA per SM hides less DMMA latency than two
+// staging-copy CTAs (c4 2.40 -> 2.75, c6 0.479 -> 0.556 ms), KP = 32 neutral-worse.
+// OFSC_C4_WS=0/1 forces either kernel.
+static int c4_ws(int KP) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("OFSC_C4_WS");
+    v = (e && *e) ? atoi(e) : -1;
+  }
+  return v >= 0 ? v : (KP == 48 ? 1 : 0);
+}
+
+template <typename T, int KP>
+static void launch_c4_ws(const IterParams& p, int nblk, cudaStream_t s) {
+  const size_t smem = C4SmemWS<T, KP>::bytes;
+  auto kern = k_direction_gram_ws<T, KP>;
+  static bool set = false;
+  if (!set) {
+    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = true;
+  }
+  kern<<<nblk, kGWS_THREADS, smem, s>>>(p);
+  OFSC_LAUNCH_CHECK();
+}
+
 int c4_grid(ofsc_dtype dt, int KP, int64_t n) {
   size_t b = 0;
   OFSC_DISPATCH_KP(KP, {
-    b = dt == OFSC_F64 ? C4Smem<double, KPC>::bytes : C4Smem<float, KPC>::bytes;
+    if (c4_ws(KPC)) b = dt == OFSC_F64 ? C4SmemWS<double, KPC>::bytes : C4SmemWS<float, KPC>::bytes;
+    else b = dt == OFSC_F64 ? C4Smem<double, KPC>::bytes : C4Smem<float, KPC>::bytes;
   });
   return stream_grid(n, b);
 }
 
 void launch_direction_gram(ofsc_dtype dt, const IterParams& p, int nblk, cudaStream_t s) {
   OFSC_DISPATCH_KP(p.KP, {
-    if (dt == OFSC_F64) launch_c4<double, KPC>(p, nblk, s);
-    else launch_c4<float, KPC>(p, nblk, s);
+    if (c4_ws(KPC)) {
+      if (dt == OFSC_F64) launch_c4_ws<double, KPC>(p, nblk, s);
+      else launch_c4_ws<float, KPC>(p, nblk, s);
+    } else {
+      if (dt == OFSC_F64) launch_c4<double, KPC>(p, nblk, s);
+      else launch_c4<float, KPC>(p, nblk, s);
+    }
   });
 }
 
@@ -471,9 +625,6 @@ k_gram_stream(int64_t n_local, const T* __restrict__ gZ, const T* __restrict__ g
 // (producers) wait for each TMA stage, convert it into one of two padded fp64
 // tiles and hand it over on an mbarrier, so the tensor-pipe warps never wait
 // for the staging copy.  Same products and summation order as k_gram_stream.
-constexpr int kGWS_NS = 3;          // TMA stages
-constexpr int kGWS_NP = 2;          // padded tiles
-constexpr int kGWS_THREADS = 384;   // 8 consumer + 4 producer warps
 
 template <typename T, int KP>
 struct GSmemWS {
