@@ -46,11 +46,11 @@ struct DBuf {
   cudaStream_t s = nullptr;
   DBuf() = default;
   DBuf(size_t bytes, cudaStream_t st) : s(st) {
-    if (bytes) OFSC_CUDA(cudaMallocAsync(&p, bytes, st));
+    if (bytes) dev_alloc(&p, bytes, st);
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    dev_free_async(p, s);
     p = nullptr;
   }
   DBuf(const DBuf&) = delete;
@@ -308,9 +308,9 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     int64_t n_comm = 0;
     double intra = 0.0;
     auto free_csr = [&] {   // stream-ordered pool frees: no device-wide synchronisation
-      if (csr.row_ptr) cudaFreeAsync(csr.row_ptr, s);
-      if (csr.col) cudaFreeAsync(csr.col, s);
-      if (csr.s) cudaFreeAsync(csr.s, s);
+      dev_free_async(csr.row_ptr, s);
+      dev_free_async(csr.col, s);
+      dev_free_async(csr.s, s);
       csr.row_ptr = nullptr;
       csr.col = nullptr;
       csr.s = nullptr;
@@ -1579,6 +1579,7 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
     OFSC_CUDA(cudaStreamWaitEvent(side.st, side.b, 0));
     OFSC_CUDA(cudaMemcpyAsync(dXf.p, h_X, (size_t)n * k * es, cudaMemcpyHostToDevice, side.st));
     OFSC_CUDA(cudaEventRecord(side.a, side.st));
+    trace_point("spectral_cluster: X0 uploaded (side stream)", side.st);
     // default: reorder when the run is long enough to repay the LPA pass
     // (c4: ~60 ms for LPA + second CSR build vs ~3 ms saved per iteration;
     // profiles/r01/SUMMARY.md, tools/build_probe.py)
@@ -1617,6 +1618,7 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
       OFSC_CUDA(cudaEventRecord(side.b, s));
       OFSC_CUDA(cudaStreamWaitEvent(side.st, side.b, 0));
       OFSC_CUDA(cudaMemcpyAsync(h_X, dXf.p, (size_t)n * k * es, cudaMemcpyDeviceToHost, side.st));
+      trace_point("spectral_cluster: features downloaded (side stream)", side.st);
     } else {
       launch_copy_out(dt, k, k, nl, dX.p,
                       (char*)dXf.p + (perm ? 0 : (size_t)g->row_begin * k * es), k,

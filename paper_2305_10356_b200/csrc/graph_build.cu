@@ -24,11 +24,9 @@ struct DevBuf {
   size_t n = 0;
   cudaStream_t s = nullptr;
   explicit DevBuf(size_t count, cudaStream_t st) : n(count), s(st) {
-    if (count) OFSC_CUDA(cudaMallocAsync(&p, count * sizeof(T), st));
+    if (count) dev_alloc((void**)&p, count * sizeof(T), st);
   }
-  ~DevBuf() {
-    if (p) cudaFreeAsync(p, s);
-  }
+  ~DevBuf() { dev_free_async(p, s); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
 };
@@ -181,9 +179,9 @@ void build_csr(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
   out.n_dups = m - out.n_loops - E;
   out.nnz = 2 * E;
   OFSC_REQUIRE(out.nnz < (int64_t(1) << 40), OFSC_ERR_ARG, "graph too large");
-  OFSC_CUDA(cudaMallocAsync(&out.row_ptr, (n + 1) * sizeof(int64_t), st));
-  OFSC_CUDA(cudaMallocAsync(&out.col, (out.nnz > 0 ? out.nnz : 1) * sizeof(int32_t), st));
-  OFSC_CUDA(cudaMallocAsync(&out.s, n * sizeof(double), st));
+  dev_alloc((void**)&out.row_ptr, (n + 1) * sizeof(int64_t), st);
+  dev_alloc((void**)&out.col, (out.nnz > 0 ? out.nnz : 1) * sizeof(int32_t), st);
+  dev_alloc((void**)&out.s, n * sizeof(double), st);
   DevBuf<int> deg(n, st);
   OFSC_CUDA(cudaMemsetAsync(deg.p, 0, n * sizeof(int), st));
   if (E > 0) {

@@ -10,6 +10,10 @@
 #include "sm100.cuh"
 
 #include <chrono>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <unordered_map>
 #include <cstring>
 #include <vector>
 #include <cstdio>
@@ -52,19 +56,33 @@ void trace_point(const char* what, cudaStream_t st) {
     const char* what;
     double host_ms;
     cudaEvent_t ev;
+    double reserved_gb, used_gb;   // default mempool
   };
   static std::vector<Pt> pts;
   cudaEvent_t ev;
   cudaEventCreate(&ev);
   cudaEventRecord(ev, st);
-  pts.push_back({what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), ev});
+  double rg = 0.0, ug = 0.0;
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    uint64_t r = 0, u = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u);
+    }
+    rg = r / 1e9;
+    ug = u / 1e9;
+  }
+  pts.push_back({what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), ev, rg, ug});
   const size_t L = strlen(what);
   if (L >= 5 && strcmp(what + L - 5, ": end") == 0) {
     cudaEventSynchronize(ev);
     for (auto& p : pts) {
       float d = 0.f;
       cudaEventElapsedTime(&d, pts[0].ev, p.ev);
-      fprintf(stderr, "[ofsc trace2] host %9.2f  device %9.2f ms  %s\n", p.host_ms - pts[0].host_ms, d, p.what);
+      fprintf(stderr, "[ofsc trace2] host %9.2f  device %9.2f ms  pool %6.2f/%6.2f GB  %s\n",
+              p.host_ms - pts[0].host_ms, d, p.used_gb, p.reserved_gb, p.what);
     }
     for (auto& p : pts) cudaEventDestroy(p.ev);
     pts.clear();
@@ -87,13 +105,77 @@ void keep_pool() {
   if (dev < 64) done |= 1ull << dev;
 }
 
+// Exact-size block cache on top of the pool.  Repeated calls with the same shapes
+// (e.g. ofsc_spectral_cluster in a loop) get their buffers back without a pool
+// round trip: with other large allocations resident, cudaMallocAsync was seen to
+// block the host for 100-800 ms on some calls (bench.py e2e, OFSC_TRACE=2).
+// A block freed stream-ordered (dev_free_async) is reused only on that stream;
+// one freed with no queued user left (dev_free) on any stream.
+namespace {
+struct BlockCache {
+  std::mutex m;
+  std::map<std::tuple<int, size_t, cudaStream_t>, std::vector<void*>> free_blocks;
+  std::unordered_map<void*, std::pair<int, size_t>> owned;   // ptr -> (device, bytes)
+  size_t cached = 0;
+  static constexpr size_t kCap = size_t(40) << 30;             // bytes kept in the cache
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache();   // process lifetime (freed memory stays cached)
+  return *c;
+}
+void* cache_take(BlockCache& c, int dev, size_t bytes, cudaStream_t key) {
+  auto it = c.free_blocks.find(std::make_tuple(dev, bytes, key));
+  if (it == c.free_blocks.end() || it->second.empty()) return nullptr;
+  void* p = it->second.back();
+  it->second.pop_back();
+  c.cached -= bytes;
+  return p;
+}
+void cache_put(void* p, cudaStream_t key, cudaStream_t free_st) {
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> lk(c.m);
+  auto it = c.owned.find(p);
+  if (it == c.owned.end()) {   // not ours (plain pool allocation)
+    cudaFreeAsync(p, free_st);
+    return;
+  }
+  const int dev = it->second.first;
+  const size_t bytes = it->second.second;
+  if (c.cached + bytes > BlockCache::kCap) {
+    c.owned.erase(it);
+    cudaFreeAsync(p, free_st);
+    return;
+  }
+  c.free_blocks[std::make_tuple(dev, bytes, key)].push_back(p);
+  c.cached += bytes;
+}
+}  // namespace
+
 void dev_alloc(void** p, size_t bytes, cudaStream_t st) {
   keep_pool();
+  int dev = 0;
+  OFSC_CUDA(cudaGetDevice(&dev));
+  BlockCache& c = block_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.m);
+    void* q = cache_take(c, dev, bytes, nullptr);
+    if (!q) q = cache_take(c, dev, bytes, st);
+    if (q) {
+      *p = q;
+      return;
+    }
+  }
   OFSC_CUDA(cudaMallocAsync(p, bytes, st));
+  std::lock_guard<std::mutex> lk(c.m);
+  c.owned[*p] = std::make_pair(dev, bytes);
 }
 
 void dev_free(void* p) {
-  if (p) cudaFreeAsync(p, 0);
+  if (p) cache_put(p, nullptr, 0);
+}
+
+void dev_free_async(void* p, cudaStream_t st) {
+  if (p) cache_put(p, st, st);
 }
 
 int grid_rows(int64_t n_rows, int blocks_per_sm) {

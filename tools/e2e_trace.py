@@ -17,6 +17,11 @@ hs, hd = torch.from_numpy(s).pin_memory(), torch.from_numpy(d).pin_memory()
 hx = torch.from_numpy(X0).pin_memory()
 import ctypes as C  # noqa: E402
 L = ofsc.lib()
+if os.environ.get("E2E_RESIDENT"):       # keep a built graph + run workspace alive (as bench.py)
+    g_res = ofsc.Graph(cfg.n, s, d, reorder=True)
+    X_res = torch.from_numpy(X0).cuda()
+    ofsc.run(g_res, "ofm_f2", X_res, 10)
+    torch.cuda.synchronize()
 h_lab = torch.empty(cfg.n, dtype=torch.int32).pin_memory()
 h_rows = torch.from_numpy(rows).pin_memory()
 o = ofsc.make_opts(cfg.k, cfg.iters)
