@@ -153,19 +153,35 @@ __global__ void __launch_bounds__(256) k_beta(IterParams p, int nblk, int reduce
   if (p.ctl->stop) return;
   const int tid = threadIdx.x, KP = p.KP, k = p.k;
   const int t = p.ctl->iter;
-  if (tid < KP) {
-    double a = 0.0, b = 0.0;
-    if (reduced) {
-      a = p.colred[tid];
-      b = p.colred[KP + tid];
-    } else {
-      for (int q = 0; q < nblk; ++q) {
-        a += p.part_cols[(int64_t)q * 2 * KP + tid];
-        b += p.part_cols[(int64_t)q * 2 * KP + KP + tid];
-      }
+  if (reduced) {
+    if (tid < KP) {
+      s_gg[tid] = p.colred[tid];
+      s_dg[tid] = p.colred[KP + tid];
     }
-    s_gg[tid] = a;
-    s_dg[tid] = b;
+  } else {
+    // column c summed by 4 threads over 4 contiguous block ranges, then in range order
+    const int c = tid % KP, part = tid / KP, nparts = 256 / KP;
+    const int per = (nblk + nparts - 1) / nparts;
+    const int q0 = part * per, q1 = min(nblk, q0 + per);
+    double a = 0.0, b = 0.0;
+    if (part < nparts)
+      for (int q = q0; q < q1; ++q) {
+        a += p.part_cols[(int64_t)q * 2 * KP + c];
+        b += p.part_cols[(int64_t)q * 2 * KP + KP + c];
+      }
+    red[tid] = a;
+    red[256 + tid] = b;
+    __syncthreads();
+    if (tid < KP) {
+      double x = red[tid], y = red[256 + tid];
+      for (int q = 1; q < nparts; ++q) {
+        x += red[q * KP + tid];
+        y += red[256 + q * KP + tid];
+      }
+      s_gg[tid] = x;
+      s_dg[tid] = y;
+    }
+    __syncthreads();
   }
   // objective from M, W: f1 = ||A||^2 + 2 tr W + ||M||^2 ; f2 = 2 tr W - tr(M W); and tr M
   const bool f1 = (p.method == OFSC_OFM_F1 || p.method == OFSC_TRIOFM_F1);

@@ -262,17 +262,43 @@ void launch_gram_pair(ofsc_dtype dt, int KP, int64_t n, const void* A, const voi
 // ----------------------------------------------------------------------------
 // Fixed-order reduction of per-CTA partials (deterministic; no fp atomics).
 // ----------------------------------------------------------------------------
-__global__ void k_reduce_partials(const double* part, int nblk, int per_blk, double* out) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= per_blk) return;
+// Fixed-order reduction of nblk partial arrays: a CTA owns 32 consecutive outputs;
+// its 8 warps sum the partials of 8 contiguous segments of [0, nblk) in order, then
+// the 8 segment sums are added in segment order (deterministic; 8 independent load
+// streams per output instead of one dependent chain).
+__global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ part, int nblk,
+                                                         int per_blk, double* __restrict__ out) {
+  __shared__ double seg[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = blockIdx.x * 32 + lane;
+  const int per_seg = (nblk + 7) / 8;
+  const int b0 = w * per_seg, b1 = min(nblk, b0 + per_seg);
   double a = 0.0;
-  for (int b = 0; b < nblk; ++b) a += part[(int64_t)b * per_blk + g];
-  out[g] = a;
+  if (g < per_blk) {
+    int b = b0;
+    for (; b + 4 <= b1; b += 4) {   // loads of 4 partials in flight, added in order
+      const double v0 = part[(int64_t)b * per_blk + g], v1 = part[(int64_t)(b + 1) * per_blk + g];
+      const double v2 = part[(int64_t)(b + 2) * per_blk + g], v3 = part[(int64_t)(b + 3) * per_blk + g];
+      a += v0;
+      a += v1;
+      a += v2;
+      a += v3;
+    }
+    for (; b < b1; ++b) a += part[(int64_t)b * per_blk + g];
+  }
+  seg[w][lane] = a;
+  __syncthreads();
+  if (w == 0 && g < per_blk) {
+    double t = seg[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += seg[q][lane];
+    out[g] = t;
+  }
 }
 
 void launch_reduce_partials(const double* part, int nblk, int per_blk, double* out,
                             cudaStream_t st) {
-  k_reduce_partials<<<(per_blk + 255) / 256, 256, 0, st>>>(part, nblk, per_blk, out);
+  k_reduce_partials<<<(per_blk + 31) / 32, 256, 0, st>>>(part, nblk, per_blk, out);
   OFSC_LAUNCH_CHECK();
 }
 
