@@ -87,6 +87,14 @@ const char* ofsc_version(void);
 const char* ofsc_status_string(ofsc_status s);
 const char* ofsc_last_error(void);
 
+/* Device memory held for reuse: the library keeps the buffers of destroyed
+ * graphs and finished calls (exact-size block cache, <= OFSC_BLOCK_CACHE_GB,
+ * default 40, over the device's stream-ordered pool) so repeated calls with
+ * the same shapes allocate nothing.  ofsc_trim_memory synchronises the current
+ * device, releases every cached block and trims the pool, returning the memory
+ * to other allocators (e.g. PyTorch's).  Not part of any paper step. */
+ofsc_status ofsc_trim_memory(void);
+
 /* ---- communicator (NCCL over NVLink/NVSwitch) ---------------------------
  * Rank 0 calls ofsc_get_unique_id and broadcasts the 128 bytes (e.g. with
  * torch.distributed); every rank then calls ofsc_comm_create on its own GPU. */

@@ -84,6 +84,7 @@ _I32 = C.c_int32
 _ST = C.c_int
 SIGNATURES = {
     "ofsc_version": (C.c_char_p, []),
+    "ofsc_trim_memory": (_ST, []),
     "ofsc_status_string": (C.c_char_p, [_ST]),
     "ofsc_last_error": (C.c_char_p, []),
     "ofsc_get_unique_id": (_ST, [_P]),
@@ -149,6 +150,11 @@ def _check(st):
 
 def version():
     return lib().ofsc_version().decode()
+
+
+def trim_memory():
+    """Release the library's cached device blocks and trim its pool (ofsc_trim_memory)."""
+    _check(lib().ofsc_trim_memory())
 
 
 # ---------------------------------------------------------------------------

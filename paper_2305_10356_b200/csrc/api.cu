@@ -153,6 +153,10 @@ extern "C" {
 
 const char* ofsc_version(void) { return "ofsc 0.1.0 (sm_100a)"; }
 
+ofsc_status ofsc_trim_memory(void) {
+  return guard([&] { dev_trim(); });
+}
+
 const char* ofsc_status_string(ofsc_status s) {
   switch (s) {
     case OFSC_OK: return "ok";

@@ -100,6 +100,7 @@ void keep_pool();    // default mempool keeps freed scratch (no per-build re-map
 void dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p);                          // no queued work uses p any more
 void dev_free_async(void* p, cudaStream_t st);   // stream-ordered on st
+void dev_trim();   // release cached blocks and trim the pool of the current device
 void trace_point(const char* what, cudaStream_t st);   // OFSC_TRACE=1: phase timestamps
 
 // grid sizes of the TMA-pipelined streaming kernels (<= 4 * #SMs)

@@ -117,7 +117,10 @@ struct BlockCache {
   std::map<std::tuple<int, size_t, cudaStream_t>, std::vector<void*>> free_blocks;
   std::unordered_map<void*, std::pair<int, size_t>> owned;   // ptr -> (device, bytes)
   size_t cached = 0;
-  static constexpr size_t kCap = size_t(40) << 30;             // bytes kept in the cache
+  size_t cap = [] {                                            // bytes kept in the cache
+    const char* e = getenv("OFSC_BLOCK_CACHE_GB");               // default 40 GB
+    return (size_t)((e && *e) ? atof(e) : 40.0) << 30;
+  }();
 };
 BlockCache& block_cache() {
   static BlockCache* c = new BlockCache();   // process lifetime (freed memory stays cached)
@@ -141,7 +144,7 @@ void cache_put(void* p, cudaStream_t key, cudaStream_t free_st) {
   }
   const int dev = it->second.first;
   const size_t bytes = it->second.second;
-  if (c.cached + bytes > BlockCache::kCap) {
+  if (c.cached + bytes > c.cap) {
     c.owned.erase(it);
     cudaFreeAsync(p, free_st);
     return;
@@ -165,13 +168,54 @@ void dev_alloc(void** p, size_t bytes, cudaStream_t st) {
       return;
     }
   }
-  OFSC_CUDA(cudaMallocAsync(p, bytes, st));
+  cudaError_t e = cudaMallocAsync(p, bytes, st);
+  if (e == cudaErrorMemoryAllocation) {
+    // out of memory: hand every cached block of this device back, then retry once
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lk(c.m);
+    for (auto& kv : c.free_blocks) {
+      if (std::get<0>(kv.first) != dev) continue;
+      for (void* q : kv.second) {
+        cudaFreeAsync(q, std::get<2>(kv.first));
+        c.owned.erase(q);
+        c.cached -= std::get<1>(kv.first);
+      }
+      kv.second.clear();
+    }
+    cudaDeviceSynchronize();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(p, bytes, st);
+  }
+  OFSC_CUDA(e);
   std::lock_guard<std::mutex> lk(c.m);
   c.owned[*p] = std::make_pair(dev, bytes);
 }
 
 void dev_free(void* p) {
   if (p) cache_put(p, nullptr, 0);
+}
+
+void dev_trim() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaDeviceSynchronize();
+  BlockCache& c = block_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.m);
+    for (auto& kv : c.free_blocks) {
+      if (std::get<0>(kv.first) != dev) continue;
+      for (void* q : kv.second) {
+        cudaFreeAsync(q, std::get<2>(kv.first));
+        c.owned.erase(q);
+        c.cached -= std::get<1>(kv.first);
+      }
+      kv.second.clear();
+    }
+  }
+  cudaDeviceSynchronize();
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
 }
 
 void dev_free_async(void* p, cudaStream_t st) {
