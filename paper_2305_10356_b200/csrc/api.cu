@@ -72,6 +72,8 @@ struct Workspace {
   void* sendbuf = nullptr;  // p > 1: packed rows of the halo exchange
   cudaStream_t comm_st = nullptr;            // p > 1: halo exchange overlapped with the SpMM
   cudaEvent_t ev_v = nullptr, ev_x = nullptr;
+  cudaStream_t fork_st = nullptr;            // p == 1: C4's Gram reduction beside the SpMM
+  cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;
   double *part_cols = nullptr, *part_g4 = nullptr, *part_g2 = nullptr, *grams = nullptr;
   double* state = nullptr;  // M, W [KP*KP each], alpha, beta, gg_prev [KP], colred [2KP]
   DevCtl* ctl = nullptr;
@@ -89,6 +91,11 @@ struct Workspace {
     if (ev_x) cudaEventDestroy(ev_x);
     comm_st = nullptr;
     ev_v = ev_x = nullptr;
+    if (fork_st) cudaStreamDestroy(fork_st);
+    if (ev_f0) cudaEventDestroy(ev_f0);
+    if (ev_f1) cudaEventDestroy(ev_f1);
+    fork_st = nullptr;
+    ev_f0 = ev_f1 = nullptr;
     if (e_iter) cudaGraphExecDestroy(e_iter);
     if (e_refresh) cudaGraphExecDestroy(e_refresh);
     if (e_loop) cudaGraphExecDestroy(e_loop);
@@ -770,6 +777,11 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
     OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_v, cudaEventDisableTiming));
     OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_x, cudaEventDisableTiming));
   }
+  if (g->p == 1) {
+    OFSC_CUDA(cudaStreamCreateWithFlags(&w.fork_st, cudaStreamNonBlocking));
+    OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_f0, cudaEventDisableTiming));
+    OFSC_CUDA(cudaEventCreateWithFlags(&w.ev_f1, cudaEventDisableTiming));
+  }
   const int nbmax = num_sms() * 4;   // grids of the streaming kernels are chosen per run
   w.nb2 = gram_stream_grid(dt, KP, nl);
   dev_alloc((void**)&w.part_cols, (size_t)nbmax * 2 * KP * 8, s);
@@ -924,6 +936,16 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     pr.ph(OFSC_PH_BETA, 1, [&] { launch_beta(p, w.nb3, 1, s); });
   }
   pr.ph(OFSC_PH_DIRECTION_GRAM, 1, [&] { launch_direction_gram(dt, p, w.nb4, s); });
+  // p == 1: C4's partial Grams (Q, P) are reduced on a forked stream while the SpMM
+  // and C2b run; the line search joins it (off the critical path)
+  const bool fork_reduce = g->p == 1 && w.fork_st && !pr.timing;
+  if (fork_reduce)
+    pr.ph(OFSC_PH_GRAM_REDUCE, 1, [&] {
+      OFSC_CUDA(cudaEventRecord(w.ev_f0, s));
+      OFSC_CUDA(cudaStreamWaitEvent(w.fork_st, w.ev_f0, 0));
+      launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, w.fork_st);
+      OFSC_CUDA(cudaEventRecord(w.ev_f1, w.fork_st));
+    });
   if (g->p > 1 && overlap_exchange() && !pr.timing) {
     // halo exchange on the comm stream while the SpMM sums the own-row columns;
     // the halo columns are added once the exchange lands
@@ -954,8 +976,9 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {
     launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
   });
-  pr.ph(OFSC_PH_GRAM_REDUCE, 2, [&] {
-    launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, s);
+  pr.ph(OFSC_PH_GRAM_REDUCE, fork_reduce ? 1 : 2, [&] {
+    if (fork_reduce) OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_f1, 0));
+    else launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, s);
     launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, w.grams + 2 * p.KP * p.KP, s);
   });
   pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, w.grams, 4 * (size_t)p.KP * p.KP, s); });
