@@ -976,9 +976,14 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {
     launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
   });
-  pr.ph(OFSC_PH_GRAM_REDUCE, fork_reduce ? 1 : 2, [&] {
-    if (fork_reduce) OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_f1, 0));
-    else launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, s);
+  if (fork_reduce) {
+    // p == 1: C2b's partials reduced and the line search run by one kernel (its last CTA)
+    OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_f1, 0));
+    pr.ph(OFSC_PH_LINE_SEARCH, 1, [&] { launch_reduce_linesearch(p, w.part_g2, w.nb2, s); });
+    return;
+  }
+  pr.ph(OFSC_PH_GRAM_REDUCE, 2, [&] {
+    launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, s);
     launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, w.grams + 2 * p.KP * p.KP, s);
   });
   pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, w.grams, 4 * (size_t)p.KP * p.KP, s); });

@@ -52,6 +52,7 @@ struct DevCtl {
   int n_zero;    // degenerate cubics
   double gnorm0, gnorm, obj;
   int limit;     // device-side loop (CUDA graph while node): run while iter < limit && !stop
+  unsigned int ls_done;   // CTAs of k_reduce_linesearch done (the last one runs the line search)
 };
 
 // Everything the per-iteration kernels need, passed by value.
@@ -174,6 +175,9 @@ void launch_reduce_cols(const IterParams& p, int nblk, cudaStream_t st);
 void launch_beta(const IterParams& p, int nblk, int reduced, cudaStream_t st);
 // exact line search + algebraic M, W update (1 CTA)
 void launch_linesearch(const IterParams& p, cudaStream_t st);
+// fixed-order reduction of nblk partial (T, R') arrays into grams[2..3] fused with the
+// line search: the last CTA to finish its slice runs it (p == 1)
+void launch_reduce_linesearch(const IterParams& p, const double* part, int nblk, cudaStream_t st);
 // line-search hook: coefficients from given Grams (device), no ctl
 void launch_linesearch_hook(int method, int k, int KP, const double* grams, double* M, double* W,
                             double* alpha, int* codes, cudaStream_t st);

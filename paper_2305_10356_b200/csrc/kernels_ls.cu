@@ -461,6 +461,75 @@ void launch_linesearch(const IterParams& p, cudaStream_t st) {
   OFSC_LAUNCH_CHECK();
 }
 
+__global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const double* __restrict__ part,
+                                                           int nblk) {
+  __shared__ double red[11 * 256];
+  __shared__ LsOut out;
+  __shared__ int s_last;
+  if (p.ctl->stop) return;
+  const int KP = p.KP;
+  const int per_blk = 2 * KP * KP;
+  double* dst = p.grams + 2 * KP * KP;              // T, R'
+  {
+    // this CTA's 32 outputs: 8 warps sum 8 contiguous partial ranges in order, then
+    // the 8 range sums in range order (as k_reduce_partials)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = blockIdx.x * 32 + lane;
+    const int per_seg = (nblk + 7) / 8;
+    const int b0 = w * per_seg, b1 = min(nblk, b0 + per_seg);
+    double a = 0.0;
+    if (g < per_blk) {
+      int b = b0;
+      for (; b + 4 <= b1; b += 4) {
+        const double v0 = part[(int64_t)b * per_blk + g], v1 = part[(int64_t)(b + 1) * per_blk + g];
+        const double v2 = part[(int64_t)(b + 2) * per_blk + g], v3 = part[(int64_t)(b + 3) * per_blk + g];
+        a += v0;
+        a += v1;
+        a += v2;
+        a += v3;
+      }
+      for (; b < b1; ++b) a += part[(int64_t)b * per_blk + g];
+    }
+    red[w * 32 + lane] = a;
+    __syncthreads();
+    if (w == 0 && g < per_blk) {
+      double t = red[lane];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) t += red[q * 32 + lane];
+      dst[g] = t;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&p.ctl->ls_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();                                   // every slice of T, R' is visible
+  const int t = p.ctl->iter;
+  const double* g = p.grams;
+  ls_core(p.method, p.k, KP, g, g + KP * KP, g + 2 * KP * KP, g + 3 * KP * KP, p.M, p.W,
+          p.line_search, p.alpha_fixed, p.alpha, p.hist_code ? p.hist_code + (int64_t)t * KP : nullptr,
+          red, &out);
+  __syncthreads();
+  const int tid = threadIdx.x;
+  if (p.hist_alpha && tid < KP) p.hist_alpha[(int64_t)t * KP + tid] = p.alpha[tid];
+  if (tid == 0) {
+    p.hist[(int64_t)t * 4 + 2] = out.amin;
+    p.hist[(int64_t)t * 4 + 3] = out.amax;
+    p.ctl->n_three += out.n_three;
+    p.ctl->n_zero += out.n_zero;
+    if (out.diverged) p.ctl->stop = 2;
+    else p.ctl->iter = t + 1;
+    p.ctl->ls_done = 0u;                             // next iteration
+  }
+}
+
+void launch_reduce_linesearch(const IterParams& p, const double* part, int nblk, cudaStream_t st) {
+  const int per_blk = 2 * p.KP * p.KP;
+  k_reduce_linesearch<<<(per_blk + 31) / 32, 256, 0, st>>>(p, part, nblk);
+  OFSC_LAUNCH_CHECK();
+}
+
 __global__ void __launch_bounds__(256) k_linesearch_hook(int method, int k, int KP,
                                                          const double* g, double* M, double* W,
                                                          double* alpha, int* codes) {
