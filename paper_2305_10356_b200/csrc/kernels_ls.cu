@@ -164,11 +164,26 @@ __global__ void __launch_bounds__(256) k_beta(IterParams p, int nblk, int reduce
     const int per = (nblk + nparts - 1) / nparts;
     const int q0 = part * per, q1 = min(nblk, q0 + per);
     double a = 0.0, b = 0.0;
-    if (part < nparts)
-      for (int q = q0; q < q1; ++q) {
+    if (part < nparts) {
+      int q = q0;
+      for (; q + 8 <= q1; q += 8) {      // 16 loads in flight, added in order
+        double va[8], vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          va[u] = p.part_cols[(int64_t)(q + u) * 2 * KP + c];
+          vb[u] = p.part_cols[(int64_t)(q + u) * 2 * KP + KP + c];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a += va[u];
+          b += vb[u];
+        }
+      }
+      for (; q < q1; ++q) {
         a += p.part_cols[(int64_t)q * 2 * KP + c];
         b += p.part_cols[(int64_t)q * 2 * KP + KP + c];
       }
+    }
     red[tid] = a;
     red[256 + tid] = b;
     __syncthreads();
@@ -480,13 +495,12 @@ __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const d
     double a = 0.0;
     if (g < per_blk) {
       int b = b0;
-      for (; b + 4 <= b1; b += 4) {
-        const double v0 = part[(int64_t)b * per_blk + g], v1 = part[(int64_t)(b + 1) * per_blk + g];
-        const double v2 = part[(int64_t)(b + 2) * per_blk + g], v3 = part[(int64_t)(b + 3) * per_blk + g];
-        a += v0;
-        a += v1;
-        a += v2;
-        a += v3;
+      for (; b + 8 <= b1; b += 8) {      // 8 loads in flight, added in order
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = part[(int64_t)(b + u) * per_blk + g];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a += v[u];
       }
       for (; b < b1; ++b) a += part[(int64_t)b * per_blk + g];
     }

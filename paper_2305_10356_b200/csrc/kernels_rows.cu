@@ -320,13 +320,12 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restric
   double a = 0.0;
   if (g < per_blk) {
     int b = b0;
-    for (; b + 4 <= b1; b += 4) {   // loads of 4 partials in flight, added in order
-      const double v0 = part[(int64_t)b * per_blk + g], v1 = part[(int64_t)(b + 1) * per_blk + g];
-      const double v2 = part[(int64_t)(b + 2) * per_blk + g], v3 = part[(int64_t)(b + 3) * per_blk + g];
-      a += v0;
-      a += v1;
-      a += v2;
-      a += v3;
+    for (; b + 8 <= b1; b += 8) {   // loads of 8 partials in flight, added in order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(int64_t)(b + u) * per_blk + g];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
     }
     for (; b < b1; ++b) a += part[(int64_t)b * per_blk + g];
   }
