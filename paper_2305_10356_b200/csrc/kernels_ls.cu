@@ -201,8 +201,14 @@ __global__ void __launch_bounds__(256) k_beta(IterParams p, int nblk, int reduce
   // objective from M, W: f1 = ||A||^2 + 2 tr W + ||M||^2 ; f2 = 2 tr W - tr(M W); and tr M
   const bool f1 = (p.method == OFSC_OFM_F1 || p.method == OFSC_TRIOFM_F1);
   double v[3] = {0.0, 0.0, 0.0};
-  for (int e = tid; e < k * k; e += 256) {
-    const int i = e / k, j = e % k;
+  int oi = tid / k, oj = tid % k;
+  const int odi = 256 / k, odj = 256 % k;
+  for (int e = tid; e < k * k; e += 256, oi += odi, oj += odj) {
+    if (oj >= k) {
+      oj -= k;
+      ++oi;
+    }
+    const int i = oi, j = oj;
     const double m = p.M[i * KP + j];
     v[0] += f1 ? m * m : m * p.W[j * KP + i];
     if (i == j) {
@@ -300,8 +306,14 @@ __device__ void ls_core(int method, int k, int KP, const double* Q, const double
     double v[11];
 #pragma unroll
     for (int q = 0; q < 11; ++q) v[q] = 0.0;
-    for (int e = tid; e < k * k; e += 256) {
-      const int i = e / k, j = e % k;
+    // (i, j) = (e / k, e % k) for e = tid, tid + 256, ..., stepped without divisions
+    int i = tid / k, j = tid % k;
+    const int di = 256 / k, dj = 256 % k;
+    for (int e = tid; e < k * k; e += 256, i += di, j += dj) {
+      if (j >= k) {
+        j -= k;
+        ++i;
+      }
       const double q_ij = QQ(i, j), p_ij = PP(i, j);
       if (method == OFSC_OFM_F1) {
         v[0] += q_ij * QQ(j, i);          // tr(QQ)
@@ -433,8 +445,13 @@ __device__ void ls_core(int method, int k, int KP, const double* Q, const double
   }
   if (!div && M) {
     // M += P^T D + D P + D Q D ; W += R' D + D R'^T + D T D   (D = diag alpha)
-    for (int e = tid; e < KP * KP; e += 256) {
-      const int i = e / KP, j = e % KP;
+    int i = tid / KP, j = tid % KP;
+    const int di = 256 / KP, dj = 256 % KP;
+    for (int e = tid; e < KP * KP; e += 256, i += di, j += dj) {
+      if (j >= KP) {
+        j -= KP;
+        ++i;
+      }
       const double ai = s_alpha[i], aj = s_alpha[j];
       M[e] = M[e] + PP(j, i) * aj + ai * PP(i, j) + ai * QQ(i, j) * aj;
       W[e] = W[e] + RR(i, j) * aj + ai * RR(j, i) + ai * TT(i, j) * aj;
