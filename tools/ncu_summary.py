@@ -45,7 +45,8 @@ for r in rows:
 ids = sorted(launch)
 short = {"k_update_direction": "update_direction", "k_direction_gram": "direction_gram",
          "k_spmm": "spmm", "k_gram_stream": "gram_stream", "k_beta": "beta",
-         "k_linesearch": "line_search", "k_reduce_partials": "gram_reduce"}
+         "k_linesearch": "line_search", "k_reduce_linesearch": "line_search",
+         "k_reduce_partials": "gram_reduce"}
 # the last iteration: the last k_update_direction launch and what follows it
 last_c3 = max(i for i in ids if launch[i]["kernel"].startswith("void ofsc::k_update_direction")
               or launch[i]["kernel"].startswith("k_update_direction"))
@@ -54,7 +55,7 @@ for i in ids:                                   # one iteration: C3 ... line sea
     if i < last_c3:
         continue
     it.append(launch[i])
-    if "k_linesearch" in launch[i]["kernel"]:
+    if "linesearch" in launch[i]["kernel"]:       # k_linesearch or k_reduce_linesearch
         break
 summ = []
 for d in it:
