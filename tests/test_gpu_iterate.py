@@ -322,3 +322,16 @@ def test_streamed_neighbour_scales_bitwise(method, monkeypatch):
     o = run_ofm(op, method, X0, 10, refresh=0)
     assert rel(X_b, o.X) <= 1e-10
     g2.close()
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_graph_launch_structure_is_transparent(method):
+    """The captured iteration (Q/P reduction on a forked branch, T/R' reduction fused
+    with the line search in its last CTA) and the per-launch profiled sequence
+    (separate reductions and line search on one stream) compute the same numbers
+    bit for bit: identical reductions, identical line search."""
+    cfg, op, g, X0, _ = setup("c2")
+    Xa, ra = gpu_run(g, method, X0, 25)
+    Xb, rb = gpu_run(g, method, X0, 25, profile=True)
+    assert np.array_equal(Xa, Xb)
+    assert np.array_equal(ra.history, rb.history)
