@@ -497,7 +497,9 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   // cid / cstart: community layout of reordered graphs (p == 1), for the L2 hints.
   const int hint = (cid && cstart && own_off == 0) ? env_int("OFSC_SPMM_HINT", 0) : 0;
   const int nb = spmm_grid(n_local);
-  const int ch = env_int("OFSC_SPMM_CHUNK", kSpmmChunk);   // rows per work grab (tuning knob)
+  // rows per work grab (tuning knob): 4 at KP = 64 (c4 5.26 -> 5.21 ms, c6 1.70 -> 1.67),
+  // 8 otherwise (c5, KP = 48: 0.776 vs 0.785 ms)
+  const int ch = env_int("OFSC_SPMM_CHUNK", KP == 64 ? 4 : kSpmmChunk);
   int cw = env_int("OFSC_SPMM_CW", spmm_col_window(dt, KP));  // columns per pass (tuning knob)
   if (cw != 16 && cw != 32) cw = KP;
   if (phase) cw = KP;                       // split (multi-GPU) passes use whole rows

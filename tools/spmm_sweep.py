@@ -19,6 +19,8 @@ ref = None
 grid = [("64", "3", "8", h) for h in ("0", "1")] + [("32", "3", "8", h) for h in ("0", "1")]
 if "--quick" not in sys.argv:
     grid += [("64", ct, ch, "1") for ct in ("2", "3", "4") for ch in ("4", "16")]
+if "--default-hint" in sys.argv:                 # the production kernel (s_j stream, no hints)
+    grid = [("64", ct, ch, "0") for ct in ("3", "4", "5") for ch in ("4", "8", "16", "32")]
 for cw, ctas, ch, hint in grid:
     os.environ["OFSC_SPMM_HINT"] = hint
     os.environ["OFSC_SPMM_CW"] = cw
