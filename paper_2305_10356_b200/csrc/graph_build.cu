@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(256) k_lpa_pass(int64_t n, const int64_t* __re
                                                   const int32_t* __restrict__ col,
                                                   const int* __restrict__ lin, int* __restrict__ lout,
                                                   int colour, uint32_t seed,
-                                                  unsigned long long* changes) {
+                                                  unsigned long long* changes, int fast) {
   __shared__ int keys[8][kLpaSlots];
   __shared__ int cnts[8][kLpaSlots];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -787,6 +787,36 @@ __global__ void __launch_bounds__(256) k_lpa_pass(int64_t n, const int64_t* __re
     const int deg = (int)min((int64_t)kLpaCap, row_ptr[i + 1] - beg);
     if (deg == 0) {
       if (lane == 0) lout[i] = own;
+      continue;
+    }
+    if (deg <= 32 && fast) {
+      // one neighbour per lane: __match_any_sync groups the lanes holding the same
+      // label, so its popcount is that label's count (no table, no atomics); the
+      // selection below is the table path's (count, hash, label) rule exactly
+      const bool has = lane < deg;
+      const int L = has ? lin[col[beg + lane]] : -1 - lane;   // padding lanes: singletons
+      const unsigned m = __match_any_sync(0xffffffffu, L);
+      const int c = has ? __popc(m) : 0;
+      int owncnt = (has && L == own) ? c : 0;
+      int bc = has ? c : 0, bl = has ? L : -1;
+      uint32_t bh = has ? mix32((uint32_t)L, seed) : 0xffffffffu;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        const uint32_t oh = __shfl_xor_sync(0xffffffffu, bh, o);
+        if (oc > bc || (oc == bc && (oh < bh || (oh == bh && ol < bl)))) {
+          bc = oc;
+          bl = ol;
+          bh = oh;
+        }
+        owncnt = max(owncnt, __shfl_xor_sync(0xffffffffu, owncnt, o));
+      }
+      const int nl = (owncnt >= bc) ? own : bl;
+      if (lane == 0) {
+        lout[i] = nl;
+        nchg += nl != own;
+      }
       continue;
     }
     // open-addressing table sized to the (capped) degree: >= 2 deg slots, >= 32
@@ -909,13 +939,17 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
   int* cur = la.p;
   int* nxt = lb.p;
   const int nb = num_sms() * 8;
+  static const int fast = [] {          // OFSC_LPA_FAST=0: table path for every node (A/B)
+    const char* e = getenv("OFSC_LPA_FAST");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
   // sweeps until fewer than n/1000 labels change (at least 6, at most `sweeps`)
   unsigned long long chg = 0, *h_chg = &chg;   // pageable: no pinned alloc / free (device syncs)
   for (int sw = 0; sw < sweeps; ++sw) {
     OFSC_CUDA(cudaMemsetAsync(ic.p, 0, sizeof(unsigned long long), st));
     for (int colour = 0; colour < 2; ++colour) {
       k_lpa_pass<<<nb, 256, 0, st>>>(n, csr.row_ptr, csr.col, cur, nxt, colour,
-                                     (uint32_t)(2 * sw + colour + 1), ic.p);
+                                     (uint32_t)(2 * sw + colour + 1), ic.p, fast);
       OFSC_LAUNCH_CHECK();
       std::swap(cur, nxt);
     }
