@@ -1368,7 +1368,8 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
     const int W = dim + 1;
     DBuf chg(3 * 8, s), pin((size_t)nb * 8, s), part((size_t)nbp * K * W * 8, s),
         red((size_t)K * W * 8, s), tot(8, s),
-        lbd(fused ? (size_t)std::max<int64_t>(n_local, 1) * 8 : 8, s), dlt((size_t)K * 8, s);
+        lbd(fused ? (size_t)std::max<int64_t>(n_local, 1) * 8 : 8, s), dlt((size_t)K * 8, s),
+        sep((size_t)K * 8, s);
     OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
     // pinned counter readback, allocated once per host thread (cudaFreeHost would
     // synchronise the whole device, e.g. the feature download of spectral_cluster)
@@ -1383,6 +1384,8 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
     }
     const bool stats = getenv("OFSC_KMEANS_STATS") != nullptr;   // per-step skip statistics
     const bool noskip = getenv("OFSC_KMEANS_NOSKIP") != nullptr; // A/B: no bound test
+    const char* elk = getenv("OFSC_KMEANS_ELKAN");                // A/B: 0 = Hamerly bound only
+    const bool elkan = !(elk && elk[0] == '0');
     int it = 0;
     double inertia = 0.0;
     for (it = 1; it <= max_iters; ++it) {
@@ -1397,7 +1400,8 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
       if (n_local > 0 && fused)
         launch_kmeans_step(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
                            chg.as<unsigned long long>(), pin.as<double>(), part.as<double>(),
-                           lbd.as<double>(), it > 1 && !noskip ? dlt.as<double>() : nullptr, nb, s);
+                           lbd.as<double>(), it > 1 && !noskip ? dlt.as<double>() : nullptr,
+                           elkan ? sep.as<double>() : nullptr, nb, s);
       else if (n_local > 0)
         launch_kmeans_assign(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
                              chg.as<unsigned long long>(), pin.as<double>(), nb, s);
@@ -1431,7 +1435,10 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
       launch_reduce_partials(part.as<double>(), nbp, K * W, red.as<double>(), s);
       if (comm && comm->nranks > 1)
         OFSC_NCCL(ncclAllReduce(red.p, red.p, (size_t)K * W, ncclFloat64, ncclSum, comm->nccl, s));
-      if (fused) launch_kmeans_finish_delta(K, dim, red.as<double>(), d_centroids, dlt.as<double>(), s);
+      if (fused) {
+        launch_kmeans_finish_delta(K, dim, red.as<double>(), d_centroids, dlt.as<double>(), s);
+        launch_kmeans_halfsep(K, dim, d_centroids, sep.as<double>(), s);
+      }
       else launch_kmeans_finish(K, dim, red.as<double>(), d_centroids, s);
     }
     OFSC_CUDA(cudaStreamSynchronize(s));

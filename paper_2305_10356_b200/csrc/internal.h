@@ -214,7 +214,9 @@ int kmeans_step_blocks(int64_t n);
 void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                         const double* C, int* labels, unsigned long long* changes,
                         double* part_inertia, double* part, double* lbound, const double* delta,
-                        int nblk, cudaStream_t st);
+                        const double* sep, int nblk, cudaStream_t st);
+// sep[c] = half the distance of centroid c to its nearest other centroid (deflated)
+void launch_kmeans_halfsep(int K, int dim, const double* C, double* sep, cudaStream_t st);
 // fused path: C = means (empty keeps), delta[c] = ||C_new - C_old|| (dim <= 64)
 void launch_kmeans_finish_delta(int K, int dim, const double* red, double* C, double* delta,
                                 cudaStream_t st);

@@ -464,7 +464,8 @@ __global__ void __launch_bounds__(kKmThreads, NBW == 1 ? 2 : 1)
 k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
               const double* __restrict__ C, int* __restrict__ labels,
               unsigned long long* changes, double* part_inertia, double* part,
-              double* __restrict__ lbound, const double* __restrict__ delta) {
+              double* __restrict__ lbound, const double* __restrict__ delta,
+              const double* __restrict__ sep) {
   // DP: dim rounded up to a multiple of 16 (padding columns are zero)
   constexpr int TR = kKsRows;
   constexpr int PRE = TR * DP / kKmThreads;       // tile elements per thread
@@ -624,8 +625,12 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
         const double dm = old_lab == s_i1 ? s_m2 : s_m1;
         Da = sd;
         lnew = old_lb - dm - kKmRel * (old_lb + dm);
-        // sqrt(Da) (1 + rel) < lnew, compared in squares (Da >= 0)
-        skip = lnew > 0.0 && Da * ((1.0 + kKmRel) * (1.0 + kKmRel)) < lnew * lnew;
+        // sqrt(Da) (1 + rel) < lnew, compared in squares (Da >= 0); or Elkan's test:
+        // sqrt(Da) (1 + rel) < sep[a] (half the distance from c_a to its nearest other
+        // centroid, deflated) -> every other centroid is farther by the triangle inequality
+        const double da2 = Da * ((1.0 + kKmRel) * (1.0 + kKmRel));
+        const double sa = sep ? sep[old_lab] : 0.0;
+        skip = (lnew > 0.0 && da2 < lnew * lnew) || (sa > 0.0 && da2 < sa * sa);
       }
       if (rw == 0) fl[rrow] = (vrow && !skip) ? 1 : 0;
       if (rw == 0 && skip) ++nskip;
@@ -831,14 +836,15 @@ int kmeans_step_blocks(int64_t n) {
 void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                         const double* C, int* labels, unsigned long long* changes,
                         double* part_inertia, double* part, double* lbound, const double* delta,
-                        int nblk, cudaStream_t st) {
+                        const double* sep, int nblk, cudaStream_t st) {
   const size_t smem = kmeans_step_smem(dim, K);
 #define OFSC_KS3(TT, NB, DPC)                                                                    \
   {                                                                                              \
     OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_step<TT, NB, DPC>,                                   \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
     k_kmeans_step<TT, NB, DPC><<<nblk, kKmThreads, smem, st>>>(                                  \
-        n, dim, (const TT*)Y, ldy, K, C, labels, changes, part_inertia, part, lbound, delta);   \
+        n, dim, (const TT*)Y, ldy, K, C, labels, changes, part_inertia, part, lbound, delta,    \
+        sep);                                                                                    \
   }
 #define OFSC_KS(TT, NB)                                                                          \
   switch ((dim + 15) / 16) {                                                                     \
@@ -885,6 +891,35 @@ __global__ void k_kmeans_finish_delta(int K, int dim, const double* red, double*
 void launch_kmeans_finish_delta(int K, int dim, const double* red, double* C, double* delta,
                                 cudaStream_t st) {
   k_kmeans_finish_delta<<<K, 64, 0, st>>>(K, dim, red, C, delta);
+  OFSC_LAUNCH_CHECK();
+}
+
+// sep[c] = half the distance from centroid c to its nearest other centroid, deflated
+// by 1e-12 so it bounds the exact value from below (+inf when K == 1)
+__global__ void k_kmeans_halfsep(int K, int dim, const double* __restrict__ C, double* sep) {
+  __shared__ double s[128];
+  const int c = blockIdx.x, t = threadIdx.x;
+  double best = CUDART_INF;
+  for (int o = t; o < K; o += blockDim.x) {
+    if (o == c) continue;
+    double a = 0.0;
+    for (int d = 0; d < dim; ++d) {
+      const double df = C[c * dim + d] - C[o * dim + d];
+      a = a + df * df;
+    }
+    best = fmin(best, a);
+  }
+  s[t] = best;
+  __syncthreads();
+  if (t == 0) {
+    double m = CUDART_INF;
+    for (int q = 0; q < (int)blockDim.x; ++q) m = fmin(m, s[q]);
+    sep[c] = isinf(m) ? CUDART_INF : 0.5 * sqrt(m) * (1.0 - 1e-12);
+  }
+}
+
+void launch_kmeans_halfsep(int K, int dim, const double* C, double* sep, cudaStream_t st) {
+  k_kmeans_halfsep<<<K, 128, 0, st>>>(K, dim, C, sep);
   OFSC_LAUNCH_CHECK();
 }
 
