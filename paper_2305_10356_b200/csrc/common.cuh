@@ -38,6 +38,39 @@ __device__ __forceinline__ double ld1(const float* p) { return (double)*p; }
 __device__ __forceinline__ void st1(double* p, double v) { *p = v; }
 __device__ __forceinline__ void st1(float* p, double v) { *p = (float)v; }
 
+// Fixed-order reduction of nblk partial arrays (part[b][g], g < per_blk) by one
+// 256-thread CTA for its 32 consecutive outputs g = blockIdx.x * 32 + lane: its 8
+// warps sum 8 contiguous ranges of b in order (8 loads in flight), then the 8 range
+// sums are added in range order (deterministic).  seg: 256 doubles of shared memory.
+__device__ __forceinline__ void reduce_slice32(const double* __restrict__ part, int nblk,
+                                               int per_blk, double* __restrict__ out,
+                                               double* seg) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = blockIdx.x * 32 + lane;
+  const int per_seg = (nblk + 7) / 8;
+  const int b0 = w * per_seg, b1 = min(nblk, b0 + per_seg);
+  double a = 0.0;
+  if (g < per_blk) {
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(int64_t)(b + u) * per_blk + g];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
+    }
+    for (; b < b1; ++b) a += part[(int64_t)b * per_blk + g];
+  }
+  seg[w * 32 + lane] = a;
+  __syncthreads();
+  if (w == 0 && g < per_blk) {
+    double t = seg[lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += seg[q * 32 + lane];
+    out[g] = t;
+  }
+}
+
 // Dispatch on the padded width.
 #define OFSC_DISPATCH_KP(KP, ...)                       \
   switch (KP) {                                         \

@@ -502,34 +502,7 @@ __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const d
   const int KP = p.KP;
   const int per_blk = 2 * KP * KP;
   double* dst = p.grams + 2 * KP * KP;              // T, R'
-  {
-    // this CTA's 32 outputs: 8 warps sum 8 contiguous partial ranges in order, then
-    // the 8 range sums in range order (as k_reduce_partials)
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int g = blockIdx.x * 32 + lane;
-    const int per_seg = (nblk + 7) / 8;
-    const int b0 = w * per_seg, b1 = min(nblk, b0 + per_seg);
-    double a = 0.0;
-    if (g < per_blk) {
-      int b = b0;
-      for (; b + 8 <= b1; b += 8) {      // 8 loads in flight, added in order
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = part[(int64_t)(b + u) * per_blk + g];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) a += v[u];
-      }
-      for (; b < b1; ++b) a += part[(int64_t)b * per_blk + g];
-    }
-    red[w * 32 + lane] = a;
-    __syncthreads();
-    if (w == 0 && g < per_blk) {
-      double t = red[lane];
-#pragma unroll
-      for (int q = 1; q < 8; ++q) t += red[q * 32 + lane];
-      dst[g] = t;
-    }
-  }
+  reduce_slice32(part, nblk, per_blk, dst, red);    // this CTA's 32 outputs (common.cuh)
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&p.ctl->ls_done, 1u) == gridDim.x - 1;

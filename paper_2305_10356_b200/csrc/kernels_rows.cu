@@ -306,37 +306,11 @@ void launch_gram_pair(ofsc_dtype dt, int KP, int64_t n, const void* A, const voi
 // ----------------------------------------------------------------------------
 // Fixed-order reduction of per-CTA partials (deterministic; no fp atomics).
 // ----------------------------------------------------------------------------
-// Fixed-order reduction of nblk partial arrays: a CTA owns 32 consecutive outputs;
-// its 8 warps sum the partials of 8 contiguous segments of [0, nblk) in order, then
-// the 8 segment sums are added in segment order (deterministic; 8 independent load
-// streams per output instead of one dependent chain).
+// Fixed-order reduction of nblk partial arrays (reduce_slice32, common.cuh).
 __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ part, int nblk,
                                                          int per_blk, double* __restrict__ out) {
-  __shared__ double seg[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int g = blockIdx.x * 32 + lane;
-  const int per_seg = (nblk + 7) / 8;
-  const int b0 = w * per_seg, b1 = min(nblk, b0 + per_seg);
-  double a = 0.0;
-  if (g < per_blk) {
-    int b = b0;
-    for (; b + 8 <= b1; b += 8) {   // loads of 8 partials in flight, added in order
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = part[(int64_t)(b + u) * per_blk + g];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a += v[u];
-    }
-    for (; b < b1; ++b) a += part[(int64_t)b * per_blk + g];
-  }
-  seg[w][lane] = a;
-  __syncthreads();
-  if (w == 0 && g < per_blk) {
-    double t = seg[0][lane];
-#pragma unroll
-    for (int q = 1; q < 8; ++q) t += seg[q][lane];
-    out[g] = t;
-  }
+  __shared__ double seg[256];
+  reduce_slice32(part, nblk, per_blk, out, seg);
 }
 
 void launch_reduce_partials(const double* part, int nblk, int per_blk, double* out,
