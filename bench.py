@@ -467,6 +467,8 @@ class OracleSampler:
         self.W = self.X.T @ self.AX
         self.Gp = direction(method, self.X, self.AX, self.M, self.W)
         self.Vp = -self.Gp
+        from oracle import colsum
+        self.gg_prev = colsum(self.Gp * self.Gp)      # PR denominator over all rows
         n = cfg.n
         self.blocks = 1 if n <= 250_000 else max(1, int(round(n / 312_500)))   # ~1-2 s per sample at c4
         self.bounds = np.linspace(0, n, self.blocks + 1).astype(np.int64)
@@ -485,7 +487,7 @@ class OracleSampler:
         r0, r1 = int(self.bounds[b]), int(self.bounds[b + 1])
         t = time.perf_counter()
         iteration_rows(self.op, self.method, self.X, self.AX, self.Gp, self.Vp, self.M, self.W,
-                       r0, r1, S_rows=self.S_rows[b], sVp=self.sVp)
+                       r0, r1, S_rows=self.S_rows[b], sVp=self.sVp, gg_prev=self.gg_prev)
         return time.perf_counter() - t, r1 - r0
 
     def describe(self, cfg, nsteps):

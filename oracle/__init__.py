@@ -26,7 +26,7 @@ No function is "parity unpinned".
 """
 from .operator import (Operator, build_operator, apply_A, dense_A, fro2_A)
 from .methods import (METHODS, direction, objective, grams, cubic_coefficients,
-                      run_ofm, OFMResult, stop_constant)
+                      run_ofm, OFMResult, stop_constant, beta_pr, colsum, gram, pairwise_sum)
 from .cubic import cubic_roots, select_step, psi, BRANCH
 from .cluster import row_normalize, kmeans_lloyd, ari, nmi
 from .eig import jacobi_eigh
@@ -34,7 +34,7 @@ from .eig import jacobi_eigh
 __all__ = [
     "Operator", "build_operator", "apply_A", "dense_A", "fro2_A",
     "METHODS", "direction", "objective", "grams", "cubic_coefficients",
-    "run_ofm", "OFMResult", "stop_constant",
+    "run_ofm", "OFMResult", "stop_constant", "beta_pr", "colsum", "gram", "pairwise_sum",
     "cubic_roots", "select_step", "psi", "BRANCH",
     "row_normalize", "kmeans_lloyd", "ari", "nmi", "jacobi_eigh",
 ]

@@ -13,6 +13,11 @@ transpose of X^T A V"), M = X^T X, W = X^T A X.
 Algorithm 2: G = g(X); beta = sumeachcol((G - Gp).G) / sumeachcol(Gp.Gp)
 (column-wise Polak-Ribiere, P:359, with PR+ clamp by default, R5); V = -G + beta.Vp;
 exact line search; X_i += alpha_i V_i.
+
+Summation rule for every reduction over the N rows (Grams, column dots; SURVEY
+8(c).2 step 2, R29): sums over fixed 1024-row blocks, then the block
+sums combined pairwise in block order, so the oracle's own rounding stays at
+~u (1024 + log2(N/1024)) at N = 5M instead of growing with N.
 """
 from __future__ import annotations
 
@@ -52,9 +57,70 @@ def objective(method, M, W, fro2):
     return 2.0 * np.trace(W) - np.sum(M * W.T)
 
 
+BLOCK_ROWS = 1024
+
+
+def pairwise_sum(parts):
+    """Sum of parts[0], parts[1], ... combined pairwise in order: ((p0+p1)+(p2+p3))+..."""
+    parts = np.asarray(parts)
+    if parts.shape[0] == 0:
+        return np.zeros(parts.shape[1:])
+    while parts.shape[0] > 1:
+        m = parts.shape[0] // 2
+        nxt = parts[0:2 * m:2] + parts[1:2 * m:2]
+        parts = np.concatenate([nxt, parts[2 * m:]]) if parts.shape[0] % 2 else nxt
+    return parts[0]
+
+
+def _row_blocks(Z):
+    """Z's rows as full 1024-row blocks (a view) plus the ragged tail block (or None)."""
+    n = Z.shape[0]
+    nb = n // BLOCK_ROWS
+    full = Z[:nb * BLOCK_ROWS].reshape((nb, BLOCK_ROWS) + Z.shape[1:])
+    tail = Z[nb * BLOCK_ROWS:] if n % BLOCK_ROWS else None
+    return full, tail
+
+
+def colsum(Z):
+    """sum_r Z[r, :] by the summation rule (1024-row blocks, pairwise over blocks)."""
+    full, tail = _row_blocks(np.asarray(Z, dtype=np.float64))
+    parts = full.sum(axis=1)
+    if tail is not None:
+        parts = np.concatenate([parts, tail.sum(axis=0)[None]])
+    return pairwise_sum(parts)
+
+
+def gram(A, B):
+    """A^T B = sum_r A[r]^T B[r] by the summation rule (1024-row blocks, pairwise)."""
+    fa, ta = _row_blocks(np.asarray(A, dtype=np.float64))
+    fb, tb = _row_blocks(np.asarray(B, dtype=np.float64))
+    parts = np.matmul(fa.transpose(0, 2, 1), fb)
+    if ta is not None:
+        parts = np.concatenate([parts, (ta.T @ tb)[None]])
+    return pairwise_sum(parts)
+
+
 def grams(V, X, AV):
     """Q = V^T V, P = V^T X, T = V^T (AV), R' = X^T (AV)."""
-    return V.T @ V, V.T @ X, V.T @ AV, X.T @ AV
+    return gram(V, V), gram(V, X), gram(V, AV), gram(X, AV)
+
+
+def beta_pr(G, Gp, gg_prev, rule="pr+"):
+    """Column-wise Polak-Ribiere (Alg. 2 l.9):
+    beta_i = sum_r (G - Gp)_ri G_ri / sum_r Gp_ri^2, 0 where the denominator is 0;
+    rule "pr+" clamps at 0 (R5), "pr" is the printed formula, "zero" gives 0.
+    gg_prev = sum_r Gp_ri^2 (column sums kept from the previous iteration)."""
+    k = G.shape[1]
+    if rule == "zero":
+        return np.zeros(k)
+    num = colsum((G - Gp) * G)
+    den = np.asarray(gg_prev, dtype=np.float64)
+    beta = np.where(den > 0.0, num / np.where(den > 0.0, den, 1.0), 0.0)
+    if rule == "pr+":
+        beta = np.maximum(beta, 0.0)
+    elif rule != "pr":
+        raise ValueError(rule)
+    return beta
 
 
 def _d(A, B):
@@ -102,6 +168,7 @@ class OFMResult:
     objective: float
     history: np.ndarray                     # [T, 4] objective, ||G||_F, alpha min, alpha max
     alphas: list = field(default_factory=list)     # per iteration: k-vector
+    betas: list = field(default_factory=list)      # per iteration: k-vector (0 at t = 0)
     codes: list = field(default_factory=list)      # per iteration: k branch codes
     state: dict = field(default_factory=dict)      # final AX, M, W (tests)
 
@@ -125,8 +192,8 @@ def run_ofm(op: Operator, method: str, X0, T: int, *, tol=0.0, beta_rule="pr+",
     fro2 = fro2_A(op)
     X = rnd(np.array(X0, dtype=np.float64))
     AX = apply_A(op, X, precision)
-    M = X.T @ X
-    W = X.T @ AX
+    M = gram(X, X)
+    W = gram(X, AX)
     Gp = Vp = gg_prev = None
     hist = np.full((T, 4), np.nan)
     res = OFMResult(X=X, iters=0, converged=False, diverged=False, grad_norm0=np.nan,
@@ -135,10 +202,10 @@ def run_ofm(op: Operator, method: str, X0, T: int, *, tol=0.0, beta_rule="pr+",
     for t in range(T):
         if t > 0 and refresh >= 1 and t % refresh == 0:
             AX = apply_A(op, X, precision)
-            M = X.T @ X
-            W = X.T @ AX
+            M = gram(X, X)
+            W = gram(X, AX)
         G = rnd(direction(method, X, AX, M, W))            # Alg. 2 l.8
-        gg = np.sum(G * G, axis=0)
+        gg = colsum(G * G)
         gnorm = float(np.sqrt(np.sum(gg)))
         obj = float(objective(method, M, W, fro2))
         hist[t, 0], hist[t, 1] = obj, gnorm
@@ -152,13 +219,12 @@ def run_ofm(op: Operator, method: str, X0, T: int, *, tol=0.0, beta_rule="pr+",
             res.converged = True
             break
         if t == 0 or beta_rule == "zero":                  # Alg. 2 l.4
+            beta = np.zeros(k)
             V = -G
         else:                                              # Alg. 2 l.9-10
-            num = np.sum((G - Gp) * G, axis=0)
-            beta = np.where(gg_prev > 0.0, num / np.where(gg_prev > 0.0, gg_prev, 1.0), 0.0)
-            if beta_rule == "pr+":
-                beta = np.maximum(beta, 0.0)
+            beta = beta_pr(G, Gp, gg_prev, beta_rule)
             V = rnd(-G + Vp * beta[None, :])
+        res.betas.append(beta.copy())
         AV = apply_A(op, V, precision)
         Q, P, Tm, Rp = grams(V, X, AV)
         if line_search:                                    # Alg. 2 l.11

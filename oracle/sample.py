@@ -10,31 +10,38 @@ the arithmetic of `methods.run_ofm`'s loop body (same functions: `direction`,
 `grams`, `cubic_coefficients`, `select_step`; the SpMM is `apply_A`'s formula
 -Z - s (S (s Z)) on the block's rows of S) on rows [r0, r1) with the k x k
 line search done once, and the caller scales the time by N / (r1 - r0).
-One deviation, cost-neutral: a block cannot see the new direction of the
+Two deviations, both cost-neutral: a block cannot see the new direction of the
 other rows, so its SpMM gathers the previous direction Vp (same sparsity,
-same flops and bytes as A V).  The numbers it produces are not used for
-parity; the timed arithmetic is the oracle's own, untuned.
+same flops and bytes as A V), and its beta numerator sums the block's rows
+only (the denominator ||Gp_i||^2 is the previous iteration's full column sum,
+`gg_prev`, computed untimed by the caller, as Alg. 2 l.9 and
+`methods.beta_pr` divide).  The numbers it produces are not used for parity;
+the timed arithmetic is the oracle's own, untuned.
 """
 from __future__ import annotations
 
 import numpy as np
 
 from .cubic import select_step
-from .methods import cubic_coefficients, direction, grams
+from .methods import beta_pr, colsum, cubic_coefficients, direction, grams
 
 
-def iteration_rows(op, method, X, AX, Gp, Vp, M, W, r0, r1, beta=None, S_rows=None, sVp=None):
+def iteration_rows(op, method, X, AX, Gp, Vp, M, W, r0, r1, beta=None, S_rows=None, sVp=None,
+                   gg_prev=None, beta_rule="pr+"):
     """One Algorithm-2 iteration on rows [r0, r1).  X, AX, Gp, Vp are
     full n x k arrays (V is gathered through S at all rows); returns alpha.
+    gg_prev = sum_r Gp_ri^2 over ALL rows (the PR denominator); when None
+    it is the block's own column sums of Gp.
     S_rows = op.S[r0:r1] and sVp = s * Vp (all rows) may be passed precomputed:
     the block's share of s * Vp is then recomputed inside (its per-block cost)."""
     k = X.shape[1]
     rows = slice(r0, r1)
     G = direction(method, X[rows], AX[rows], M, W)                  # Alg. 2 l.8
-    gg = np.sum(G * G, axis=0)
-    num = np.sum((G - Gp[rows]) * G, axis=0)                        # Alg. 2 l.9
-    if beta is None:
-        beta = np.maximum(num / np.maximum(gg, 1e-300), 0.0)
+    gg = colsum(G * G)                                              # ||G_i||^2 (next gg_prev)
+    if beta is None:                                                # Alg. 2 l.9
+        if gg_prev is None:
+            gg_prev = colsum(Gp[rows] * Gp[rows])
+        beta = beta_pr(G, Gp[rows], gg_prev, beta_rule)
     V = -G + Vp[rows] * beta[None, :]                               # Alg. 2 l.10
     s = op.s[:, None]
     if S_rows is None:

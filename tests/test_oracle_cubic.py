@@ -103,3 +103,50 @@ def test_selected_root_minimises_psi_on_grid(seed):
     a, _ = select_step(*c)
     grid = np.linspace(-2 * abs(a), 2 * abs(a), 101)
     assert psi(*c, a) <= min(psi(*c, g) for g in grid) + 1e-10
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_random_cubics_negative_leading_coefficient(seed):
+    """c3 < 0 (TriOFM-f2 can produce it): the bullets of P:307-312 are
+    followed literally -- the only real root, the single-multiplicity root, or
+    among three real roots the one of minimal psi.  For c3 < 0, psi is a quartic
+    opening downwards whose three critical points are max, min, max, so the
+    minimal-psi root is the MIDDLE root (the only local minimum of psi)."""
+    rng = np.random.default_rng(10_000 + seed)
+    eps = 10.0 ** rng.uniform(-6, 0)
+    c = (-rng.uniform(0.1, 1) * eps * eps, rng.standard_normal() * eps,
+         rng.standard_normal(), rng.standard_normal())
+    a, code = select_step(*c)
+    scale = abs(c[0]) * abs(a) ** 3 + abs(c[1]) * a * a + abs(c[2]) * abs(a) + abs(c[3])
+    assert abs(((c[0] * a + c[1]) * a + c[2]) * a + c[3]) <= 1e-12 * scale
+    brute = brute_real_roots(c)
+    assert min(abs(a - r) for r in brute) <= 1e-7 * (1 + abs(a))
+    best = min(brute, key=lambda r: psi(*c, r))
+    assert psi(*c, a) <= psi(*c, best) + 1e-10 * (1 + abs(psi(*c, best)))
+    if len(brute) == 3:
+        assert code in (BRANCH["three0"], BRANCH["three1"], BRANCH["three2"])
+        assert abs(a - brute[1]) <= 1e-7 * (1 + abs(a))
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_negative_leading_three_roots_selects_middle(seed):
+    """c3 < 0 with three well-separated real roots r0 < r1 < r2: alpha = r1."""
+    rng = np.random.default_rng(300 + seed)
+    r = np.sort(rng.standard_normal(3) * 2)
+    while np.min(np.diff(r)) < 0.1:
+        r = np.sort(rng.standard_normal(3) * 2)
+    c3 = -rng.uniform(0.5, 2)
+    c = (c3, -c3 * r.sum(), c3 * (r[0] * r[1] + r[0] * r[2] + r[1] * r[2]), -c3 * r.prod())
+    a, code = select_step(*c)
+    assert code in (BRANCH["three0"], BRANCH["three1"], BRANCH["three2"])
+    assert abs(a - r[1]) <= 1e-12 * (1 + abs(r[1]))
+    # psi(r1) is a local minimum: psi increases to both sides up to the other roots
+    for x in np.linspace(r[0], r[2], 41):
+        if r[0] < x < r[2]:
+            assert psi(*c, a) <= psi(*c, x) + 1e-12
+
+
+def test_negative_leading_one_root_is_taken():
+    """c3 < 0 with one real root: that root, although it maximises psi."""
+    a, code = select_step(-1.0, 0.0, -1.0, 2.0)          # -(a^3 + a - 2) = -(a - 1)(a^2 + a + 2)
+    assert code == BRANCH["one"] and abs(a - 1.0) < 1e-15
