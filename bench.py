@@ -57,7 +57,32 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-methods", action="store_true")
+    ap.add_argument("--passes", type=int, default=5, help="timed passes of K steps (median, min)")
+    ap.add_argument("--no-random-ids", action="store_true")
+    ap.add_argument("--no-ari", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check: each rank prints its rank / world size and exits")
     return ap.parse_args()
+
+
+def launch_ranks(args):
+    """`--gpus N` outside torchrun: re-launch this command as N ranks (one process per
+    GPU, torch.distributed.run on 127.0.0.1).  Inside torchrun WORLD_SIZE must equal N."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus and args.gpus != 1:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def peaks():
@@ -549,6 +574,12 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
+    launch_ranks(a)
+    if a.dry_run:
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")),
+                          "world": int(os.environ.get("WORLD_SIZE", "1")),
+                          "gpus": a.gpus}), flush=True)
+        sys.exit(0)
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -107,6 +107,20 @@ ofsc_status ofsc_comm_destroy(ofsc_comm comm);
  * rank-partial reductions; ofsc_run / ofsc_kmeans reject it (OFSC_ERR_STATE).
  * Lets one process check the multi-rank partition and layout on one GPU. */
 ofsc_status ofsc_comm_create_local(int nranks, int rank, ofsc_comm* out);
+/* In-process world of `nranks` ranks on the CURRENT device, WITHOUT NCCL:
+ * h_out[r] (host array of nranks handles, filled) is the communicator of rank
+ * r.  Every call of the library then runs the full p > 1 schedule of the
+ * row-partitioned multi-GPU path: halo exchange
+ * of V / X rows, sums over ranks (all-gather + fixed rank-order sum, the same
+ * kernel the NCCL path runs), split SpMM, K-means reductions.  The transport
+ * is host barriers + device-to-device copies between the ranks' buffers, so
+ * EACH RANK MUST BE DRIVEN BY ITS OWN HOST THREAD (a collective returns only
+ * when every rank has reached it) and every rank must make the same sequence
+ * of calls.  No kernel waits on another rank's kernel.  Iterations run as
+ * eager launches (host barriers cannot be captured in a CUDA graph).  For
+ * tests and emulation of the multi-GPU schedule on one GPU; destroy each
+ * handle with ofsc_comm_destroy.  OFSC_ERR_ARG: nranks < 1 or h_out NULL. */
+ofsc_status ofsc_comm_create_local_world(int nranks, ofsc_comm* h_out);
 /* Host-only: contiguous split of rows [0, n) over p ranks with ~equal nnz(A)
  * = sum_i (deg_i + 1), from CSR offsets h_row_ptr[n+1]; h_begins[p+1] out. */
 ofsc_status ofsc_partition_rows(int64_t n, const int64_t* h_row_ptr, int p, int64_t* h_begins);

@@ -91,6 +91,7 @@ SIGNATURES = {
     "ofsc_comm_create": (_ST, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "ofsc_comm_destroy": (_ST, [_P]),
     "ofsc_comm_create_local": (_ST, [C.c_int, C.c_int, C.POINTER(_P)]),
+    "ofsc_comm_create_local_world": (_ST, [C.c_int, C.POINTER(_P)]),
     "ofsc_partition_rows": (_ST, [_I64, _P, C.c_int, _P]),
     "ofsc_graph_build": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, _P, C.POINTER(_P)]),
     "ofsc_graph_build_ex": (_ST, [_P, _I64, _I64, _P, _P, C.c_int, C.POINTER(BuildOpts), _P,
@@ -237,6 +238,68 @@ class LocalComm:
         if self.handle:
             _check(lib().ofsc_comm_destroy(self.handle))
             self.handle = None
+
+
+class LocalWorld:
+    """In-process world of `size` ranks on the current GPU without NCCL
+    (ofsc_comm_create_local_world): every call runs the full p > 1 schedule
+    (halo exchange, rank-order sums, split SpMM) between the ranks.  Each rank
+    must be driven by its own host thread: use `run`."""
+
+    class _RankComm:
+        def __init__(self, handle, size, rank):
+            self.handle, self.size, self.rank = handle, size, rank
+
+        def close(self):
+            if self.handle:
+                _check(lib().ofsc_comm_destroy(self.handle))
+                self.handle = None
+
+    def __init__(self, size):
+        arr = (C.c_void_p * int(size))()
+        _check(lib().ofsc_comm_create_local_world(int(size), arr))
+        self.size = int(size)
+        self.comms = [LocalWorld._RankComm(C.c_void_p(arr[r]), self.size, r)
+                      for r in range(self.size)]
+
+    def run(self, fn, timeout=900.0):
+        """fn(rank, comm) on one host thread per rank (each with its own CUDA stream);
+        returns the per-rank results, re-raising the first exception.  A rank that
+        fails outside a collective leaves the others waiting at the next one: the
+        threads are daemons and `timeout` (s) turns that into a TimeoutError."""
+        import threading
+        torch = _torch()
+        dev = torch.cuda.current_device()
+        out = [None] * self.size
+        err = [None] * self.size
+
+        def body(r):
+            try:
+                torch.cuda.set_device(dev)
+                with torch.cuda.stream(torch.cuda.Stream()):
+                    out[r] = fn(r, self.comms[r])
+                    torch.cuda.current_stream().synchronize()
+            except BaseException as e:  # noqa: BLE001 (re-raised below)
+                err[r] = e
+
+        ths = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(self.size)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join(timeout)
+        for e in err:
+            if e is not None:
+                raise e
+        if any(t.is_alive() for t in ths):
+            raise TimeoutError("local world: a rank did not reach a collective")
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+
+    def close(self):
+        for c in self.comms:
+            c.close()
 
 
 def partition_rows(row_ptr, p):

@@ -139,6 +139,7 @@ struct ofsc_graph_s {
   std::vector<int64_t> recv_cnt, recv_off, send_cnt, send_off;
   int32_t* d_send_idx = nullptr;   // own rows to send, grouped by peer
   int64_t total_send = 0;
+  double* red_gather = nullptr;    // p > 1: [p][4 KP^2] scratch of the rank-order sums (comm.cu)
   // the local CSR split per row: own-row columns | halo columns (p > 1, for the overlap)
   int64_t* row_ptr_loc = nullptr;
   int32_t* col_loc = nullptr;
@@ -256,6 +257,23 @@ ofsc_status ofsc_partition_rows(int64_t n, const int64_t* h_row_ptr, int p, int6
   });
 }
 
+ofsc_status ofsc_comm_create_local_world(int nranks, ofsc_comm* out) {
+  return guard([&] {
+    OFSC_REQUIRE(out && nranks >= 1, OFSC_ERR_ARG, "bad communicator arguments");
+    int dev = 0;
+    OFSC_CUDA(cudaGetDevice(&dev));
+    auto world = make_local_world(nranks);
+    for (int r = 0; r < nranks; ++r) {
+      auto* c = new ofsc_comm_s();
+      c->nranks = nranks;
+      c->rank = r;
+      c->device = dev;
+      c->world = world;
+      out[r] = c;
+    }
+  });
+}
+
 ofsc_status ofsc_comm_create_local(int nranks, int rank, ofsc_comm* out) {
   return guard([&] {
     OFSC_REQUIRE(out && nranks >= 1 && rank >= 0 && rank < nranks, OFSC_ERR_ARG,
@@ -281,6 +299,7 @@ static void graph_free(ofsc_graph g) {
   dfree(g->cstart);
   dfree(g->d_gid);
   dfree(g->d_send_idx);
+  dfree(g->red_gather);
   dfree(g->row_ptr_loc);
   dfree(g->col_loc);
   dfree(g->row_ptr_rem);
@@ -348,7 +367,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
           lpa_order(csr, sweeps, g->perm, inv.as<int32_t>(), &n_comm, &intra, g->cid, &g->cstart, s);
           DBuf s2(m * sizeof(int64_t), s), d2(m * sizeof(int64_t), s);
           trace_point("graph_build: LPA order", s);
-          relabel_edges(m, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
+          relabel_edges(m, n, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
           free_csr();
           build_csr(n, m, s2.as<int64_t>(), d2.as<int64_t>(), csr, s);
           g->reordered = true;
@@ -428,6 +447,7 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
       g->col_rem = hl.col_rem;
       g->own_off = 0;
       g->slot_rows = hl.ext_rows;
+      dev_alloc((void**)&g->red_gather, (size_t)p * 4 * OFSC_MAX_K * OFSC_MAX_K * sizeof(double), s);
       OFSC_CUDA(cudaStreamSynchronize(s));
       build_heavy(g->row_ptr_loc, g->n_local, g->heavy_loc, s);
       build_heavy(g->row_ptr_rem, g->n_local, g->heavy_rem, s);
@@ -493,7 +513,7 @@ ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const
     if (g->reordered) {   // original ids -> internal (community-ordered) rows; the order is kept
       k_invert_perm_b<<<num_sms() * 8, 256, 0, s>>>(n, g->perm, inv.as<int32_t>());
       OFSC_LAUNCH_CHECK();
-      relabel_edges(m, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
+      relabel_edges(m, n, psrc, pdst, inv.as<int32_t>(), s2.as<int64_t>(), d2.as<int64_t>(), s);
       psrc = s2.as<int64_t>();
       pdst = d2.as<int64_t>();
     }
@@ -647,28 +667,24 @@ __global__ void k_pack_rows(int64_t rows, int KP, const int32_t* idx, const void
 
 static void halo_exchange(ofsc_graph g, ofsc_dtype dt, int KP, void* ext, void* sendbuf,
                           cudaStream_t s) {
-  const size_t es = esize(dt);
+  if (!comm_active(g->comm)) return;   // a bare local test communicator has no transport
   if (g->total_send > 0) {
     k_pack_rows<<<num_sms() * 8, 256, 0, s>>>(g->total_send, KP, g->d_send_idx, ext, sendbuf,
                                              dt == OFSC_F64);
     OFSC_LAUNCH_CHECK();
   }
-  OFSC_NCCL(ncclGroupStart());
-  for (int q = 0; q < g->p; ++q) {
-    if (q == g->rank) continue;
-    if (g->send_cnt[q] > 0)
-      OFSC_NCCL(ncclSend((const char*)sendbuf + (size_t)g->send_off[q] * KP * es,
-                         (size_t)g->send_cnt[q] * KP, nccl_type(dt), q, g->comm->nccl, s));
-    if (g->recv_cnt[q] > 0)
-      OFSC_NCCL(ncclRecv((char*)ext + (size_t)g->recv_off[q] * KP * es,
-                         (size_t)g->recv_cnt[q] * KP, nccl_type(dt), q, g->comm->nccl, s));
-  }
-  OFSC_NCCL(ncclGroupEnd());
+  comm_exchange(g->comm, nccl_type(dt), KP, esize(dt), sendbuf, g->send_cnt, g->send_off, ext,
+                g->recv_cnt, g->recv_off, s);
 }
 
+// Sum over ranks of k x k partials (Grams, column dots): all-gather + rank-order sum
+// (comm.cu), identical bits on every rank.  A bare local test communicator keeps
+// rank-partial sums.
 static void allreduce_d(ofsc_graph g, double* buf, size_t count, cudaStream_t s) {
-  if (g->p > 1 && g->comm->nccl)   // a local test communicator keeps rank-partial sums
-    OFSC_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, g->comm->nccl, s));
+  if (g->p > 1 && comm_active(g->comm)) {
+    OFSC_REQUIRE(count <= (size_t)4 * OFSC_MAX_K * OFSC_MAX_K, OFSC_ERR_STATE, "reduction too large");
+    comm_sum_f64(g->comm, buf, count, g->red_gather, s);
+  }
 }
 
 __global__ void k_extract_kk(const double* in, int KP, int k, double* out) {
@@ -996,7 +1012,9 @@ static bool use_graphs(ofsc_graph g) {
     const char* e = getenv("OFSC_NO_GRAPH");
     env = (e && e[0] == '1') ? 0 : 1;
   }
-  return env == 1 && g->p == 1;
+  // p > 1: captured with the NCCL calls inside (the init refresh before the capture
+  // has already connected every peer); the local world's host barriers cannot be captured
+  return env == 1 && (g->p == 1 || (g->comm && g->comm->nccl));
 }
 
 // Device-side iteration loop: a CUDA graph whose single node is a conditional
@@ -1080,8 +1098,9 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
     OFSC_REQUIRE(ldx >= o.k && o.max_iters >= 0, OFSC_ERR_ARG, "bad ldx / max_iters");
     OFSC_REQUIRE(o.beta_rule >= 0 && o.beta_rule <= 2 && o.refresh >= 0 && o.tol >= 0.0,
                  OFSC_ERR_ARG, "bad options");
-    OFSC_REQUIRE(g->p == 1 || g->comm->nccl, OFSC_ERR_STATE,
-                 "ofsc_run needs an NCCL communicator when p > 1 (local test communicator given)");
+    OFSC_REQUIRE(g->p == 1 || comm_active(g->comm), OFSC_ERR_STATE,
+                 "ofsc_run needs an NCCL communicator or a local world when p > 1 "
+                 "(bare local test communicator given)");
     cudaStream_t s = (cudaStream_t)stream;
     const int KP = padded_k(o.k);
     trace_point("run: start", s);
@@ -1115,10 +1134,10 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
     // The iteration is captured once per call as CUDA graphs (plain and refresh
     // iteration); they bake in this call's history buffers.  Profiling runs
     // eager launches bracketed by events instead.
-    const bool graphs = use_graphs(g) && !o.profile;
+    bool graphs = use_graphs(g) && !o.profile;
     // device-side loop only on request and in tolerance mode; a fixed T launches the
     // captured iteration T times (measured faster: the host queues launches ahead)
-    const bool devloop = graphs && o.refresh == 0 && o.tol > 0.0 && use_devloop();
+    const bool devloop = graphs && g->p == 1 && o.refresh == 0 && o.tol > 0.0 && use_devloop();
     int n_launch_iter = 0, n_launch_refresh = 0;
     if (graphs) {
       if (w.e_iter) cudaGraphExecDestroy(w.e_iter);
@@ -1133,18 +1152,35 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
       // which cannot be captured); the graphs are then launched on the caller's stream.
       if (!w.cap) OFSC_CUDA(cudaStreamCreateWithFlags(&w.cap, cudaStreamNonBlocking));
       Prof c1, c2;
-      if (devloop) {
-        capture_loop(&w.g_loop, &w.e_loop, w.cap, w.ctl,
-                     [&] { iteration_ops(g, dt, p, false, w.cap, c1); });
-        n_launch_iter = c1.total() + 1;   // + the loop-condition kernel
-      } else {
-        capture(&w.g_iter, &w.e_iter, w.cap, [&] { iteration_ops(g, dt, p, false, w.cap, c1); });
-        n_launch_iter = c1.total();
-      }
-      if (o.refresh >= 1) {
-        capture(&w.g_refresh, &w.e_refresh, w.cap,
-                [&] { iteration_ops(g, dt, p, true, w.cap, c2); });
-        n_launch_refresh = c2.total();
+      try {
+        if (devloop) {
+          capture_loop(&w.g_loop, &w.e_loop, w.cap, w.ctl,
+                       [&] { iteration_ops(g, dt, p, false, w.cap, c1); });
+          n_launch_iter = c1.total() + 1;   // + the loop-condition kernel
+        } else {
+          capture(&w.g_iter, &w.e_iter, w.cap, [&] { iteration_ops(g, dt, p, false, w.cap, c1); });
+          n_launch_iter = c1.total();
+        }
+        if (o.refresh >= 1) {
+          capture(&w.g_refresh, &w.e_refresh, w.cap,
+                  [&] { iteration_ops(g, dt, p, true, w.cap, c2); });
+          n_launch_refresh = c2.total();
+        }
+      } catch (const Error& e) {
+        // p > 1: an NCCL build that cannot capture its calls -> eager launches
+        // (same kernels and collectives, same arithmetic); p == 1 never falls back
+        if (g->p == 1) throw;
+        cudaGetLastError();
+        if (w.e_iter) cudaGraphExecDestroy(w.e_iter);
+        if (w.e_refresh) cudaGraphExecDestroy(w.e_refresh);
+        if (w.g_iter) cudaGraphDestroy(w.g_iter);
+        if (w.g_refresh) cudaGraphDestroy(w.g_refresh);
+        w.e_iter = w.e_refresh = nullptr;
+        w.g_iter = w.g_refresh = nullptr;
+        graphs = false;
+        if (getenv("OFSC_TRACE"))
+          fprintf(stderr, "[ofsc] p > 1 iteration not captured (%s): eager launches\n",
+                  e.msg.c_str());
       }
     }
     trace_point("run: graphs captured", s);
@@ -1357,8 +1393,8 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                      n_clusters >= 1 && n_clusters <= 128 && max_iters >= 1,
                  OFSC_ERR_ARG, "bad kmeans args");
     OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
-    OFSC_REQUIRE(!comm || comm->nranks == 1 || comm->nccl, OFSC_ERR_STATE,
-                 "ofsc_kmeans needs an NCCL communicator when p > 1");
+    OFSC_REQUIRE(!comm || comm->nranks == 1 || comm_active(comm), OFSC_ERR_STATE,
+                 "ofsc_kmeans needs an NCCL communicator or a local world when p > 1");
     cudaStream_t s = (cudaStream_t)stream;
     const int K = n_clusters;
     const bool fused = kmeans_step_supported(dim, K);   // assign + partial sums in one pass
@@ -1366,8 +1402,10 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                          : kmeans_blocks(std::max<int64_t>(n_local, 1));
     const int nbp = fused ? nb : kmeans_partial_blocks(std::max<int64_t>(n_local, 1));
     const int W = dim + 1;
+    const int P = comm ? comm->nranks : 1;
     DBuf chg(3 * 8, s), pin((size_t)nb * 8, s), part((size_t)nbp * K * W * 8, s),
         red((size_t)K * W * 8, s), tot(8, s),
+        gat(P > 1 ? (size_t)P * std::max(K * W, 3) * 8 : 0, s),
         lbd(fused ? (size_t)std::max<int64_t>(n_local, 1) * 8 : 8, s), dlt((size_t)K * 8, s),
         sep((size_t)K * 8, s);
     OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
@@ -1407,9 +1445,9 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
                              chg.as<unsigned long long>(), pin.as<double>(), nb, s);
       if (stats) OFSC_CUDA(cudaEventRecord(eb, s));
       launch_reduce_partials(pin.as<double>(), nb, 1, tot.as<double>(), s);
-      if (comm && comm->nranks > 1) {
-        OFSC_NCCL(ncclAllReduce(chg.p, chg.p, 1, ncclUint64, ncclSum, comm->nccl, s));
-        OFSC_NCCL(ncclAllReduce(tot.p, tot.p, 1, ncclFloat64, ncclSum, comm->nccl, s));
+      if (comm_active(comm)) {
+        comm_sum_u64(comm, chg.as<unsigned long long>(), 3, gat.as<unsigned long long>(), s);
+        comm_sum_f64(comm, tot.as<double>(), 1, gat.as<double>(), s);
       }
       k_publish_counters<<<1, 32, 0, s>>>(chg.as<unsigned long long>(), tot.as<double>(), d_hchg);
       OFSC_LAUNCH_CHECK();
@@ -1433,8 +1471,7 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
       else if (n_local == 0)
         OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nbp * K * W * 8, s));
       launch_reduce_partials(part.as<double>(), nbp, K * W, red.as<double>(), s);
-      if (comm && comm->nranks > 1)
-        OFSC_NCCL(ncclAllReduce(red.p, red.p, (size_t)K * W, ncclFloat64, ncclSum, comm->nccl, s));
+      if (comm_active(comm)) comm_sum_f64(comm, red.as<double>(), (size_t)K * W, gat.as<double>(), s);
       if (fused) {
         launch_kmeans_finish_delta(K, dim, red.as<double>(), d_centroids, dlt.as<double>(), s);
         launch_kmeans_halfsep(K, dim, d_centroids, sep.as<double>(), s);
@@ -1456,8 +1493,8 @@ ofsc_status ofsc_rayleigh_ritz(ofsc_graph g, ofsc_dtype dt, int32_t k, const voi
     OFSC_REQUIRE(k >= 1 && k <= OFSC_MAX_K && k <= g->n, OFSC_ERR_ARG,
                  "need 1 <= k <= min(n, 64)");
     OFSC_REQUIRE(ldx >= k && (!d_U || ldu >= k), OFSC_ERR_ARG, "bad ldx / ldu");
-    OFSC_REQUIRE(g->p == 1 || g->comm->nccl, OFSC_ERR_STATE,
-                 "ofsc_rayleigh_ritz needs an NCCL communicator when p > 1");
+    OFSC_REQUIRE(g->p == 1 || comm_active(g->comm), OFSC_ERR_STATE,
+                 "ofsc_rayleigh_ritz needs an NCCL communicator or a local world when p > 1");
     cudaStream_t s = (cudaStream_t)stream;
     const int KP = padded_k(k);
     ensure_workspace(g, dt, KP, s);
@@ -1678,8 +1715,10 @@ extern "C" ofsc_status ofsc_spectral_cluster(ofsc_comm comm, int64_t n, int64_t 
         n_clusters, k, dR.as<int64_t>(), inv, g->p == 1 ? 0 : g->row_begin, nl, dY.p, k,
         dt == OFSC_F64, dC.as<double>());
     OFSC_LAUNCH_CHECK();
-    if (comm && comm->nranks > 1)
-      OFSC_NCCL(ncclAllReduce(dC.p, dC.p, (size_t)n_clusters * k, ncclFloat64, ncclSum, comm->nccl, s));
+    if (comm_active(comm)) {
+      DBuf gat((size_t)comm->nranks * n_clusters * k * 8, s);
+      comm_sum_f64(comm, dC.as<double>(), (size_t)n_clusters * k, gat.as<double>(), s);
+    }
     trace_point("spectral_cluster: normalised", s);
     r = ofsc_kmeans(comm, dt, nl, k, dY.p, k, n_clusters, dC.as<double>(), km_max_iters,
                     dL.as<int32_t>(), nullptr, nullptr, stream);

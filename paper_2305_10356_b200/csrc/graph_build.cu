@@ -914,12 +914,15 @@ __global__ void k_intra_edges(int64_t n, const int64_t* row_ptr, const int32_t* 
   if (c) atomicAdd(cnt, c);
 }
 
-__global__ void k_relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
-                                int64_t* s2, int64_t* d2) {
+// endpoints outside [0, n) are not looked up: they become -1, which the CSR build /
+// merge that follows rejects with OFSC_ERR_RANGE (k_make_keys)
+__global__ void k_relabel_edges(int64_t m, int64_t n, const int64_t* src, const int64_t* dst,
+                                const int32_t* inv, int64_t* s2, int64_t* d2) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
        e += (int64_t)gridDim.x * blockDim.x) {
-    s2[e] = inv[src[e]];
-    d2[e] = inv[dst[e]];
+    const int64_t u = src[e], v = dst[e];
+    s2[e] = (u >= 0 && u < n) ? (int64_t)inv[u] : -1;
+    d2[e] = (v >= 0 && v < n) ? (int64_t)inv[v] : -1;
   }
 }
 
@@ -994,10 +997,10 @@ void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv
   OFSC_CUDA(cudaStreamSynchronize(st));
 }
 
-void relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
-                   int64_t* s2, int64_t* d2, cudaStream_t st) {
+void relabel_edges(int64_t m, int64_t n, const int64_t* src, const int64_t* dst,
+                   const int32_t* inv, int64_t* s2, int64_t* d2, cudaStream_t st) {
   if (m <= 0) return;
-  k_relabel_edges<<<blocks_for(m), 256, 0, st>>>(m, src, dst, inv, s2, d2);
+  k_relabel_edges<<<blocks_for(m), 256, 0, st>>>(m, n, src, dst, inv, s2, d2);
   OFSC_LAUNCH_CHECK();
 }
 

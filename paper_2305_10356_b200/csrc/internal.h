@@ -6,6 +6,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -240,8 +241,9 @@ void append_csr(CsrDevice& csr, int64_t m, const int64_t* d_src, const int64_t* 
 // (also community id per internal row and community start rows, for L2 cache hints)
 void lpa_order(const CsrDevice& csr, int sweeps, int32_t* d_perm, int32_t* d_inv, int64_t* n_comm,
                double* intra_frac, int32_t* d_cid, int64_t** d_cstart, cudaStream_t st);
-void relabel_edges(int64_t m, const int64_t* src, const int64_t* dst, const int32_t* inv,
-                   int64_t* s2, int64_t* d2, cudaStream_t st);
+// original -> internal ids; endpoints outside [0, n) map to -1 (rejected by the build)
+void relabel_edges(int64_t m, int64_t n, const int64_t* src, const int64_t* dst,
+                   const int32_t* inv, int64_t* s2, int64_t* d2, cudaStream_t st);
 void scatter_slots(const double* s, int64_t n, double* s_slot, float* s32_slot,
                    const int64_t* d_begins, int p, int64_t slot_rows, cudaStream_t st);
 void rebase_row_ptr(const int64_t* in, int64_t rows, int64_t base, int64_t* out, cudaStream_t st);
@@ -265,9 +267,30 @@ struct HaloLayout {
 void build_halo(const CsrDevice& csr, const int64_t* h_begins, const int64_t* d_begins, int p,
                 int rank, HaloLayout& out, cudaStream_t st);
 
+// ---- collectives (comm.cu): NCCL, or an in-process local world on one device ----
+struct LocalWorld;
+std::shared_ptr<LocalWorld> make_local_world(int nranks);
 }  // namespace ofsc
 
 struct ofsc_comm_s {
   ncclComm_t nccl = nullptr;
   int nranks = 1, rank = 0, device = 0;
+  std::shared_ptr<ofsc::LocalWorld> world;   // in-process world (ofsc_comm_create_local_world)
 };
+
+namespace ofsc {
+// p > 1 with a transport (NCCL or a local world); a bare local test communicator
+// (ofsc_comm_create_local) has none: its reductions stay rank-partial
+bool comm_active(const ofsc_comm_s* c);
+// buf[0..count) <- sum over ranks in rank order (same bits on every rank); gather: p*count scratch
+void comm_sum_f64(ofsc_comm_s* c, double* buf, size_t count, double* gather, cudaStream_t s);
+void comm_sum_u64(ofsc_comm_s* c, unsigned long long* buf, size_t count,
+                  unsigned long long* gather, cudaStream_t s);
+// grouped point-to-point: rows [send_off[q], +send_cnt[q]) of sendbuf go to rank q,
+// recv_cnt[q] rows from q land at recvbuf row recv_off[q] (row = row_elems elements)
+void comm_exchange(ofsc_comm_s* c, ncclDataType_t type, size_t row_elems, size_t elem_bytes,
+                   const void* sendbuf, const std::vector<int64_t>& send_cnt,
+                   const std::vector<int64_t>& send_off, void* recvbuf,
+                   const std::vector<int64_t>& recv_cnt, const std::vector<int64_t>& recv_off,
+                   cudaStream_t s);
+}  // namespace ofsc

@@ -68,7 +68,11 @@ __device__ __forceinline__ void stg2h(float* p, float2 v, uint64_t pol) {
                "l"(pol));
 }
 
-template <typename T, int KP, int CW, int HINT, int PHASE, int SV = 0>
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+template <typename T, int KP, int CW, int HINT, int PHASE, int SV = 0, int PF = 0>
 __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
@@ -146,6 +150,18 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       for (int u = 0; u < 8; ++u) {
         if constexpr (HINT) c[u] = ldg1h(col + e + u, pf);
         else c[u] = __ldg(col + e + u);
+      }
+      if constexpr (PF) {
+        // PF = 1: the next batch's neighbour rows are prefetched into L2 (no register
+        // destination), so twice as many rows are in flight as registers hold
+        if (e + 16 <= end) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int cn = __ldg(col + e + 8 + u);
+            prefetch_l2(zc + (int64_t)cn * KP);
+            prefetch_l2(zc + (int64_t)cn * KP + H2);
+          }
+        }
       }
       V2 z0[8], z1[8];
       T sv[8];
@@ -505,25 +521,29 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   if (phase) cw = KP;                       // split (multi-GPU) passes use whole rows
   if (KP % cw) cw = KP;
   const int passes = KP / cw;
+  const int pfe = env_int("OFSC_SPMM_PF", 0);   // experiment: L2 prefetch of the next batch
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
     unsigned long long* c = ctr ? ctr + ps : nullptr;
     const int c0 = ps * cw;
-#define OFSC_SPMM_LAUNCH_S(CWC, H, PH, SVV)                                                     \
+#define OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, PFF)                                                \
     if (dt == OFSC_F64)                                                                         \
-      k_spmm<double, KPC, CWC, H, PH, SVV><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr,  \
-          col, s, s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart, hth,        \
-          (const double*)sval);                                                                 \
+      k_spmm<double, KPC, CWC, H, PH, SVV, PFF><<<nb, kThreads, 0, st>>>(n_local, own_off,      \
+          row_ptr, col, s, s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart,    \
+          hth, (const double*)sval);                                                            \
     else                                                                                        \
-      k_spmm<float, KPC, CWC, H, PH, SVV><<<nb, kThreads, 0, st>>>(n_local, own_off, row_ptr,   \
-          col, s, s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth,          \
+      k_spmm<float, KPC, CWC, H, PH, SVV, PFF><<<nb, kThreads, 0, st>>>(n_local, own_off,       \
+          row_ptr, col, s, s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth, \
           (const float*)sval);
+#define OFSC_SPMM_LAUNCH_S(CWC, H, PH, SVV) OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, 0)
 #define OFSC_SPMM_LAUNCH_P(CWC, H, PH) OFSC_SPMM_LAUNCH_S(CWC, H, PH, 0)
 #define OFSC_SPMM_LAUNCH_H(CWC, H) OFSC_SPMM_LAUNCH_P(CWC, H, 0)
 #define OFSC_SPMM_LAUNCH(CWC) \
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
-      if (sval && phase == 0 && cw == KPC && !hint) { OFSC_SPMM_LAUNCH_S(KPC, 0, 0, 1) }
+      if (sval && phase == 0 && cw == KPC && !hint) {
+        if (pfe) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 1) } else { OFSC_SPMM_LAUNCH_S(KPC, 0, 0, 1) }
+      }
       else if (phase == 1) { OFSC_SPMM_LAUNCH_P(KPC, 0, 1) }
       else if (phase == 2) { OFSC_SPMM_LAUNCH_P(KPC, 0, 2) }
       else if (cw == KPC) { OFSC_SPMM_LAUNCH(KPC) }
@@ -534,6 +554,7 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #undef OFSC_SPMM_LAUNCH_H
 #undef OFSC_SPMM_LAUNCH_P
 #undef OFSC_SPMM_LAUNCH_S
+#undef OFSC_SPMM_LAUNCH_F
     OFSC_LAUNCH_CHECK();
   }
   if (hv) launch_heavy(dt, KP, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, phase, *heavy);

@@ -98,6 +98,28 @@ def test_append_edge_cases():
     assert g.info["n_isolated"] == n - 7
 
 
+def test_append_out_of_range_on_reordered_graph():
+    """A reordered graph relabels the new edges through its permutation; endpoints
+    outside [0, n) must be rejected (OFSC_ERR_RANGE) before any lookup, and the
+    graph must stay unchanged (no out-of-bounds read of the inverse)."""
+    n = 3000
+    src, dst, _ = dcsbm_graph(n, 8, 24000, 3.0, 91, 5.0)
+    g = ofsc.Graph(n, src[:20000], dst[:20000], reorder=True)
+    info0 = dict(g.info)
+    rp0, col0, s0 = g.copy_csr()
+    for bad_s, bad_d in ((np.array([0, 7]), np.array([n, 8])),
+                         (np.array([-1, 7]), np.array([3, 8])),
+                         (np.array([5, 2 ** 40]), np.array([6, 9]))):
+        with pytest.raises(ofsc.OfscError) as e:
+            g.append(bad_s, bad_d)
+        assert e.value.status == 2
+        assert g.info == info0
+        rp, col, s_ = g.copy_csr()
+        assert np.array_equal(rp, rp0) and np.array_equal(col, col0) and np.array_equal(s_, s0)
+    g.append(src[20000:], dst[20000:])                          # a valid batch still merges
+    assert g.info["n_edges_kept"] == 24000
+
+
 @pytest.mark.parametrize("method", ["ofm_f1", "triofm_f2"])
 def test_iteration_on_appended_graph(method):
     """The run workspace is rebuilt after an append: 10 iterations on the

@@ -1,6 +1,18 @@
 """Streaming protocol (config c5 shape at small N): snapshots of
 cumulative edge parts, each run warm-started from the previous features and
-stopped at the gradient tolerance (R14).  GPU vs oracle from the same warm start."""
+stopped at the gradient tolerance (R14).  GPU vs oracle from the same warm
+start, compared on the FEATURES (principal-angle sines of the converged
+subspaces), not only on the objective.
+
+Both runs stop at tol = 1e-10 (||G||_F <= tol c_m ||X||_F), so both have
+converged and the sines are bounded by ~||G|| / (gap ||X||) << 1e-6 wherever
+the spectral gap lambda_{k+1} - lambda_k is not tiny.  Where the eigenvalue -2
+(one per connected component) has multiplicity > k, span U_k is not unique
+(Theorems 1/3, P:201-203, P:244-246 hold for any k-subset of the eigenspace;
+R22): there the test checks what IS unique -- the Ritz values of the features
+equal lambda_1..k, the features span an invariant subspace, and the objective
+equals its closed-form minimum f2* = sum_{i<=k} lambda_i (f1* = sum_{i>k} lambda_i^2).
+"""
 import numpy as np
 import pytest
 
@@ -8,8 +20,10 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2305_10356_b200 as ofsc  # noqa: E402
-from oracle import build_operator, run_ofm  # noqa: E402
+from oracle import build_operator, dense_A, fro2_A, run_ofm  # noqa: E402
 from synth import dcsbm_graph, stream_parts, x0_block  # noqa: E402
+
+TOL = 1e-10
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -19,30 +33,77 @@ def cuda():
     ofsc.lib()
 
 
+def sines(A, B):
+    """Principal-angle sines: singular values of (I - Qa Qa^T) Qb (accurate for small angles)."""
+    qa, _ = np.linalg.qr(A)
+    qb, _ = np.linalg.qr(B)
+    return np.linalg.svd(qb - qa @ (qa.T @ qb), compute_uv=False)
+
+
+def snapshots(n, blocks, edges, ratio, nparts):
+    s, d, _ = dcsbm_graph(n, blocks, edges, ratio, 77, 5.0)
+    parts = stream_parts(s, d, nparts, 78)
+    for i in range(1, nparts + 1):
+        yield (np.concatenate([p[0] for p in parts[:i]]),
+               np.concatenate([p[1] for p in parts[:i]]))
+
+
+def run_both(method, n, ss, dd, X, reorder):
+    op = build_operator(n, ss, dd)
+    g = ofsc.Graph(n, ss, dd, reorder=reorder)
+    Xg = torch.from_numpy(X.copy()).cuda()
+    r = ofsc.run(g, method, Xg, 20000, tol=TOL, check_every=1)
+    o = run_ofm(op, method, X, 20000, tol=TOL, refresh=0)
+    assert r.report["converged"] == 1 and o.converged
+    return op, r, o, Xg.cpu().numpy()
+
+
 @pytest.mark.parametrize("method", ["ofm_f1", "ofm_f2"])
-def test_warm_started_snapshots_match_oracle(method):
-    n, k = 3000, 8
-    s, d, lab = dcsbm_graph(n, 8, 24000, 3.0, 77, 5.0)
-    parts = stream_parts(s, d, 5, 78)
+def test_warm_started_snapshots_features_match_oracle(method):
+    """Well-separated stream (gap >= 0.18 at every snapshot): per snapshot the GPU
+    features span the oracle's subspace and the exact U_k to sines <= 1e-6."""
+    n, k = 2000, 6
     X = x0_block(n, k, 79)
     iters = []
-    for i in range(1, 6):
-        ss = np.concatenate([p[0] for p in parts[:i]])
-        dd = np.concatenate([p[1] for p in parts[:i]])
-        op = build_operator(n, ss, dd)
-        g = ofsc.Graph(n, ss, dd, reorder=True)
-        Xg = torch.from_numpy(X.copy()).cuda()
-        r = ofsc.run(g, method, Xg, 3000, tol=1e-4, check_every=1)
-        o = run_ofm(op, method, X, 3000, tol=1e-4, refresh=0)
-        assert r.report["converged"] == 1 and o.converged
-        # 100+ step trajectories agree only to rounding amplification (R22): the
-        # step at which the tolerance is met may move a little, and at a 1e-4
-        # gradient tolerance the clustered trailing directions are not yet fixed;
-        # the objective agrees
-        assert abs(r.report["iters"] - o.iters) <= max(3, 0.2 * o.iters)
-        Xn = Xg.cpu().numpy()
-        assert abs(r.report["objective"] - o.objective) <= 1e-6 * abs(o.objective)
+    for ss, dd in snapshots(n, 6, 40000, 5.0, 4):
+        op, r, o, Xn = run_both(method, n, ss, dd, X, reorder=True)
+        w, U = np.linalg.eigh(dense_A(op))
+        assert w[k] - w[k - 1] > 0.1
+        assert sines(Xn, o.X).max() <= 1e-6
+        assert sines(Xn, U[:, :k]).max() <= 1e-6
+        assert sines(o.X, U[:, :k]).max() <= 1e-6
+        assert abs(r.report["objective"] - o.objective) <= 1e-10 * abs(o.objective)
+        # the same trajectory to rounding: the stopping step agrees closely
+        assert abs(r.report["iters"] - o.iters) <= max(3, 0.1 * o.iters)
         iters.append(r.report["iters"])
         X = Xn                                        # warm start for the next snapshot
     # warm starts converge faster than the cold first snapshot (P:609)
-    assert min(iters[2:]) < iters[0]
+    assert max(iters[1:]) < iters[0]
+
+
+@pytest.mark.parametrize("method", ["ofm_f1", "ofm_f2"])
+def test_c5_shaped_stream_unique_invariants(method):
+    """The c5-shaped stream (avg degree 16 revealed in 5 parts): early snapshots
+    have many small components, so -2 has multiplicity > k and span U_k is not
+    unique.  Compare subspaces where the gap allows it, else the unique parts."""
+    n, k = 3000, 8
+    X = x0_block(n, k, 79)
+    for ss, dd in snapshots(n, 8, 24000, 3.0, 5):
+        op, r, o, Xn = run_both(method, n, ss, dd, X, reorder=False)
+        A = dense_A(op)
+        w, U = np.linalg.eigh(A)
+        gap = w[k] - w[k - 1]
+        # Ritz values of the GPU features = lambda_1..k; invariant subspace
+        q, _ = np.linalg.qr(Xn)
+        H = q.T @ A @ q
+        assert np.allclose(np.linalg.eigvalsh(H), w[:k], atol=1e-8)
+        assert np.linalg.norm(A @ q - q @ H) <= 1e-7
+        # objective at its closed-form minimum, and equal to the oracle's
+        fstar = (np.sum(w[k:] ** 2) if method == "ofm_f1" else np.sum(w[:k]))
+        assert abs(r.report["objective"] - fstar) <= 1e-8 * max(1.0, abs(fstar))
+        assert abs(r.report["objective"] - o.objective) <= 1e-10 * max(1.0, abs(o.objective))
+        if gap > 1e-3:                                # unique subspace: compare features
+            assert sines(Xn, o.X).max() <= 1e-6
+            assert sines(Xn, U[:, :k]).max() <= 1e-6
+        X = Xn
+    assert fro2_A(op) > 0
