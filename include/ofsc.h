@@ -210,7 +210,8 @@ ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const
 ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void* d_Z,
                              int64_t ldz, void* d_Y, int64_t ldy, ofsc_stream stream);
 
-/* Kernel-level hook of the fused SpMM + Gram step: Y = A Z (local rows) and
+/* Kernel-level hook of the SpMM + Gram step (the SpMM kernel C2a, then the
+ * TMA-streamed DMMA Gram kernel C2b): Y = A Z (local rows) and
  * the k x k fp64 Grams d_grams[0..3] = Z^T Z, Z^T X, Z^T Y, X^T Y (row-major,
  * 4 consecutive k x k blocks, summed over all ranks).  Z: n x ldz (all rows),
  * X: local rows x ldx. */

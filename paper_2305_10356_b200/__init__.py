@@ -403,7 +403,7 @@ class Graph:
         return Y
 
     def apply_gram(self, Z, X, stream=None):
-        """Fused SpMM + Gram hook: Y = A Z and (Z^T Z, Z^T X, Z^T Y, X^T Y)."""
+        """SpMM + Gram hook (C2a then C2b): Y = A Z and (Z^T Z, Z^T X, Z^T Y, X^T Y)."""
         torch = _torch()
         Z, X = _dev2d(Z), _dev2d(X)
         k = Z.shape[1]

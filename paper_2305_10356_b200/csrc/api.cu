@@ -709,17 +709,40 @@ ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void*
     OFSC_REQUIRE(g && d_Z && d_Y && k >= 1 && ldz >= k && ldy >= k, OFSC_ERR_ARG, "bad apply args");
     OFSC_REQUIRE(dt == OFSC_F64 || dt == OFSC_F32, OFSC_ERR_ARG, "bad dtype");
     cudaStream_t s = (cudaStream_t)stream;
-    if (g->p == 1 && !g->reordered) {
-      launch_spmm_plain(dt, k, g->n_local, 0, g->row_ptr, g->col, g->s_slot, g->s32_slot, d_Z, ldz,
-                        d_Y, ldy, s);
-    } else {
-      DBuf zs((size_t)g->ext_rows * k * esize(dt), s);
+    if (k > OFSC_MAX_K) {   // wider than the iteration's kernels: one thread per (row, column)
+      DBuf zs(g->p == 1 && !g->reordered ? 0 : (size_t)g->ext_rows * k * esize(dt), s);
       DBuf ys(g->user_perm() ? (size_t)std::max<int64_t>(g->n_local, 1) * k * esize(dt) : 0, s);
-      to_slots(g, dt, k, k, d_Z, ldz, zs.p, s);
+      const void* Z = d_Z;
+      int64_t lz = ldz;
+      if (zs.p) {
+        to_slots(g, dt, k, k, d_Z, ldz, zs.p, s);
+        Z = zs.p;
+        lz = k;
+      }
       launch_spmm_plain(dt, k, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
-                        zs.p, k, g->user_perm() ? ys.p : d_Y, g->user_perm() ? k : ldy, s);
+                        Z, lz, g->user_perm() ? ys.p : d_Y, g->user_perm() ? k : ldy, s);
       if (g->user_perm()) launch_copy_out(dt, k, k, g->n_local, ys.p, d_Y, ldy, g->user_perm(), s);
+      return;
     }
+    // the iteration's SpMM kernel (C2a: k_spmm, degree binning, s_j stream, and for
+    // p > 1 the split own-column / halo-column passes) on KP-padded copies
+    const int KP = padded_k(k);
+    const size_t es = esize(dt);
+    const int64_t nl = g->n_local;
+    DBuf zs((size_t)g->ext_rows * KP * es, s), ys(std::max<int64_t>(nl, 1) * KP * es, s),
+        ctr(4 * sizeof(unsigned long long), s);
+    to_slots(g, dt, k, KP, d_Z, ldz, zs.p, s);
+    if (g->p > 1) {
+      launch_spmm(dt, KP, nl, 0, g->row_ptr_loc, g->col_loc, g->s_slot, g->s32_slot, zs.p, ys.p,
+                  nullptr, s, nullptr, nullptr, ctr.as<unsigned long long>(), 1, &g->heavy_loc);
+      launch_spmm(dt, KP, nl, 0, g->row_ptr_rem, g->col_rem, g->s_slot, g->s32_slot, zs.p, ys.p,
+                  nullptr, s, nullptr, nullptr, ctr.as<unsigned long long>(), 2, &g->heavy_rem);
+    } else {
+      launch_spmm(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p, ys.p,
+                  nullptr, s, nullptr, nullptr, ctr.as<unsigned long long>(), 0, &g->heavy,
+                  dt == OFSC_F64 ? (const void*)g->sval : (const void*)g->sval32);
+    }
+    launch_copy_out(dt, k, KP, nl, ys.p, d_Y, ldy, g->user_perm(), s);
   });
 }
 
@@ -752,7 +775,7 @@ ofsc_status ofsc_graph_apply_gram(ofsc_graph g, ofsc_dtype dt, int32_t k, const 
                   nullptr, s, nullptr, nullptr, nullptr, 2, &g->heavy_rem);
       launch_gram_stream(dt, KP, nl, zown, xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s);
     } else {
-      launch_spmm_gram(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p,
+      launch_spmm_then_gram(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p,
                        xs.p, ys.p, p2.as<double>(), 0, nullptr, nb2, s, &g->heavy);
     }
     launch_reduce_partials(p4.as<double>(), nb, 2 * KP * KP, gr.as<double>(), s);
@@ -915,7 +938,7 @@ static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaSt
     Zg = w.Xg;
   }
   pr.ph(OFSC_PH_REFRESH, 3, [&] {
-    launch_spmm_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
+    launch_spmm_then_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
                      g->s32_slot, Zg, nullptr, w.AX, w.part_g2, 1, &p.ctl->stop, w.nb2, s,
                      &g->heavy);
     launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, p.M, s);  // M, W contiguous

@@ -116,8 +116,9 @@ void launch_update_x(ofsc_dtype dt, const IterParams& p, cudaStream_t s);
 // C4: V = -G + beta Vp, partial Grams Q = V^T V, P = V^T X.
 void launch_direction_gram(ofsc_dtype dt, const IterParams& p, int nblk, cudaStream_t s);
 struct HeavyRows;
-// C2: Y = A Z (Z gathered), partial Grams. mode 0: (Zown^T Y, Xown^T Y); mode 1: (Zown^T Zown, Zown^T Y)
-void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
+// C2: Y = A Z (Z gathered; C2a), then the partial Grams over the own rows (C2b, a
+// separate TMA-streamed DMMA kernel). mode 0: (Zown^T Y, Xown^T Y); mode 1: (Zown^T Zown, Zown^T Y)
+void launch_spmm_then_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       const int64_t* row_ptr, const int32_t* col, const double* s,
                       const float* s32, const void* Zg, const void* Xown, void* Y,
                       double* part, int mode, const int* stop, int nblk, cudaStream_t st,

@@ -1,15 +1,23 @@
-// C2: the SpMM + Gram step (eq:spmm P:440).
+// C2a: the SpMM of the SpMM + Gram step (eq:spmm P:440,
+// P:468-487).
 //
 //   Y_i = (A Z)_i = -Z_i - s_i * sum_{j in N(i)} s_j Z_j        (A = L - 2I)
 //
-// One warp (or a KP/2-lane group) per row gathers the neighbour rows of Z with
-// 16-byte vector loads (coalesced 2*KP*sizeof(T) bytes per neighbour), summing
-// in CSR (ascending column) order.  Row tiles of 32 rows are staged in shared
-// memory and the epilogue accumulates per-CTA partial Grams on the fp64 tensor
-// path (DmmaGram, mma.sync m8n8k4); a fixed-order reduction (kernels_rows.cu) finishes them, so
-// runs are bitwise reproducible.
-//   mode 0 (iteration):  T = Z^T Y, R' = X^T Y    (Z = V)
-//   mode 1 (refresh):    M = Z^T Z, W = Z^T Y     (Z = X)
+// A group of KP/4 lanes owns a row and gathers its neighbour rows of Z with
+// 16-byte vector loads (each load instruction covers a contiguous half row),
+// 8 neighbour rows in flight per group, summing in CSR (ascending column)
+// order; rows are handed out in order from a global counter so the gathered
+// window stays L2-resident on locality-ordered graphs.  The Grams of the step
+// are NOT formed here: they are computed by the TMA-streamed DMMA kernel C2b
+// (k_gram_stream_ws, kernels_stream.cu) right after, over the SpMM's output
+// (launch_spmm_then_gram).  A fused SpMM + Gram kernel was measured worse on
+// B200: the gathers need all 24 warps and the L1 of the SM as landing space
+// (c4 SpMM 5.20 ms at 3 CTAs/SM, 6.95 ms at 2, 12.8 ms at 1:
+// tools/spmm_occupancy.py, profiles/r02), so there are no registers or
+// shared memory left for DMMA accumulators without slowing the gathers by
+// more than C2b costs.
+//   mode 0 (iteration):  C2b T = Z^T Y, R' = X^T Y    (Z = V)
+//   mode 1 (refresh):    C2b M = Z^T Z, W = Z^T Y     (Z = X)
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -144,6 +152,16 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       a3 = p1.y;
     }
     int64_t e = beg;
+    if constexpr (PF == 2) {
+      // lane l prefetches (into L2) the whole row of neighbour beg + 8 + l: with the
+      // 8 rows the registers hold, up to 8 + LPR neighbour rows of this row are in flight
+      const int64_t qn = beg + 8 + l;
+      if (qn < end) {
+        const char* rp = (const char*)(Zg + (int64_t)__ldg(col + qn) * KP + c0);
+#pragma unroll
+        for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
+      }
+    }
     for (; e + 8 <= end; e += 8) {
       int c[8];
 #pragma unroll
@@ -151,7 +169,17 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
         if constexpr (HINT) c[u] = ldg1h(col + e + u, pf);
         else c[u] = __ldg(col + e + u);
       }
-      if constexpr (PF) {
+      if constexpr (PF == 2) {
+        // PF = 2: lanes 0..7 of the group prefetch the whole rows of neighbours
+        // e + 16 .. e + 23 (the row start covered e + 8 .. e + 23)
+        const int64_t qn = e + 16 + l;
+        if (e >= 8 && l < 8 && qn < end) {
+          const char* rp = (const char*)(Zg + (int64_t)__ldg(col + qn) * KP + c0);
+#pragma unroll
+          for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
+        }
+      }
+      if constexpr (PF == 1) {
         // PF = 1: the next batch's neighbour rows are prefetched into L2 (no register
         // destination), so twice as many rows are in flight as registers hold
         if (e + 16 <= end) {
@@ -521,7 +549,10 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   if (phase) cw = KP;                       // split (multi-GPU) passes use whole rows
   if (KP % cw) cw = KP;
   const int passes = KP / cw;
-  const int pfe = env_int("OFSC_SPMM_PF", 0);   // experiment: L2 prefetch of the next batch
+  // L2 prefetch of neighbour rows beyond the 8 the registers hold (s_j-stream path of
+  // the large graphs): PF = 2 default, measured c4 SpMM 5.19 -> 5.08 ms and 5.34 -> 5.16
+  // (profiles/r02/occ2_c4.jsonl); 1 = next batch only (5.15 / 5.25); 0 = off
+  const int pfe = env_int("OFSC_SPMM_PF", 2);
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
     unsigned long long* c = ctr ? ctr + ps : nullptr;
@@ -542,7 +573,9 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
       if (sval && phase == 0 && cw == KPC && !hint) {
-        if (pfe) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 1) } else { OFSC_SPMM_LAUNCH_S(KPC, 0, 0, 1) }
+        if (pfe == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 2) }
+        else if (pfe == 1) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 1) }
+        else { OFSC_SPMM_LAUNCH_S(KPC, 0, 0, 1) }
       }
       else if (phase == 1) { OFSC_SPMM_LAUNCH_P(KPC, 0, 1) }
       else if (phase == 2) { OFSC_SPMM_LAUNCH_P(KPC, 0, 2) }
@@ -560,7 +593,7 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   if (hv) launch_heavy(dt, KP, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, phase, *heavy);
 }
 
-void launch_spmm_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
+void launch_spmm_then_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       const int64_t* row_ptr, const int32_t* col, const double* s,
                       const float* s32, const void* Zg, const void* Xown, void* Y, double* part,
                       int mode, const int* stop, int nblk, cudaStream_t st,

@@ -243,24 +243,6 @@ def test_p2_wide_kernels(k, method):
     assert np.allclose(r.history[:, :2], o.history[:, :2], rtol=1e-9, atol=0)
 
 
-def test_full_size_c4_two_iterations():
-    """BASELINE c4 at full size (N = 5M, E = 50M, k = 64) in the bench launch
-    configuration (LPA-reordered graph, OFM-f2): two whole iterations (the
-    second with the PR+ beta) against the oracle's Algorithm 2 on all rows."""
-    cfg = CONFIGS["c4"]
-    s, d, _ = config_graph(cfg)
-    op = build_operator(cfg.n, s, d)
-    g = ofsc.Graph(cfg.n, s, d, reorder=True)
-    X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)
-    o = run_ofm(op, "ofm_f2", X0, 2, refresh=0)
-    X, r = gpu_run(g, "ofm_f2", X0, 2)
-    assert r.report["iters"] == 2
-    assert [list(c) for c in r.codes] == [list(c) for c in o.codes]
-    assert np.max(np.abs(r.alphas - np.array(o.alphas))) <= 1e-12 * np.max(np.abs(o.alphas))
-    assert rel(X, o.X) <= 1e-12
-    g.close()
-
-
 def _degenerate_cases():
     rng = np.random.default_rng(21)
     cases = {

@@ -78,6 +78,42 @@ def test_spmm_f64(name, k):
     assert np.max(np.abs(Y - Yo)) <= 1e-14 * np.max(np.abs(Yo)) * 4
 
 
+@pytest.mark.parametrize("variant", ["sval", "sval_pf1", "sval_pf2", "heavy", "reorder",
+                                     "k80", "f32_sval"])
+def test_spmm_production_variants(variant, monkeypatch):
+    """ofsc_graph_apply runs the iteration's SpMM kernel (k_spmm) on KP-padded copies:
+    P0 parity of the variants the iteration uses -- the per-nonzero s_j stream (on by
+    default above 2e7 nonzeros, forced here), its L2-prefetch forms (OFSC_SPMM_PF),
+    degree binning of heavy rows (threshold forced low), the LPA-reordered operator,
+    fp32 -- and the plain kernel for k > 64."""
+    s, d, n = GRAPHS["c2"]()
+    op = build_operator(n, s, d)
+    k = 80 if variant == "k80" else 64
+    if variant.startswith("sval") or variant == "f32_sval":
+        monkeypatch.setenv("OFSC_SPMM_SVAL", "1")
+    if variant == "sval_pf1":
+        monkeypatch.setenv("OFSC_SPMM_PF", "1")
+    if variant == "sval_pf2":
+        monkeypatch.setenv("OFSC_SPMM_PF", "2")
+    if variant == "heavy":
+        monkeypatch.setenv("OFSC_HEAVY_THRESH", "24")
+    g = ofsc.Graph(n, s, d, reorder=(variant == "reorder"))
+    Z = np.random.default_rng(5).standard_normal((n, k))
+    if variant == "f32_sval":
+        Z32 = Z.astype(np.float32)
+        Y = g.apply(torch.from_numpy(Z32).cuda()).double().cpu().numpy()
+        Yo = oracle_apply_f32(op, Z32)
+        assert np.max(np.abs(Y - Yo)) <= 1e-6 * np.max(np.abs(Yo))
+        return
+    Y = g.apply(torch.from_numpy(Z).cuda()).cpu().numpy()
+    Yo = apply_A(op, Z)
+    assert np.max(np.abs(Y - Yo)) <= 4e-14 * np.max(np.abs(Yo))
+
+
+def oracle_apply_f32(op, Z32):
+    return apply_A(op, Z32.astype(np.float64), "f32")
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "ragged"])
 @pytest.mark.parametrize("k", [3, 11, 16, 32, 48, 64])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])

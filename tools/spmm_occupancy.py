@@ -16,8 +16,10 @@ cfg = CONFIGS[name]
 s, d, _ = config_graph(cfg)
 g = ofsc.Graph(cfg.n, s, d, reorder=True)
 X0 = torch.from_numpy(x0_block(cfg.n, cfg.k, cfg.seed_x0)).cuda()
-for ctas in (3, 2, 1):
-    for pf in (0, 1):
+grid = [(int(a), int(b)) for a, b in (x.split(":") for x in os.environ.get(
+    "GRID", "3:0,3:1,3:2,3:0,3:1,3:2,2:0,2:2").split(","))]
+for ctas, pf in grid:
+    if True:
         os.environ["OFSC_SPMM_CTAS_PER_SM"] = str(ctas)
         os.environ["OFSC_SPMM_PF"] = str(pf)
         X = X0.clone()
