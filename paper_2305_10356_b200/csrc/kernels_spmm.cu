@@ -119,20 +119,38 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
   // ctr == NULL: static interleaved assignment.
   const int CH = ch;
   int64_t round = 0;
-  while (true) {
-    int64_t base;
+  auto grab = [&]() -> int64_t {
     if (ctr) {
       unsigned long long b0 = 0;
       if (lane == 0) b0 = atomicAdd(ctr, (unsigned long long)CH);
-      base = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
-    } else {
-      base = (gw + round * nw) * CH;
-      ++round;
+      return (int64_t)__shfl_sync(0xffffffffu, b0, 0);
     }
+    const int64_t b = (gw + round * nw) * CH;
+    ++round;
+    return b;
+  };
+  // PF >= 3: the next chunk is grabbed one chunk early, so the rows a group will sum
+  // next (the next row pair of this chunk, or the first rows of the next chunk) can
+  // have their first LPR neighbour rows prefetched into L2 while this row is summed
+  int64_t base_next = grab();
+  while (true) {
+    const int64_t base = base_next;
     if (base >= n_local) break;
+    if constexpr (PF >= 3) base_next = grab();
 #pragma unroll 1
     for (int q = 0; q < CH; q += RPW) {
     const int64_t i = base + q + sub;
+    if constexpr (PF >= 3) {
+      const int64_t inext = (q + RPW < CH) ? i + RPW : base_next + sub;
+      if (active && inext < n_local) {
+        const int64_t nb = row_ptr[inext], ne = row_ptr[inext + 1];
+        if (nb + l < ne && ne - nb <= heavy) {
+          const char* rp = (const char*)(Zg + (int64_t)__ldg(col + nb + l) * KP + c0);
+#pragma unroll
+          for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
+        }
+      }
+    }
     if (!active || i >= n_local) continue;
     const int64_t beg = row_ptr[i], end = row_ptr[i + 1];
     if (end - beg > heavy) continue;               // uniform within the row group
@@ -152,7 +170,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       a3 = p1.y;
     }
     int64_t e = beg;
-    if constexpr (PF == 2) {
+    if constexpr (PF >= 2) {
       // lane l prefetches (into L2) the whole row of neighbour beg + 8 + l: with the
       // 8 rows the registers hold, up to 8 + LPR neighbour rows of this row are in flight
       const int64_t qn = beg + 8 + l;
@@ -169,8 +187,8 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
         if constexpr (HINT) c[u] = ldg1h(col + e + u, pf);
         else c[u] = __ldg(col + e + u);
       }
-      if constexpr (PF == 2) {
-        // PF = 2: lanes 0..7 of the group prefetch the whole rows of neighbours
+      if constexpr (PF >= 2) {
+        // PF >= 2: lanes 0..7 of the group prefetch the whole rows of neighbours
         // e + 16 .. e + 23 (the row start covered e + 8 .. e + 23)
         const int64_t qn = e + 16 + l;
         if (e >= 8 && l < 8 && qn < end) {
@@ -256,6 +274,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       *reinterpret_cast<V2*>(Y + i * KP + c0 + 2 * l + H2) = y1;
     }
     }
+    if constexpr (PF < 3) base_next = grab();
   }
 }
 
@@ -573,7 +592,8 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
       if (sval && phase == 0 && cw == KPC && !hint) {
-        if (pfe == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 2) }
+        if (pfe == 3) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 3) }
+        else if (pfe == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 2) }
         else if (pfe == 1) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 1) }
         else { OFSC_SPMM_LAUNCH_S(KPC, 0, 0, 1) }
       }
