@@ -740,7 +740,7 @@ ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void*
     } else {
       launch_spmm(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p, ys.p,
                   nullptr, s, nullptr, nullptr, ctr.as<unsigned long long>(), 0, &g->heavy,
-                  dt == OFSC_F64 ? (const void*)g->sval : (const void*)g->sval32);
+                  dt == OFSC_F64 ? (const void*)g->sval : (const void*)g->sval32, g->nnz_local);
     }
     launch_copy_out(dt, k, KP, nl, ys.p, d_Y, ldy, g->user_perm(), s);
   });
@@ -1009,7 +1009,8 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
                   w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
                   g->p == 1 ? g->cstart : nullptr, w.ctr, 0, &g->heavy,
                   g->p == 1 ? (dt == OFSC_F64 ? (const void*)g->sval : (const void*)g->sval32)
-                            : nullptr);
+                            : nullptr,
+                  g->nnz_local);
     });
   }
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {

@@ -149,7 +149,8 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
                  const int64_t* cstart = nullptr, unsigned long long* ctr = nullptr,
                  int phase = 0,    // 1: raw partial sums into Y; 2: continue from Y and finish
                  const HeavyRows* heavy = nullptr,
-                 const void* sval = nullptr);   // per-nonzero s_j (type of the run), or NULL
+                 const void* sval = nullptr,    // per-nonzero s_j (type of the run), or NULL
+                 int64_t nnz = -1);             // nonzeros of this CSR (L2-prefetch default), -1: unknown
 // per-nonzero neighbour scales s_j = s[col[e]] (streamed with the column ids by the
 // SpMM of large graphs instead of a random 8-byte gather per neighbour)
 void build_sval(int64_t nnz, const int32_t* col, const double* s, const float* s32, double** sval,

@@ -554,7 +554,7 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart,
                  unsigned long long* ctr, int phase, const HeavyRows* heavy,
-                 const void* sval) {
+                 const void* sval, int64_t nnz) {
   const bool hv = heavy && heavy->n_rows > 0;
   const int64_t hth = hv ? heavy->thresh : INT64_MAX;
   // cid / cstart: community layout of reordered graphs (p == 1), for the L2 hints.
@@ -568,10 +568,22 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   if (phase) cw = KP;                       // split (multi-GPU) passes use whole rows
   if (KP % cw) cw = KP;
   const int passes = KP / cw;
-  // L2 prefetch of neighbour rows beyond the 8 the registers hold (s_j-stream path of
-  // the large graphs): PF = 2 default, measured c4 SpMM 5.19 -> 5.08 ms and 5.34 -> 5.16
-  // (profiles/r02/occ2_c4.jsonl); 1 = next batch only (5.15 / 5.25); 0 = off
-  const int pfe = env_int("OFSC_SPMM_PF", 2);
+  // L2 prefetch of the neighbour rows beyond the 8 the registers hold (PF = 2: the
+  // row start prefetches neighbours 8..8+LPR-1, each batch the rows 16..23 ahead;
+  // PF = 1: next batch only; PF = 3: + the next row's first LPR neighbours).
+  // Measured (profiles/r02/spmm_pf_sweep.jsonl, SpMM ms, PF 0 / 1 / 2 / 3):
+  //   c4 5.30 / 5.19 / 4.99 / 6.10   c5 0.792 / 0.777 / 0.743 / 0.771
+  //   c6 1.70 / 1.85 / 1.78 / 2.01   c3 0.150 / 0.154 / 0.150 / 0.171
+  // i.e. it pays where the gathered operand is well beyond L2 and rows are short
+  // (c4, c5: most neighbour rows miss L2), and costs where the community windows
+  // stay L2-resident (c3) or long rows already keep many loads in flight (c6, avg
+  // degree 47).  Default: PF = 2 when N KP w > 256 MB and nnz / N <= 32, else 0;
+  // OFSC_SPMM_PF overrides (s_j-stream graphs), OFSC_SPMM_PF_SMALL (the others).
+  const int64_t gather_mb = n_local * KP * (dt == OFSC_F64 ? 8 : 4) >> 20;
+  const bool short_rows = n_local > 0 && nnz >= 0 && nnz <= 32 * n_local;
+  const int pf_auto = (gather_mb > 256 && short_rows) ? 2 : 0;
+  const int pfe = env_int("OFSC_SPMM_PF", pf_auto);
+  const int pfn = env_int("OFSC_SPMM_PF_SMALL", pf_auto);
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
     unsigned long long* c = ctr ? ctr + ps : nullptr;
@@ -599,6 +611,11 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
       }
       else if (phase == 1) { OFSC_SPMM_LAUNCH_P(KPC, 0, 1) }
       else if (phase == 2) { OFSC_SPMM_LAUNCH_P(KPC, 0, 2) }
+      else if (cw == KPC && !hint && pfn > 0) {     // gathered s_j + L2 prefetch
+        if (pfn == 3) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 0, 3) }
+        else if (pfn == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 0, 2) }
+        else { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 0, 1) }
+      }
       else if (cw == KPC) { OFSC_SPMM_LAUNCH(KPC) }
       else if (cw == 32) { if constexpr (KPC % 32 == 0) { OFSC_SPMM_LAUNCH(32) } }
       else { if constexpr (KPC % 16 == 0) { OFSC_SPMM_LAUNCH(16) } }

@@ -78,8 +78,8 @@ def test_spmm_f64(name, k):
     assert np.max(np.abs(Y - Yo)) <= 1e-14 * np.max(np.abs(Yo)) * 4
 
 
-@pytest.mark.parametrize("variant", ["sval", "sval_pf0", "sval_pf1", "sval_pf3", "heavy",
-                                     "reorder", "k80", "f32_sval"])
+@pytest.mark.parametrize("variant", ["sval", "sval_pf1", "sval_pf2", "sval_pf3", "plain_pf2",
+                                     "plain_pf3", "heavy", "reorder", "k80", "f32_sval"])
 def test_spmm_production_variants(variant, monkeypatch):
     """ofsc_graph_apply runs the iteration's SpMM kernel (k_spmm) on KP-padded copies:
     P0 parity of the variants the iteration uses -- the per-nonzero s_j stream (on by
@@ -91,9 +91,11 @@ def test_spmm_production_variants(variant, monkeypatch):
     k = 80 if variant == "k80" else 64
     if variant.startswith("sval") or variant == "f32_sval":
         monkeypatch.setenv("OFSC_SPMM_SVAL", "1")
-    for pf in ("0", "1", "3"):
+    for pf in ("1", "2", "3"):
         if variant == "sval_pf" + pf:
             monkeypatch.setenv("OFSC_SPMM_PF", pf)
+        if variant == "plain_pf" + pf:
+            monkeypatch.setenv("OFSC_SPMM_PF_SMALL", pf)
     if variant == "heavy":
         monkeypatch.setenv("OFSC_HEAVY_THRESH", "24")
     g = ofsc.Graph(n, s, d, reorder=(variant == "reorder"))
