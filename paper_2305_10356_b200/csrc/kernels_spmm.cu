@@ -80,18 +80,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-__device__ __forceinline__ double ldg_sv(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ float ldg_sv(const float* p, uint64_t pol) {
-  float v;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-  return v;
-}
-
-template <typename T, int KP, int CW, int HINT, int PHASE, int SV = 0, int PF = 0, int SH = 0>
+template <typename T, int KP, int CW, int HINT, int PHASE, int SV = 0, int PF = 0>
 __global__ void __launch_bounds__(kThreads, 3)
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
@@ -107,12 +96,10 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
   // the sums from Y over this CSR (the halo columns) and finish Y = -Z_i - s_i sum
   if (stop && *stop) return;
   uint64_t pf = 0, pn = 0;
-  if constexpr (HINT || SH) {
+  if constexpr (HINT) {
     pf = pol_evict_first();
     pn = pol_evict_normal();
   }
-  // SH = 1: the read-once streams (column ids, per-nonzero s_j) are loaded with an L2
-  // evict_first policy, so they do not displace the community's neighbour rows
   using V2 = typename Vec2<T>::type;
   constexpr int LPR = CW / 4;
   constexpr int RPW = 32 / LPR;
@@ -197,7 +184,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       int c[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if constexpr (HINT || SH) c[u] = ldg1h(col + e + u, pf);
+        if constexpr (HINT) c[u] = ldg1h(col + e + u, pf);
         else c[u] = __ldg(col + e + u);
       }
       if constexpr (PF >= 2) {
@@ -236,8 +223,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
           z0[u] = __ldg(reinterpret_cast<const V2*>(zr));
           z1[u] = __ldg(reinterpret_cast<const V2*>(zr + H2));
         }
-        if constexpr (SV && SH) sv[u] = ldg_sv(sval + e + u, pf);
-        else if constexpr (SV) sv[u] = __ldg(sval + e + u);
+        if constexpr (SV) sv[u] = __ldg(sval + e + u);
         else if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
         else sv[u] = (T)__ldg(s32 + c[u]);
       }
@@ -598,21 +584,19 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   const int pf_auto = (gather_mb > 256 && short_rows) ? 2 : 0;
   const int pfe = env_int("OFSC_SPMM_PF", pf_auto);
   const int pfn = env_int("OFSC_SPMM_PF_SMALL", pf_auto);
-  const int sh = env_int("OFSC_SPMM_STREAM_HINT", 0);   // experiment (s_j-stream path, PF = 2)
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
     unsigned long long* c = ctr ? ctr + ps : nullptr;
     const int c0 = ps * cw;
-#define OFSC_SPMM_LAUNCH_G(CWC, H, PH, SVV, PFF, SHH)                                           \
+#define OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, PFF)                                                \
     if (dt == OFSC_F64)                                                                         \
-      k_spmm<double, KPC, CWC, H, PH, SVV, PFF, SHH><<<nb, kThreads, 0, st>>>(n_local, own_off, \
+      k_spmm<double, KPC, CWC, H, PH, SVV, PFF><<<nb, kThreads, 0, st>>>(n_local, own_off,      \
           row_ptr, col, s, s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart,    \
           hth, (const double*)sval);                                                            \
     else                                                                                        \
-      k_spmm<float, KPC, CWC, H, PH, SVV, PFF, SHH><<<nb, kThreads, 0, st>>>(n_local, own_off,  \
+      k_spmm<float, KPC, CWC, H, PH, SVV, PFF><<<nb, kThreads, 0, st>>>(n_local, own_off,       \
           row_ptr, col, s, s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth, \
           (const float*)sval);
-#define OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, PFF) OFSC_SPMM_LAUNCH_G(CWC, H, PH, SVV, PFF, 0)
 #define OFSC_SPMM_LAUNCH_S(CWC, H, PH, SVV) OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, 0)
 #define OFSC_SPMM_LAUNCH_P(CWC, H, PH) OFSC_SPMM_LAUNCH_S(CWC, H, PH, 0)
 #define OFSC_SPMM_LAUNCH_H(CWC, H) OFSC_SPMM_LAUNCH_P(CWC, H, 0)
@@ -621,7 +605,6 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
     OFSC_DISPATCH_KP(KP, {
       if (sval && phase == 0 && cw == KPC && !hint) {
         if (pfe == 3) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 3) }
-        else if (pfe == 2 && sh) { OFSC_SPMM_LAUNCH_G(KPC, 0, 0, 1, 2, 1) }
         else if (pfe == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 2) }
         else if (pfe == 1) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 1) }
         else { OFSC_SPMM_LAUNCH_S(KPC, 0, 0, 1) }
@@ -642,7 +625,6 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #undef OFSC_SPMM_LAUNCH_P
 #undef OFSC_SPMM_LAUNCH_S
 #undef OFSC_SPMM_LAUNCH_F
-#undef OFSC_SPMM_LAUNCH_G
     OFSC_LAUNCH_CHECK();
   }
   if (hv) launch_heavy(dt, KP, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, phase, *heavy);
