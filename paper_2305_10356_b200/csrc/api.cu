@@ -148,8 +148,7 @@ struct ofsc_graph_s {
   int32_t* cid = nullptr;          // community of each internal row (reordered graphs)
   int64_t* cstart = nullptr;       // community start rows [n_comm + 1]
   HeavyRows heavy, heavy_loc, heavy_rem;  // power-law rows split into chunks (SpMM binning)
-  double* sval = nullptr;          // per-nonzero s_j (p == 1, large graphs; build_sval)
-  float* sval32 = nullptr;
+  SvalStream svs;                  // neighbour-scale stream of the SpMM (p == 1, large graphs)
   bool reordered = false;
   ofsc_graph_info info{};
   Workspace ws;
@@ -307,8 +306,7 @@ static void graph_free(ofsc_graph g) {
   g->heavy.release();
   g->heavy_loc.release();
   g->heavy_rem.release();
-  dfree(g->sval);
-  dfree(g->sval32);
+  g->svs.release();
 }
 
 ofsc_status ofsc_graph_build(ofsc_comm comm, int64_t n, int64_t m, const int64_t* src,
@@ -471,7 +469,9 @@ ofsc_status ofsc_graph_build_ex(ofsc_comm comm, int64_t n, int64_t m, const int6
     in.n_communities = n_comm;
     in.intra_edge_fraction = intra;
     build_heavy(g->row_ptr, g->n_local, g->heavy, s);
-    if (p == 1) build_sval(g->nnz_local, g->col, g->s_slot, g->s32_slot, &g->sval, &g->sval32, s);
+    if (p == 1)
+      build_sval(n, g->nnz_local, g->row_ptr, g->col, g->s_slot, g->s32_slot, in.max_degree,
+                 g->svs, s);
     in.halo_rows = g->ext_rows - g->n_local;
     in.send_rows = g->total_send;
     trace_point("graph_build: done", s);
@@ -535,7 +535,7 @@ ofsc_status ofsc_graph_append(ofsc_graph g, int64_t m, const int64_t* src, const
     g->col = csr.col;
     scatter_slots(csr.s, n, g->s_slot, g->s32_slot, g->d_begins, 1, n, s);
     build_heavy(g->row_ptr, n, g->heavy, s);
-    build_sval(csr.nnz, g->col, g->s_slot, g->s32_slot, &g->sval, &g->sval32, s);
+    build_sval(n, csr.nnz, g->row_ptr, g->col, g->s_slot, g->s32_slot, csr.max_deg, g->svs, s);
     OFSC_CUDA(cudaStreamSynchronize(s));
     g->nnz_local = csr.nnz;
     ofsc_graph_info& in = g->info;
@@ -740,7 +740,7 @@ ofsc_status ofsc_graph_apply(ofsc_graph g, ofsc_dtype dt, int32_t k, const void*
     } else {
       launch_spmm(dt, KP, nl, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot, zs.p, ys.p,
                   nullptr, s, nullptr, nullptr, ctr.as<unsigned long long>(), 0, &g->heavy,
-                  dt == OFSC_F64 ? (const void*)g->sval : (const void*)g->sval32, g->nnz_local);
+                  &g->svs, g->nnz_local);
     }
     launch_copy_out(dt, k, KP, nl, ys.p, d_Y, ldy, g->user_perm(), s);
   });
@@ -1008,9 +1008,7 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
       launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
                   w.Vg, w.AV, &p.ctl->stop, s, g->p == 1 ? g->cid : nullptr,
                   g->p == 1 ? g->cstart : nullptr, w.ctr, 0, &g->heavy,
-                  g->p == 1 ? (dt == OFSC_F64 ? (const void*)g->sval : (const void*)g->sval32)
-                            : nullptr,
-                  g->nnz_local);
+                  g->p == 1 ? &g->svs : nullptr, g->nnz_local);
     });
   }
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {

@@ -132,6 +132,17 @@ void launch_spmm_then_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_o
 // heavy row's chunk partials in chunk order.
 constexpr int64_t kHeavyThresh = 256;   // r22 (KP = 16): SpMM 21.4 ms unsplit, 4.5 at 4096, 3.1 at 256
 constexpr int64_t kHeavyChunk = 512;
+// Neighbour scales s_j for the SpMM of large graphs (p == 1), instead of a random
+// 8-byte gather s[col[e]] per neighbour: mode 1 streams s_j per nonzero (sval[nnz]);
+// mode 2 packs the column's node degree into the column stream (colpack[e] = col |
+// deg << 23) and reads s_j from a per-degree table (sval[max_deg + 1]).
+struct SvalStream {
+  int mode = 0;
+  double* sval = nullptr;
+  float* sval32 = nullptr;
+  int32_t* colpack = nullptr;
+  void release();
+};
 struct HeavyRows {
   int64_t thresh = INT64_MAX;      // rows with deg > thresh are heavy
   int64_t n_rows = 0, n_chunks = 0;
@@ -149,12 +160,11 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
                  const int64_t* cstart = nullptr, unsigned long long* ctr = nullptr,
                  int phase = 0,    // 1: raw partial sums into Y; 2: continue from Y and finish
                  const HeavyRows* heavy = nullptr,
-                 const void* sval = nullptr,    // per-nonzero s_j (type of the run), or NULL
+                 const SvalStream* svs = nullptr,   // neighbour-scale stream (p == 1), or NULL
                  int64_t nnz = -1);             // nonzeros of this CSR (L2-prefetch default), -1: unknown
-// per-nonzero neighbour scales s_j = s[col[e]] (streamed with the column ids by the
-// SpMM of large graphs instead of a random 8-byte gather per neighbour)
-void build_sval(int64_t nnz, const int32_t* col, const double* s, const float* s32, double** sval,
-                float** sval32, cudaStream_t st);
+void build_sval(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                const double* s, const float* s32, int64_t max_deg, SvalStream& out,
+                cudaStream_t st);
 constexpr int kSpmmChunk = 8;  // rows per dynamic work grab of the SpMM
 // C2b: TMA-streamed Gram pair over own rows (mode 0: Z^T Y, X^T Y; mode 1: Z^T Z, Z^T Y)
 int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n);

@@ -76,6 +76,17 @@ __device__ __forceinline__ void stg2h(float* p, float2 v, uint64_t pol) {
                "l"(pol));
 }
 
+// SV = 2: the column stream holds (column id | degree of the column's node << 23)
+// and s_j is read from a per-degree table (sval = table[max_deg + 1]), so one 4-byte
+// stream replaces the column ids AND the 8-byte per-nonzero s_j stream
+constexpr int kPackShift = 23;
+constexpr int kPackMask = (1 << kPackShift) - 1;
+template <int SV>
+__device__ __forceinline__ int col_id(int raw) {
+  if constexpr (SV == 2) return raw & kPackMask;
+  else return raw;
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -145,7 +156,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       if (active && inext < n_local) {
         const int64_t nb = row_ptr[inext], ne = row_ptr[inext + 1];
         if (nb + l < ne && ne - nb <= heavy) {
-          const char* rp = (const char*)(Zg + (int64_t)__ldg(col + nb + l) * KP + c0);
+          const char* rp = (const char*)(Zg + (int64_t)col_id<SV>(__ldg(col + nb + l)) * KP + c0);
 #pragma unroll
           for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
         }
@@ -175,24 +186,29 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       // 8 rows the registers hold, up to 8 + LPR neighbour rows of this row are in flight
       const int64_t qn = beg + 8 + l;
       if (qn < end) {
-        const char* rp = (const char*)(Zg + (int64_t)__ldg(col + qn) * KP + c0);
+        const char* rp = (const char*)(Zg + (int64_t)col_id<SV>(__ldg(col + qn)) * KP + c0);
 #pragma unroll
         for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
       }
     }
     for (; e + 8 <= end; e += 8) {
       int c[8];
+      int dg[SV == 2 ? 8 : 1];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if constexpr (HINT) c[u] = ldg1h(col + e + u, pf);
         else c[u] = __ldg(col + e + u);
+        if constexpr (SV == 2) {
+          dg[u] = (int)((unsigned)c[u] >> kPackShift);
+          c[u] &= kPackMask;
+        }
       }
       if constexpr (PF >= 2) {
         // PF >= 2: lanes 0..7 of the group prefetch the whole rows of neighbours
         // e + 16 .. e + 23 (the row start covered e + 8 .. e + 23)
         const int64_t qn = e + 16 + l;
         if (e >= 8 && l < 8 && qn < end) {
-          const char* rp = (const char*)(Zg + (int64_t)__ldg(col + qn) * KP + c0);
+          const char* rp = (const char*)(Zg + (int64_t)col_id<SV>(__ldg(col + qn)) * KP + c0);
 #pragma unroll
           for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
         }
@@ -203,7 +219,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
         if (e + 16 <= end) {
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const int cn = __ldg(col + e + 8 + u);
+            const int cn = col_id<SV>(__ldg(col + e + 8 + u));
             prefetch_l2(zc + (int64_t)cn * KP);
             prefetch_l2(zc + (int64_t)cn * KP + H2);
           }
@@ -223,7 +239,8 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
           z0[u] = __ldg(reinterpret_cast<const V2*>(zr));
           z1[u] = __ldg(reinterpret_cast<const V2*>(zr + H2));
         }
-        if constexpr (SV) sv[u] = __ldg(sval + e + u);
+        if constexpr (SV == 2) sv[u] = __ldg(sval + dg[u]);
+        else if constexpr (SV) sv[u] = __ldg(sval + e + u);
         else if constexpr (sizeof(T) == 8) sv[u] = (T)__ldg(s + c[u]);
         else sv[u] = (T)__ldg(s32 + c[u]);
       }
@@ -236,12 +253,14 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       }
     }
     for (; e < end; ++e) {
-      const int c = __ldg(col + e);
+      const int raw = __ldg(col + e);
+      const int c = col_id<SV>(raw);
       const T* zr = zc + (int64_t)c * KP;
       const V2 z0 = __ldg(reinterpret_cast<const V2*>(zr));
       const V2 z1 = __ldg(reinterpret_cast<const V2*>(zr + H2));
       T sv;
-      if constexpr (SV) sv = __ldg(sval + e);
+      if constexpr (SV == 2) sv = __ldg(sval + ((unsigned)raw >> kPackShift));
+      else if constexpr (SV) sv = __ldg(sval + e);
       else if constexpr (sizeof(T) == 8) sv = (T)__ldg(s + c);
       else sv = (T)__ldg(s32 + c);
       a0 = fma(sv, z0.x, a0);
@@ -523,21 +542,68 @@ __global__ void k_gather_sval(int64_t nnz, const int32_t* col, const double* s, 
   }
 }
 
-void build_sval(int64_t nnz, const int32_t* col, const double* s, const float* s32, double** sval,
-                float** sval32, cudaStream_t st) {
-  if (*sval || *sval32) cudaDeviceSynchronize();   // pool frees below: no queued user left
-  dev_free(*sval);
-  dev_free(*sval32);
-  *sval = nullptr;
-  *sval32 = nullptr;
-  // auto: graphs whose gathers mostly miss L2 (measured c4: SpMM 5.6 -> 5.3 ms; on
-  // L2-resident c3 the extra stream costs 3 %): OFSC_SPMM_SVAL=1 forces it, 0 disables
-  const int mode = env_int("OFSC_SPMM_SVAL", -1);
-  if (nnz <= 0 || mode == 0 || (mode < 0 && nnz < 20000000)) return;
-  dev_alloc((void**)sval, nnz * sizeof(double), st);
-  dev_alloc((void**)sval32, nnz * sizeof(float), st);
-  k_gather_sval<<<num_sms() * 16, 256, 0, st>>>(nnz, col, s, s32, *sval, *sval32);
+// packed stream: colpack[e] = col[e] | deg(col[e]) << 23; tables tab[d] = s of any
+// node of degree d (every node of one degree has the same s bits: s = d^{-1/2} is a
+// function of d), so s_j = tab[deg_j] reproduces the s_j of the other streams exactly
+__global__ void k_pack_cols(int64_t nnz, const int32_t* col, const int64_t* row_ptr,
+                            int32_t* colpack) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = col[e];
+    const int64_t d = row_ptr[j + 1] - row_ptr[j];
+    colpack[e] = j | (int32_t)((uint32_t)d << kPackShift);
+  }
+}
+__global__ void k_deg_table(int64_t n, const int64_t* row_ptr, const double* s, const float* s32,
+                            double* tab, float* tab32) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = row_ptr[i + 1] - row_ptr[i];
+    tab[d] = s[i];        // the same bits from every node of degree d
+    tab32[d] = s32[i];
+  }
+}
+
+void SvalStream::release() {
+  if (sval || sval32 || colpack) cudaDeviceSynchronize();   // pool frees: no queued user left
+  dev_free(sval);
+  dev_free(sval32);
+  dev_free(colpack);
+  sval = nullptr;
+  sval32 = nullptr;
+  colpack = nullptr;
+  mode = 0;
+}
+
+void build_sval(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                const double* s, const float* s32, int64_t max_deg, SvalStream& out,
+                cudaStream_t st) {
+  out.release();
+  // auto for graphs whose gathers mostly miss L2 (nnz >= 2e7; on L2-resident c3 an
+  // extra stream cost 3 %).  OFSC_SPMM_SVAL: 0 off (s_j gathered by column id),
+  // 1 per-nonzero s_j (8 extra bytes per nonzero; c4 SpMM 5.6 -> 5.3 ms in round 1),
+  // 2 packed (column | degree) stream + per-degree table (no extra bytes; needs
+  // n <= 2^23 and max degree < 2^9).  Default: 2 when it fits, else 1.
+  const int env = env_int("OFSC_SPMM_SVAL", -1);
+  const bool fits = n <= ((int64_t)1 << kPackShift) && max_deg < (1 << (32 - kPackShift));
+  int mode = env >= 0 ? env : (nnz >= 20000000 ? (fits ? 2 : 1) : 0);
+  if (mode == 2 && !fits) mode = 1;
+  if (nnz <= 0 || mode <= 0) return;
+  if (mode == 1) {
+    dev_alloc((void**)&out.sval, nnz * sizeof(double), st);
+    dev_alloc((void**)&out.sval32, nnz * sizeof(float), st);
+    k_gather_sval<<<num_sms() * 16, 256, 0, st>>>(nnz, col, s, s32, out.sval, out.sval32);
+  } else {
+    dev_alloc((void**)&out.colpack, nnz * sizeof(int32_t), st);
+    dev_alloc((void**)&out.sval, (max_deg + 1) * sizeof(double), st);
+    dev_alloc((void**)&out.sval32, (max_deg + 1) * sizeof(float), st);
+    OFSC_CUDA(cudaMemsetAsync(out.sval, 0, (max_deg + 1) * sizeof(double), st));
+    OFSC_CUDA(cudaMemsetAsync(out.sval32, 0, (max_deg + 1) * sizeof(float), st));
+    k_pack_cols<<<num_sms() * 16, 256, 0, st>>>(nnz, col, row_ptr, out.colpack);
+    k_deg_table<<<num_sms() * 8, 256, 0, st>>>(n, row_ptr, s, s32, out.sval, out.sval32);
+  }
   OFSC_LAUNCH_CHECK();
+  out.mode = mode;
 }
 
 // Default column window of the SpMM passes (see k_spmm).
@@ -554,7 +620,11 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
                  const int32_t* col, const double* s, const float* s32, const void* Zg, void* Y,
                  const int* stop, cudaStream_t st, const int32_t* cid, const int64_t* cstart,
                  unsigned long long* ctr, int phase, const HeavyRows* heavy,
-                 const void* sval, int64_t nnz) {
+                 const SvalStream* svs, int64_t nnz) {
+  const int svm = (svs && phase == 0) ? svs->mode : 0;
+  const void* sval = svm ? (dt == OFSC_F64 ? (const void*)svs->sval : (const void*)svs->sval32)
+                         : nullptr;
+  if (svm == 2) col = svs->colpack;
   const bool hv = heavy && heavy->n_rows > 0;
   const int64_t hth = hv ? heavy->thresh : INT64_MAX;
   // cid / cstart: community layout of reordered graphs (p == 1), for the L2 hints.
@@ -603,7 +673,11 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #define OFSC_SPMM_LAUNCH(CWC) \
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
-      if (sval && phase == 0 && cw == KPC && !hint) {
+      if (svm == 2 && cw == KPC && !hint) {
+        if (pfe == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 2, 2) }
+        else { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 2, 0) }
+      }
+      else if (svm == 1 && cw == KPC && !hint) {
         if (pfe == 3) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 3) }
         else if (pfe == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 2) }
         else if (pfe == 1) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 1, 1) }

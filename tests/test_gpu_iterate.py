@@ -290,13 +290,16 @@ def test_degenerate_graphs(case, method):
     g.close()
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("method", ["ofm_f2", "triofm_f1"])
-def test_streamed_neighbour_scales_bitwise(method, monkeypatch):
-    """The per-nonzero s_j stream (on by default for graphs with > 2e7 nonzeros,
-    forced here on c2) computes exactly the same sums as the gathered s_j."""
+def test_streamed_neighbour_scales_bitwise(method, mode, monkeypatch):
+    """The neighbour-scale streams (on by default for graphs with > 2e7 nonzeros,
+    forced here on c2): per-nonzero s_j (mode 1) and the packed (column | degree)
+    stream with a per-degree s table (mode 2) compute exactly the same sums as the
+    gathered s_j."""
     cfg, op, g, X0, _ = setup("c2")
     X_a, _ = gpu_run(g, method, X0, 10)
-    monkeypatch.setenv("OFSC_SPMM_SVAL", "1")
+    monkeypatch.setenv("OFSC_SPMM_SVAL", mode)
     s, d, _ = config_graph(cfg)
     g2 = ofsc.Graph(cfg.n, s, d)
     X_b, _ = gpu_run(g2, method, X0, 10)

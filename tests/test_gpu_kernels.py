@@ -78,8 +78,9 @@ def test_spmm_f64(name, k):
     assert np.max(np.abs(Y - Yo)) <= 1e-14 * np.max(np.abs(Yo)) * 4
 
 
-@pytest.mark.parametrize("variant", ["sval", "sval_pf1", "sval_pf2", "sval_pf3", "plain_pf2",
-                                     "plain_pf3", "heavy", "reorder", "k80", "f32_sval"])
+@pytest.mark.parametrize("variant", ["sval", "sval_pf1", "sval_pf2", "sval_pf3", "packed",
+                                     "packed_pf2", "plain_pf2", "plain_pf3", "heavy", "reorder",
+                                     "k80", "f32_sval", "f32_packed"])
 def test_spmm_production_variants(variant, monkeypatch):
     """ofsc_graph_apply runs the iteration's SpMM kernel (k_spmm) on KP-padded copies:
     P0 parity of the variants the iteration uses -- the per-nonzero s_j stream (on by
@@ -91,6 +92,10 @@ def test_spmm_production_variants(variant, monkeypatch):
     k = 80 if variant == "k80" else 64
     if variant.startswith("sval") or variant == "f32_sval":
         monkeypatch.setenv("OFSC_SPMM_SVAL", "1")
+    if variant.startswith("packed") or variant == "f32_packed":
+        monkeypatch.setenv("OFSC_SPMM_SVAL", "2")
+    if variant == "packed_pf2":
+        monkeypatch.setenv("OFSC_SPMM_PF", "2")
     for pf in ("1", "2", "3"):
         if variant == "sval_pf" + pf:
             monkeypatch.setenv("OFSC_SPMM_PF", pf)
@@ -100,7 +105,7 @@ def test_spmm_production_variants(variant, monkeypatch):
         monkeypatch.setenv("OFSC_HEAVY_THRESH", "24")
     g = ofsc.Graph(n, s, d, reorder=(variant == "reorder"))
     Z = np.random.default_rng(5).standard_normal((n, k))
-    if variant == "f32_sval":
+    if variant in ("f32_sval", "f32_packed"):
         Z32 = Z.astype(np.float32)
         Y = g.apply(torch.from_numpy(Z32).cuda()).double().cpu().numpy()
         Yo = oracle_apply_f32(op, Z32)
@@ -170,6 +175,38 @@ def test_line_search_kernel_matches_oracle(method, seed):
     D = np.diag(alpha)
     assert rel(Mo, M + P.T @ D + D @ P + D @ Q @ D) <= 1e-13
     assert rel(Wo, W + Rp @ D + D @ Rp.T + D @ T @ D) <= 1e-13
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_line_search_negative_leading_coefficient(seed):
+    """TriOFM-f2 columns whose cubic has c3 < 0: the device takes the
+    same root as the oracle (one real root: that root; three: the middle one, the
+    only local minimum of psi).  Grams are drawn directly (kernel-level hook) with
+    an indefinite T so that some c3_i < 0, including a k = 1 textbook case
+    (Q = 1, T = 1, P = M = W = 0, R' = r: c3 = -2, c2 = -3r, c1 = 2, c0 = 2r)."""
+    rng = np.random.default_rng(900 + seed)
+    if seed == 0:
+        k = 1
+        Q, T = np.ones((1, 1)), np.ones((1, 1))
+        P, M, W = np.zeros((1, 1)), np.zeros((1, 1)), np.zeros((1, 1))
+        Rp = np.full((1, 1), 0.1)
+    else:
+        k = 9
+        B = rng.standard_normal((40, k))
+        Q = B.T @ B / 40
+        S = rng.standard_normal((k, k))
+        T = (S + S.T) / 2
+        P, Rp = rng.standard_normal((k, k)) * 0.3, rng.standard_normal((k, k)) * 0.3
+        C = rng.standard_normal((30, k))
+        M = C.T @ C / 30
+        W = -(M + 0.1 * np.eye(k))
+    c3, c2, c1, c0 = cubic_coefficients("triofm_f2", Q, P, T, Rp, M, W)
+    assert np.any(np.asarray(c3) < 0)
+    alpha, codes, _, _ = ofsc.line_search("triofm_f2", Q, P, T, Rp, M, W)
+    want = [select_step(c3[i], c2[i], c1[i], c0[i]) for i in range(k)]
+    assert list(codes) == [w[1] for w in want]
+    wa = np.array([w[0] for w in want])
+    assert np.max(np.abs(alpha - wa)) <= 1e-11 * max(1.0, np.max(np.abs(wa)))
 
 
 def test_line_search_textbook_cubics_on_device():
