@@ -14,7 +14,7 @@ for name in (sys.argv[1:] or ["c4"]):
     s, d, _ = config_graph(cfg)
     X0 = torch.from_numpy(x0_block(cfg.n, cfg.k, cfg.seed_x0)).cuda()
     for rep in range(2):
-        for mode in ("0", "1", "2"):
+        for mode in os.environ.get("MODES", "0,1,2").split(","):
             os.environ["OFSC_SPMM_SVAL"] = mode
             g = ofsc.Graph(cfg.n, s, d, reorder=True)
             X = X0.clone()
