@@ -647,6 +647,14 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    if world > 1:
+        # torchrun sets OMP_NUM_THREADS=1 for every rank; rank 0 alone runs the oracle
+        # here, so give its BLAS the host cores it has at N = 1 (same oracle, same threads)
+        try:
+            from threadpoolctl import threadpool_limits
+            threadpool_limits(len(os.sched_getaffinity(0)))
+        except Exception:
+            pass
     cfg = CONFIGS[args.config]
     src, dst, _ = config_graph(cfg)
     X0 = x0_block(cfg.n, cfg.k, cfg.seed_x0)

@@ -583,10 +583,13 @@ void build_sval(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* c
   // extra stream cost 3 %).  OFSC_SPMM_SVAL: 0 off (s_j gathered by column id),
   // 1 per-nonzero s_j (8 extra bytes per nonzero; c4 SpMM 5.6 -> 5.3 ms in round 1),
   // 2 packed (column | degree) stream + per-degree table (no extra bytes; needs
-  // n <= 2^23 and max degree < 2^9).  Default: 2 when it fits, else 1.
+  // n <= 2^23 and max degree < 2^9).  Default: 2 when it fits and nnz >= 1e7,
+  // else 1 for nnz >= 2e7.
   const int env = env_int("OFSC_SPMM_SVAL", -1);
   const bool fits = n <= ((int64_t)1 << kPackShift) && max_deg < (1 << (32 - kPackShift));
-  int mode = env >= 0 ? env : (nnz >= 20000000 ? (fits ? 2 : 1) : 0);
+  // measured (profiles/r02/spmm_sval_ab*.jsonl): packed c4 -4 %, c6 -4 %, c5 (16M
+  // nonzeros) -2.5 %, neutral to +1 % on the L2-resident c1-c3
+  int mode = env >= 0 ? env : (fits ? (nnz >= 10000000 ? 2 : 0) : (nnz >= 20000000 ? 1 : 0));
   if (mode == 2 && !fits) mode = 1;
   if (nnz <= 0 || mode <= 0) return;
   if (mode == 1) {
