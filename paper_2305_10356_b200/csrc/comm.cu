@@ -18,8 +18,10 @@
 //    GPU); the arithmetic after the transport (the rank-order sum kernel, the
 //    split SpMM) is the NCCL path's, so the emulation tests the p > 1 schedule
 //    the multi-GPU run executes, bit for bit up to the transport.
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -35,16 +37,32 @@ struct LocalWorld {
   uint64_t gen = 0;
   std::vector<const void*> ptr;        // per rank: the buffer it posted for this collective
   std::vector<const int64_t*> off;     // per rank: its per-peer send offsets (rows)
+  bool broken = false;                 // a rank timed out: every later collective fails
+  // Every rank must reach the barrier from its own host thread; a rank that never
+  // arrives (a caller driving all ranks from one thread, or a rank that failed
+  // outside a collective) would hang the others, so the wait is bounded
+  // (OFSC_LOCAL_WORLD_TIMEOUT_S, default 600 s) and then fails with OFSC_ERR_STATE.
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    OFSC_REQUIRE(!broken, OFSC_ERR_STATE, "local world broken by an earlier timed-out collective");
     const uint64_t g = gen;
     if (++arrived == p) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return gen != g; });
+      return;
     }
+    const char* e = getenv("OFSC_LOCAL_WORLD_TIMEOUT_S");
+    const double limit = (e && *e) ? atof(e) : 600.0;
+    if (!cv.wait_for(lk, std::chrono::duration<double>(limit),
+                     [&] { return gen != g || broken; })) {
+      broken = true;
+      cv.notify_all();
+      throw Error{OFSC_ERR_STATE, "local world: a rank did not reach a collective within "
+                                  "OFSC_LOCAL_WORLD_TIMEOUT_S (each rank needs its own host "
+                                  "thread and the same sequence of calls)"};
+    }
+    OFSC_REQUIRE(!broken, OFSC_ERR_STATE, "local world broken by a timed-out collective");
   }
 };
 

@@ -193,3 +193,30 @@ def test_p5_spectral_cluster_end_to_end():
     assert rel(F, F1) <= 1e-9
     ari, _ = ofsc.scores(labels, l1)
     assert ari >= 0.999
+
+
+def test_local_world_missing_rank_fails_instead_of_hanging(monkeypatch):
+    """A rank that never reaches a collective (here rank 1 makes no call) must not
+    hang the others forever: the barrier wait is bounded (OFSC_LOCAL_WORLD_TIMEOUT_S)
+    and the call fails with OFSC_ERR_STATE; the world stays failed afterwards."""
+    monkeypatch.setenv("OFSC_LOCAL_WORLD_TIMEOUT_S", "2")
+    cfg, s, d, lab, op, X0 = c2()
+    Y = torch.from_numpy(np.ascontiguousarray(X0[:1000])).cuda()
+    world = ofsc.LocalWorld(2)
+
+    def rank_fn(r, comm):
+        if r == 1:
+            return None
+        C = Y[:4].clone().contiguous()
+        with pytest.raises(ofsc.OfscError) as e:
+            ofsc.kmeans(Y, C, 5, comm=comm)
+        assert e.value.status == 7
+        with pytest.raises(ofsc.OfscError):
+            ofsc.kmeans(Y, C, 5, comm=comm)
+        return "failed as expected"
+
+    try:
+        out = world.run(rank_fn, timeout=120)
+    finally:
+        world.close()
+    assert out[0] == "failed as expected"

@@ -1,4 +1,5 @@
 """C3 (update + direction) ms per launch: k_update_direction vs _v2 (OFSC_C3_V2),
+# NOTE: the OFSC_C3_V2 variant this script compared was removed after the measurement (profiles/r02/c3_v2_ab.jsonl).
 all four methods at the given configs; checksums must be identical (same bits)."""
 import json
 import os
