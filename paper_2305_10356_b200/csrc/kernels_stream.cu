@@ -152,6 +152,10 @@ k_update_direction(IterParams p, int apply_update) {
       double a1[2][2] = {{0, 0}, {0, 0}}, a2[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
+        // TriOFM: triu(M), triu(W) vanish below the diagonal, so the k-steps whose rows
+        // j = 4kk..4kk+3 all exceed this warp's columns 8cb..8cb+7 contribute exact
+        // zeros: skipped (warp-uniform), half of the products on average
+        if (TRI && 4 * kk > 8 * cb + 7) continue;
 #pragma unroll
         for (int rb = 0; rb < 2; ++rb) {
           const int o = (rb * 8 + gid) * LD + 4 * kk + tig;
