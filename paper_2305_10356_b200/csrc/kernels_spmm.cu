@@ -91,8 +91,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <typename T, int KP, int CW, int HINT, int PHASE, int SV = 0, int PF = 0>
-__global__ void __launch_bounds__(kThreads, 3)
+template <typename T, int KP, int CW, int HINT, int PHASE, int SV = 0, int PF = 0, int NIF = 8>
+__global__ void __launch_bounds__(kThreads, NIF >= 8 ? 3 : (NIF >= 6 ? 4 : 5))
 k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
        const int32_t* __restrict__ col, const double* __restrict__ s,
        const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ Y,
@@ -182,20 +182,20 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
     }
     int64_t e = beg;
     if constexpr (PF >= 2) {
-      // lane l prefetches (into L2) the whole row of neighbour beg + 8 + l: with the
-      // 8 rows the registers hold, up to 8 + LPR neighbour rows of this row are in flight
-      const int64_t qn = beg + 8 + l;
+      // lane l prefetches (into L2) the whole row of neighbour beg + NIF + l: with the
+      // NIF rows the registers hold, up to NIF + LPR neighbour rows of this row are in flight
+      const int64_t qn = beg + NIF + l;
       if (qn < end) {
         const char* rp = (const char*)(Zg + (int64_t)col_id<SV>(__ldg(col + qn)) * KP + c0);
 #pragma unroll
         for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
       }
     }
-    for (; e + 8 <= end; e += 8) {
-      int c[8];
-      int dg[SV == 2 ? 8 : 1];
+    for (; e + NIF <= end; e += NIF) {
+      int c[NIF];
+      int dg[SV == 2 ? NIF : 1];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NIF; ++u) {
         if constexpr (HINT) c[u] = ldg1h(col + e + u, pf);
         else c[u] = __ldg(col + e + u);
         if constexpr (SV == 2) {
@@ -204,10 +204,10 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
         }
       }
       if constexpr (PF >= 2) {
-        // PF >= 2: lanes 0..7 of the group prefetch the whole rows of neighbours
-        // e + 16 .. e + 23 (the row start covered e + 8 .. e + 23)
-        const int64_t qn = e + 16 + l;
-        if (e >= 8 && l < 8 && qn < end) {
+        // PF >= 2: lanes 0..NIF-1 of the group prefetch the whole rows of neighbours
+        // e + 2 NIF .. e + 3 NIF - 1 (the row start covered e + NIF .. e + NIF + LPR - 1)
+        const int64_t qn = e + 2 * NIF + l;
+        if (e >= NIF && l < NIF && qn < end) {
           const char* rp = (const char*)(Zg + (int64_t)col_id<SV>(__ldg(col + qn)) * KP + c0);
 #pragma unroll
           for (int b = 0; b < (int)(CW * sizeof(T)); b += 128) prefetch_l2(rp + b);
@@ -216,19 +216,19 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
       if constexpr (PF == 1) {
         // PF = 1: the next batch's neighbour rows are prefetched into L2 (no register
         // destination), so twice as many rows are in flight as registers hold
-        if (e + 16 <= end) {
+        if (e + 2 * NIF <= end) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int cn = col_id<SV>(__ldg(col + e + 8 + u));
+          for (int u = 0; u < NIF; ++u) {
+            const int cn = col_id<SV>(__ldg(col + e + NIF + u));
             prefetch_l2(zc + (int64_t)cn * KP);
             prefetch_l2(zc + (int64_t)cn * KP + H2);
           }
         }
       }
-      V2 z0[8], z1[8];
-      T sv[8];
+      V2 z0[NIF], z1[NIF];
+      T sv[NIF];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NIF; ++u) {
         if constexpr (HINT) {
           const T* zr = zc + (int64_t)c[u] * KP;
           const uint64_t pol = (c[u] >= lo && c[u] < hi) ? pn : pf;
@@ -245,7 +245,7 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
         else sv[u] = (T)__ldg(s32 + c[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NIF; ++u) {
         a0 = fma(sv[u], z0[u].x, a0);
         a1 = fma(sv[u], z0[u].y, a1);
         a2 = fma(sv[u], z1[u].x, a2);
@@ -657,26 +657,39 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   const int pf_auto = (gather_mb > 256 && short_rows) ? 2 : 0;
   const int pfe = env_int("OFSC_SPMM_PF", pf_auto);
   const int pfn = env_int("OFSC_SPMM_PF_SMALL", pf_auto);
+  // experiment: 6 neighbour rows in flight per row group at 4 CTAs per SM (64 registers)
+  const int nif = env_int("OFSC_SPMM_NIF", 8);
+  const int nb4 = (int)std::min<int64_t>((int64_t)num_sms() * 4, std::max<int64_t>(nb, 1) * 4 / 3 + 1);
+  const int nb5 = (int)std::min<int64_t>((int64_t)num_sms() * 5, std::max<int64_t>(nb, 1) * 5 / 3 + 1);
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
     unsigned long long* c = ctr ? ctr + ps : nullptr;
     const int c0 = ps * cw;
-#define OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, PFF)                                                \
+#define OFSC_SPMM_LAUNCH_N(CWC, H, PH, SVV, PFF, NN, NBB)                                       \
     if (dt == OFSC_F64)                                                                         \
-      k_spmm<double, KPC, CWC, H, PH, SVV, PFF><<<nb, kThreads, 0, st>>>(n_local, own_off,      \
+      k_spmm<double, KPC, CWC, H, PH, SVV, PFF, NN><<<NBB, kThreads, 0, st>>>(n_local, own_off, \
           row_ptr, col, s, s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart,    \
           hth, (const double*)sval);                                                            \
     else                                                                                        \
-      k_spmm<float, KPC, CWC, H, PH, SVV, PFF><<<nb, kThreads, 0, st>>>(n_local, own_off,       \
+      k_spmm<float, KPC, CWC, H, PH, SVV, PFF, NN><<<NBB, kThreads, 0, st>>>(n_local, own_off,  \
           row_ptr, col, s, s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth, \
           (const float*)sval);
+#define OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, PFF) OFSC_SPMM_LAUNCH_N(CWC, H, PH, SVV, PFF, 8, nb)
 #define OFSC_SPMM_LAUNCH_S(CWC, H, PH, SVV) OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, 0)
 #define OFSC_SPMM_LAUNCH_P(CWC, H, PH) OFSC_SPMM_LAUNCH_S(CWC, H, PH, 0)
 #define OFSC_SPMM_LAUNCH_H(CWC, H) OFSC_SPMM_LAUNCH_P(CWC, H, 0)
 #define OFSC_SPMM_LAUNCH(CWC) \
     if (hint) { OFSC_SPMM_LAUNCH_H(CWC, 1) } else { OFSC_SPMM_LAUNCH_H(CWC, 0) }
     OFSC_DISPATCH_KP(KP, {
-      if (svm == 2 && cw == KPC && !hint) {
+      if (svm == 2 && cw == KPC && !hint && nif == 6) {
+        if (pfe == 2) { OFSC_SPMM_LAUNCH_N(KPC, 0, 0, 2, 2, 6, nb4) }
+        else { OFSC_SPMM_LAUNCH_N(KPC, 0, 0, 2, 0, 6, nb4) }
+      }
+      else if (svm == 2 && cw == KPC && !hint && nif == 4) {
+        if (pfe == 2) { OFSC_SPMM_LAUNCH_N(KPC, 0, 0, 2, 2, 4, nb5) }
+        else { OFSC_SPMM_LAUNCH_N(KPC, 0, 0, 2, 0, 4, nb5) }
+      }
+      else if (svm == 2 && cw == KPC && !hint) {
         if (pfe == 2) { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 2, 2) }
         else { OFSC_SPMM_LAUNCH_F(KPC, 0, 0, 2, 0) }
       }
@@ -702,6 +715,7 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
 #undef OFSC_SPMM_LAUNCH_P
 #undef OFSC_SPMM_LAUNCH_S
 #undef OFSC_SPMM_LAUNCH_F
+#undef OFSC_SPMM_LAUNCH_N
     OFSC_LAUNCH_CHECK();
   }
   if (hv) launch_heavy(dt, KP, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, phase, *heavy);
