@@ -657,8 +657,11 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   const int pf_auto = (gather_mb > 256 && short_rows) ? 2 : 0;
   const int pfe = env_int("OFSC_SPMM_PF", pf_auto);
   const int pfn = env_int("OFSC_SPMM_PF_SMALL", pf_auto);
-  // experiment: 6 neighbour rows in flight per row group at 4 CTAs per SM (64 registers)
-  const int nif = env_int("OFSC_SPMM_NIF", 8);
+  // neighbour rows in flight per row group: 8 at 3 CTAs/SM (80 registers), 6 at 4 CTAs
+  // (64 registers: same loads in flight, a third more warps), 4 at 5 (spills).  Measured
+  // on the packed-stream path (profiles/r02/spmm_nif_ab.jsonl, SpMM ms, NIF 8 / 6 / 4):
+  // c4 4.72-4.91 / 4.68-4.79 / 5.12-5.18, c5 0.722 / 0.698 / 0.739, c6 neutral.
+  const int nif = env_int("OFSC_SPMM_NIF", svm == 2 ? 6 : 8);
   const int nb4 = (int)std::min<int64_t>((int64_t)num_sms() * 4, std::max<int64_t>(nb, 1) * 4 / 3 + 1);
   const int nb5 = (int)std::min<int64_t>((int64_t)num_sms() * 5, std::max<int64_t>(nb, 1) * 5 / 3 + 1);
   if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
