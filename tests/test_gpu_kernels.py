@@ -79,8 +79,9 @@ def test_spmm_f64(name, k):
 
 
 @pytest.mark.parametrize("variant", ["sval", "sval_pf1", "sval_pf2", "sval_pf3", "packed",
-                                     "packed_pf2", "plain_pf2", "plain_pf3", "heavy", "reorder",
-                                     "k80", "f32_sval", "f32_packed"])
+                                     "packed_pf2", "packed_nif8", "packed_nif4", "plain_pf2",
+                                     "plain_pf3", "heavy", "reorder", "k80", "f32_sval",
+                                     "f32_packed"])
 def test_spmm_production_variants(variant, monkeypatch):
     """ofsc_graph_apply runs the iteration's SpMM kernel (k_spmm) on KP-padded copies:
     P0 parity of the variants the iteration uses -- the per-nonzero s_j stream (on by
@@ -96,6 +97,9 @@ def test_spmm_production_variants(variant, monkeypatch):
         monkeypatch.setenv("OFSC_SPMM_SVAL", "2")
     if variant == "packed_pf2":
         monkeypatch.setenv("OFSC_SPMM_PF", "2")
+    if variant.startswith("packed_nif"):
+        monkeypatch.setenv("OFSC_SPMM_PF", "2")
+        monkeypatch.setenv("OFSC_SPMM_NIF", variant[-1])
     for pf in ("1", "2", "3"):
         if variant == "sval_pf" + pf:
             monkeypatch.setenv("OFSC_SPMM_PF", pf)
