@@ -16,7 +16,10 @@ Pins (tests/test_oracle_*.py, `-m "not gpu"`):
              bipartite), D^{1/2}1 eigenvector, spec in [-2,0], brute-force dense
   directions finite differences of f1/f2, k=1 reductions, theorem fixed points
   cubics     exact cubic fit through direct evaluations (A.1 of SURVEY)
-  roots      textbook cubics, brute-force bracketing, min-psi on a grid
+  roots      textbook cubics, brute-force bracketing (c3 > 0 and c3 < 0), min-psi on a grid
+  beta       G = Gp -> 0, orthogonal columns -> ratio of norms, PR+ clamp, zero
+             denominator (all exact), run_ofm's V_1 against the dense operator
+  sums       1024-row blocked pairwise column sums / Grams vs math.fsum
   iterate    monotone objective (OFM), theorem limits on bridged cliques,
              subspace vs dense eigh
   kmeans     brute-force optimal partition (n<=8), separated blobs, k=1
