@@ -223,6 +223,234 @@ k_update_direction(IterParams p, int apply_update) {
   }
 }
 
+// C3, warp-specialised: the same 8 compute warps and arithmetic as
+// k_update_direction (bitwise identical results), plus a 9th warp that owns the
+// TMA traffic.  The compute warps hand each stage over on mbarriers (phase A done:
+// X', AX' may be stored; phase C done: G may be stored) and never wait for the
+// stores' shared-memory reads -- the producer waits for those and refills the
+// stage, so the store-read latency leaves the compute warps' critical path.
+constexpr int kC3WsThreads = kThreads + 32;
+
+template <typename T, int KP, int METHOD>
+struct C3WsSmem {
+  static constexpr size_t base = C3Smem<T, KP, METHOD>::bytes;
+  static constexpr size_t bytes = base + 2 * kC3Stages * 8;          // + adone, cdone barriers
+};
+
+template <typename T, int KP, int METHOD>
+__global__ void __launch_bounds__(kC3WsThreads, 2)
+k_update_direction_ws(IterParams p, int apply_update) {
+  using S = C3Smem<T, KP, METHOD>;
+  constexpr int LD = S::LD;
+  constexpr int NS = kC3Stages;
+  constexpr bool TRI = (METHOD == OFSC_TRIOFM_F1 || METHOD == OFSC_TRIOFM_F2);
+  constexpr bool F1 = (METHOD == OFSC_OFM_F1 || METHOD == OFSC_TRIOFM_F1);
+  constexpr int NB = KP / 8;
+  constexpr int KS = KP / 4;
+  if (p.ctl->stop) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* Xp = (double*)smraw;
+  double* AXp = Xp + kSTR * LD;
+  unsigned char* stg = smraw + 2 * S::xp;
+  double* s_alpha = (double*)(stg + NS * S::stage);
+  uint64_t* full = (uint64_t*)(s_alpha + KP);
+  uint64_t* adone = full + NS;
+  uint64_t* cdone = adone + NS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int64_t ntiles = (p.n_local + kSTR - 1) / kSTR;
+  T* gX = (T*)p.X;
+  T* gAX = (T*)p.AX;
+  T* gG = (T*)p.G;
+  const T* gV = (const T*)p.V;
+  const T* gAV = (const T*)p.AV;
+  auto arr = [&](int st, int a) { return (T*)(stg + st * S::stage + a * S::arr); };
+  auto issue = [&](int st, int64_t tile) {
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, p.n_local - row0);
+    const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+    mbar_arrive_expect_tx(&full[st], (apply_update ? 5u : 3u) * b);
+    const int64_t off = row0 * KP;
+    bulk_g2s(arr(st, 0), gX + off, b, &full[st]);
+    bulk_g2s(arr(st, 1), gAX + off, b, &full[st]);
+    if (apply_update) {
+      bulk_g2s(arr(st, 2), gV + off, b, &full[st]);
+      bulk_g2s(arr(st, 3), gAV + off, b, &full[st]);
+    }
+    bulk_g2s(arr(st, 4), gG + off, b, &full[st]);
+  };
+  constexpr int NCW = kThreads / 32;               // compute warps
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&adone[s], NCW);
+      mbar_init(&cdone[s], NCW);
+    }
+    fence_barrier_init();
+  }
+  if (tid < KP) s_alpha[tid] = apply_update ? p.alpha[tid] : 0.0;
+  __syncthreads();
+  if (warp == NCW) {
+    // ---- producer warp: loads, stores, stage recycling (lane 0)
+    if (lane == 0) {
+      for (int s = 0; s < NS; ++s) {
+        const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+        if (tile < ntiles) issue(s, tile);
+      }
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % NS;
+        const uint32_t ph = (uint32_t)((it / NS) & 1);
+        const int64_t row0 = tile * kSTR;
+        const int rows = (int)imin64(kSTR, p.n_local - row0);
+        const uint32_t b = (uint32_t)rows * KP * sizeof(T);
+        mbar_wait(&adone[st], ph);
+        if (apply_update) {
+          bulk_s2g(gX + row0 * KP, arr(st, 0), b);
+          bulk_s2g(gAX + row0 * KP, arr(st, 1), b);
+          bulk_commit();
+        }
+        mbar_wait(&cdone[st], ph);
+        bulk_s2g(gG + row0 * KP, arr(st, 4), b);
+        bulk_commit();
+        const int64_t nxt = tile + (int64_t)NS * gridDim.x;
+        if (nxt < ntiles) {
+          bulk_wait_read_all();                 // stage st no longer read by the stores
+          issue(st, nxt);
+        }
+      }
+      bulk_wait_all();
+    }
+    return;
+  }
+  // ---- compute warps (k_update_direction's phases A, B, C)
+  const bool mma_warp = warp < NB;
+  const int cb = mma_warp ? warp : 0;
+  double bm[KS], bw[F1 ? 1 : KS];
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int j = 4 * kk + tig, c = cb * 8 + gid;
+    const bool keep = !TRI || j <= c;
+    bm[kk] = keep ? p.M[j * KP + c] : 0.0;
+    if (!F1) bw[kk] = keep ? p.W[j * KP + c] : 0.0;
+  }
+  double gg[2] = {0.0, 0.0}, dg[2] = {0.0, 0.0};
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % NS;
+    const int64_t row0 = tile * kSTR;
+    const int rows = (int)imin64(kSTR, p.n_local - row0);
+    mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
+    named_bar_sync(1, kThreads);                 // last tile's phase C done with Xp / AXp
+    T* sX = arr(st, 0);
+    T* sAX = arr(st, 1);
+    const T* sV = arr(st, 2);
+    const T* sAV = arr(st, 3);
+    T* sG = arr(st, 4);
+    for (int e = tid; e < kSTR * KP; e += kThreads) {
+      const int r = e / KP, c = e % KP;
+      double x = 0.0, ax = 0.0;
+      if (r < rows) {
+        x = (double)sX[e];
+        ax = (double)sAX[e];
+        if (apply_update) {
+          x = rndT<T>(x + s_alpha[c] * (double)sV[e]);
+          ax = rndT<T>(ax + s_alpha[c] * (double)sAV[e]);
+          sX[e] = (T)x;
+          sAX[e] = (T)ax;
+        }
+      }
+      Xp[r * LD + c] = x;
+      AXp[r * LD + c] = ax;
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, kThreads);
+    if (lane == 0) mbar_arrive(&adone[st]);
+    if (mma_warp) {
+      double a1[2][2] = {{0, 0}, {0, 0}}, a2[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        if (TRI && 4 * kk > 8 * cb + 7) continue;
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb) {
+          const int o = (rb * 8 + gid) * LD + 4 * kk + tig;
+          const double xa = Xp[o];
+          if (F1) {
+            dmma(a1[rb][0], a1[rb][1], xa, bm[kk]);
+          } else {
+            const double aa = AXp[o];
+            dmma(a1[rb][0], a1[rb][1], xa, bw[kk]);
+            dmma(a2[rb][0], a2[rb][1], aa, bm[kk]);
+          }
+        }
+      }
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb) {
+        const int r = rb * 8 + gid;
+        if (r < rows) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = cb * 8 + 2 * tig + h;
+            const double ax = AXp[r * LD + c];
+            double g;
+            if (METHOD == OFSC_OFM_F1) g = 4.0 * ax + 4.0 * a1[rb][h];
+            else if (METHOD == OFSC_TRIOFM_F1) g = ax + a1[rb][h];
+            else if (METHOD == OFSC_OFM_F2) g = 4.0 * ax - 2.0 * a1[rb][h] - 2.0 * a2[rb][h];
+            else g = 2.0 * ax - a2[rb][h] - a1[rb][h];
+            g = rndT<T>(g);
+            const double gp = (double)sG[r * KP + c];
+            sG[r * KP + c] = (T)g;
+            gg[h] = fma(g, g, gg[h]);
+            dg[h] = fma(g - gp, g, dg[h]);
+          }
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&cdone[st]);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      gg[h] += __shfl_xor_sync(0xffffffffu, gg[h], o);
+      dg[h] += __shfl_xor_sync(0xffffffffu, dg[h], o);
+    }
+  if (mma_warp && gid == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = cb * 8 + 2 * tig + h;
+      p.part_cols[(int64_t)blockIdx.x * 2 * KP + c] = gg[h];
+      p.part_cols[(int64_t)blockIdx.x * 2 * KP + KP + c] = dg[h];
+    }
+  }
+}
+
+template <typename T, int KP, int METHOD>
+static void launch_c3_ws(const IterParams& p, int apply, int nblk, cudaStream_t s) {
+  const size_t smem = C3WsSmem<T, KP, METHOD>::bytes;
+  auto kern = k_update_direction_ws<T, KP, METHOD>;
+  static bool set = false;
+  if (!set) {
+    OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = true;
+  }
+  kern<<<nblk, kC3WsThreads, smem, s>>>(p, apply);
+  OFSC_LAUNCH_CHECK();
+}
+
+// Default: the warp-specialised C3 for the f1 methods (one DMMA product per tile:
+// 86-88 registers, no spills; c4 OFM-f1 C3 3.30 -> 3.17 ms, 98 % of the HBM copy
+// peak), the single-role kernel for the f2 methods (two products: at the 9-warp
+// kernel's 96-register cap they spill, c4 OFM-f2 3.99 -> 4.37 ms;
+// profiles/r02/c3_ws_ab.jsonl).  OFSC_C3_WS = 0 / 1 forces either kernel.
+static int c3_ws(int method) {
+  const char* e = getenv("OFSC_C3_WS");
+  if (e && *e) return atoi(e);
+  return method == OFSC_OFM_F1 || method == OFSC_TRIOFM_F1;
+}
+
 template <typename T, int KP, int METHOD>
 static void launch_c3(const IterParams& p, int apply, int nblk, cudaStream_t s) {
   const size_t smem = C3Smem<T, KP, METHOD>::bytes;
@@ -259,6 +487,24 @@ int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n) {
 void launch_update_direction(ofsc_dtype dt, const IterParams& p, int apply_update, int nblk,
                              cudaStream_t s) {
   OFSC_DISPATCH_KP(p.KP, {
+    if (c3_ws(p.method)) {
+      if (dt == OFSC_F64) {
+        switch (p.method) {
+          case 0: launch_c3_ws<double, KPC, 0>(p, apply_update, nblk, s); break;
+          case 1: launch_c3_ws<double, KPC, 1>(p, apply_update, nblk, s); break;
+          case 2: launch_c3_ws<double, KPC, 2>(p, apply_update, nblk, s); break;
+          default: launch_c3_ws<double, KPC, 3>(p, apply_update, nblk, s); break;
+        }
+      } else {
+        switch (p.method) {
+          case 0: launch_c3_ws<float, KPC, 0>(p, apply_update, nblk, s); break;
+          case 1: launch_c3_ws<float, KPC, 1>(p, apply_update, nblk, s); break;
+          case 2: launch_c3_ws<float, KPC, 2>(p, apply_update, nblk, s); break;
+          default: launch_c3_ws<float, KPC, 3>(p, apply_update, nblk, s); break;
+        }
+      }
+      return;
+    }
     if (dt == OFSC_F64) {
       switch (p.method) {
         case 0: launch_c3<double, KPC, 0>(p, apply_update, nblk, s); break;
