@@ -320,3 +320,20 @@ def test_graph_launch_structure_is_transparent(method):
     Xb, rb = gpu_run(g, method, X0, 25, profile=True)
     assert np.array_equal(Xa, Xb)
     assert np.array_equal(ra.history, rb.history)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("method", METHODS)
+def test_c3_kernel_variants_bitwise(method, dtype, monkeypatch):
+    """C3's two kernels -- the single-role k_update_direction and the producer-warp
+    k_update_direction_ws (default for the f1 methods) -- compute the same bits
+    (same arithmetic, same order; only the TMA traffic is owned differently), on
+    the KP = 64 production width (reordered N = 20,011 graph)."""
+    op, g, X0 = setup_wide(64)
+    outs = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("OFSC_C3_WS", v)
+        X, r = gpu_run(g, method, X0, 10, dtype=dtype)
+        outs.append((X, r.history))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
