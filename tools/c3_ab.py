@@ -27,7 +27,8 @@ for name in (sys.argv[1:] or ["c4"]):
                 X2 = X0.clone()
                 r2 = ofsc.run(g, m, X2, 22, timing_skip=2)
                 print(json.dumps({"config": name, "method": m, VAR: int(v), "rep": rep,
-                                  "c3_ms": round(km[0] / 10, 4), "iter_ms": round(sum(km) / 10, 4),
+                                  "c3_ms": round(km[0] / 10, 4), "c4_ms": round(km[2] / 10, 4),
+                                  "c2b_ms": round(km[8] / 10, 4), "iter_ms": round(sum(km) / 10, 4),
                                   "graph_ms_per_iter": round(r2.report["timed_ms"] / 20, 4),
                                   "checksum": float(X.double().sum())}), flush=True)
     os.environ.pop(VAR, None)
