@@ -86,12 +86,18 @@ struct IterParams {
   double* part_g4;      // [nblk][2][KP][KP] (Q, P)
   double* part_g2;      // [nblk][2][KP][KP] (T, R')
   DevCtl* ctl;
+  unsigned long long* spmm_ctr;  // [4] SpMM row counters, zeroed by k_beta (PDL chain: no memset)
   double* hist;         // [T][4]
   double* hist_alpha;   // [T][KP]
   int* hist_code;       // [T][KP]
 };
 
 // ---- launchers (kernels_*.cu) ----
+// Programmatic dependent launch for the NEXT kernel launched by this host thread
+// (set by the iteration schedule before a launcher call; consumed by that call's
+// first kernel launch).  OFSC_PDL=0 disables it.
+void pdl_next(bool on);
+bool pdl_take();
 int grid_rows(int64_t n_rows, int blocks_per_sm);
 int num_sms();
 void keep_pool();    // default mempool keeps freed scratch (no per-build re-mapping)

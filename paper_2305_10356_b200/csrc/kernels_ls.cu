@@ -11,6 +11,7 @@
 #include <math_constants.h>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace ofsc {
 
@@ -150,9 +151,12 @@ __global__ void __launch_bounds__(256) k_beta(IterParams p, int nblk, int reduce
   __shared__ double red[3 * 256];
   __shared__ double s_gnorm;
   __shared__ int s_stop;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   const int tid = threadIdx.x, KP = p.KP, k = p.k;
   const int t = p.ctl->iter;
+  if (tid < 4 && p.spmm_ctr) p.spmm_ctr[tid] = 0ull;   // for this iteration's SpMM
   if (reduced) {
     if (tid < KP) {
       s_gg[tid] = p.colred[tid];
@@ -253,11 +257,12 @@ __global__ void __launch_bounds__(256) k_beta(IterParams p, int nblk, int reduce
 }
 
 void launch_beta(const IterParams& p, int nblk, int reduced, cudaStream_t st) {
-  k_beta<<<1, 256, 0, st>>>(p, nblk, reduced);
-  OFSC_LAUNCH_CHECK();
+  launch_k(k_beta, dim3(1), dim3(256), 0, st, pdl_take(), p, nblk, reduced);
 }
 
 __global__ void k_reduce_cols(IterParams p, int nblk) {
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   const int tid = threadIdx.x;
   if (tid < 2 * p.KP) {
@@ -468,6 +473,8 @@ __device__ void ls_core(int method, int k, int KP, const double* Q, const double
 __global__ void __launch_bounds__(256) k_linesearch(IterParams p) {
   __shared__ double red[11 * 256];
   __shared__ LsOut out;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   const int t = p.ctl->iter;
   const int KP = p.KP;
@@ -498,6 +505,8 @@ __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const d
   __shared__ double red[11 * 256];
   __shared__ LsOut out;
   __shared__ int s_last;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   const int KP = p.KP;
   const int per_blk = 2 * KP * KP;

@@ -234,6 +234,8 @@ int grid_rows(int64_t n_rows, int blocks_per_sm) {
 // ----------------------------------------------------------------------------
 template <typename T>
 __global__ void k_update_x(IterParams p) {
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   T* X = (T*)p.X;
   const T* V = (const T*)p.V;
@@ -243,6 +245,20 @@ __global__ void k_update_x(IterParams p) {
     const int c = (int)(e % p.KP);
     st1(X + e, rndT<T>(ld1(X + e) + p.alpha[c] * ld1(V + e)));
   }
+}
+
+static thread_local bool t_pdl = false;
+void pdl_next(bool on) {
+  static const bool enabled = [] {
+    const char* e = getenv("OFSC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  t_pdl = on && enabled;
+}
+bool pdl_take() {
+  const bool v = t_pdl;
+  t_pdl = false;
+  return v;
 }
 
 void launch_update_x(ofsc_dtype dt, const IterParams& p, cudaStream_t s) {

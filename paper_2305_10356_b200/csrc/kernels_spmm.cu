@@ -105,6 +105,8 @@ k_spmm(int64_t n_local, int64_t own_off, const int64_t* __restrict__ row_ptr,
   // PHASE 0: Y = A Z (whole rows); 1: Y <- raw neighbour sums over this CSR (the
   // local columns of a multi-GPU rank, while the halo is in flight); 2: continue
   // the sums from Y over this CSR (the halo columns) and finish Y = -Z_i - s_i sum
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (stop && *stop) return;
   uint64_t pf = 0, pn = 0;
   if constexpr (HINT) {
@@ -314,6 +316,8 @@ k_spmm_chunks(int64_t n_chunks, const int64_t* __restrict__ cbeg, const int64_t*
               const int32_t* __restrict__ col, const double* __restrict__ s,
               const float* __restrict__ s32, const T* __restrict__ Zg, T* __restrict__ scratch,
               const int* stop) {
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (stop && *stop) return;
   using V2 = typename Vec2<T>::type;
   constexpr int LPR = KP / 4;
@@ -378,6 +382,8 @@ __global__ void k_heavy_finish(int64_t n_heavy, int KP, const int32_t* __restric
                                int64_t own_off, const double* __restrict__ s,
                                const float* __restrict__ s32, const T* __restrict__ Zg,
                                T* __restrict__ Y, const int* stop) {
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (stop && *stop) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_heavy * KP;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -664,19 +670,23 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   const int nif = env_int("OFSC_SPMM_NIF", svm == 2 ? 6 : 8);
   const int nb4 = (int)std::min<int64_t>((int64_t)num_sms() * 4, std::max<int64_t>(nb, 1) * 4 / 3 + 1);
   const int nb5 = (int)std::min<int64_t>((int64_t)num_sms() * 5, std::max<int64_t>(nb, 1) * 5 / 3 + 1);
-  if (ctr) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
+  // a PDL launch (the iteration's SpMM right after C4) must not be preceded by a memset:
+  // there k_beta has zeroed the counters (IterParams::spmm_ctr)
+  const bool pdl_first = pdl_take();
+  if (ctr && !pdl_first) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
+    const bool pdl = pdl_first && ps == 0;
     unsigned long long* c = ctr ? ctr + ps : nullptr;
     const int c0 = ps * cw;
 #define OFSC_SPMM_LAUNCH_N(CWC, H, PH, SVV, PFF, NN, NBB)                                       \
     if (dt == OFSC_F64)                                                                         \
-      k_spmm<double, KPC, CWC, H, PH, SVV, PFF, NN><<<NBB, kThreads, 0, st>>>(n_local, own_off, \
-          row_ptr, col, s, s32, (const double*)Zg, (double*)Y, stop, c, ch, c0, cid, cstart,    \
-          hth, (const double*)sval);                                                            \
+      launch_k(k_spmm<double, KPC, CWC, H, PH, SVV, PFF, NN>, dim3(NBB), dim3(kThreads), 0, st, \
+               pdl, n_local, own_off, row_ptr, col, s, s32, (const double*)Zg, (double*)Y,       \
+               stop, c, ch, c0, cid, cstart, hth, (const double*)sval);                          \
     else                                                                                        \
-      k_spmm<float, KPC, CWC, H, PH, SVV, PFF, NN><<<NBB, kThreads, 0, st>>>(n_local, own_off,  \
-          row_ptr, col, s, s32, (const float*)Zg, (float*)Y, stop, c, ch, c0, cid, cstart, hth, \
-          (const float*)sval);
+      launch_k(k_spmm<float, KPC, CWC, H, PH, SVV, PFF, NN>, dim3(NBB), dim3(kThreads), 0, st,  \
+               pdl, n_local, own_off, row_ptr, col, s, s32, (const float*)Zg, (float*)Y, stop,   \
+               c, ch, c0, cid, cstart, hth, (const float*)sval);
 #define OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, PFF) OFSC_SPMM_LAUNCH_N(CWC, H, PH, SVV, PFF, 8, nb)
 #define OFSC_SPMM_LAUNCH_S(CWC, H, PH, SVV) OFSC_SPMM_LAUNCH_F(CWC, H, PH, SVV, 0)
 #define OFSC_SPMM_LAUNCH_P(CWC, H, PH) OFSC_SPMM_LAUNCH_S(CWC, H, PH, 0)

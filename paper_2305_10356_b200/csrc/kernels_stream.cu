@@ -58,6 +58,8 @@ k_update_direction(IterParams p, int apply_update) {
   constexpr bool F1 = (METHOD == OFSC_OFM_F1 || METHOD == OFSC_TRIOFM_F1);
   constexpr int NB = KP / 8;
   constexpr int KS = KP / 4;                     // DMMA k-steps
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* Xp = (double*)smraw;
@@ -247,6 +249,8 @@ k_update_direction_ws(IterParams p, int apply_update) {
   constexpr bool F1 = (METHOD == OFSC_OFM_F1 || METHOD == OFSC_TRIOFM_F1);
   constexpr int NB = KP / 8;
   constexpr int KS = KP / 4;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* Xp = (double*)smraw;
@@ -436,8 +440,7 @@ static void launch_c3_ws(const IterParams& p, int apply, int nblk, cudaStream_t 
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
-  kern<<<nblk, kC3WsThreads, smem, s>>>(p, apply);
-  OFSC_LAUNCH_CHECK();
+  launch_k(kern, dim3(nblk), dim3(kC3WsThreads), smem, s, pdl_take(), p, apply);
 }
 
 // Default: the warp-specialised C3 for the f1 methods (one DMMA product per tile:
@@ -460,8 +463,7 @@ static void launch_c3(const IterParams& p, int apply, int nblk, cudaStream_t s) 
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
-  kern<<<nblk, kThreads, smem, s>>>(p, apply);
-  OFSC_LAUNCH_CHECK();
+  launch_k(kern, dim3(nblk), dim3(kThreads), smem, s, pdl_take(), p, apply);
 }
 
 static int stream_grid(int64_t n_rows, size_t smem_bytes) {
@@ -539,6 +541,8 @@ template <typename T, int KP>
 __global__ void __launch_bounds__(kThreads, 2) k_direction_gram(IterParams p) {
   using S = C4Smem<T, KP>;
   constexpr int LD = S::LD;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* Vd = (double*)smraw;
@@ -623,8 +627,7 @@ static void launch_c4(const IterParams& p, int nblk, cudaStream_t s) {
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
-  kern<<<nblk, kThreads, smem, s>>>(p);
-  OFSC_LAUNCH_CHECK();
+  launch_k(kern, dim3(nblk), dim3(kThreads), smem, s, pdl_take(), p);
 }
 
 // C4, warp-specialised (KP = 48 by default, see c4_ws):
@@ -647,6 +650,8 @@ template <typename T, int KP>
 __global__ void __launch_bounds__(kGWS_THREADS, 1) k_direction_gram_ws(IterParams p) {
   using S = C4SmemWS<T, KP>;
   constexpr int LD = S::LD;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (p.ctl->stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* pads = (double*)smraw;                                       // [NP][2][kSTR][LD]
@@ -767,8 +772,7 @@ static void launch_c4_ws(const IterParams& p, int nblk, cudaStream_t s) {
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
-  kern<<<nblk, kGWS_THREADS, smem, s>>>(p);
-  OFSC_LAUNCH_CHECK();
+  launch_k(kern, dim3(nblk), dim3(kGWS_THREADS), smem, s, pdl_take(), p);
 }
 
 int c4_grid(ofsc_dtype dt, int KP, int64_t n) {
@@ -812,6 +816,8 @@ k_gram_stream(int64_t n_local, const T* __restrict__ gZ, const T* __restrict__ g
               const T* __restrict__ gY, double* __restrict__ part, const int* stop) {
   using S = GSmem<T, KP>;
   constexpr int LD = S::LD;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (stop && *stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* Zd = (double*)smraw;
@@ -891,6 +897,8 @@ k_gram_stream_ws(int64_t n_local, const T* __restrict__ gZ, const T* __restrict_
                  const T* __restrict__ gY, double* __restrict__ part, const int* stop) {
   using S = GSmemWS<T, KP>;
   constexpr int LD = S::LD;
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
   if (stop && *stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* pads = (double*)smraw;                                       // [NP][3][kSTR][LD]
@@ -986,8 +994,8 @@ static void launch_gs_ws(int64_t n, const void* Z, const void* X, const void* Y,
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
-  kern<<<nblk, kGWS_THREADS, smem, st>>>(n, (const T*)Z, (const T*)X, (const T*)Y, part, stop);
-  OFSC_LAUNCH_CHECK();
+  launch_k(kern, dim3(nblk), dim3(kGWS_THREADS), smem, st, pdl_take(), n, (const T*)Z,
+           (const T*)X, (const T*)Y, part, stop);
 }
 
 static int gs_ws() {   // warp-specialised C2b (default; OFSC_GS_WS=0: staging-copy kernel)
@@ -1009,8 +1017,8 @@ static void launch_gs(int64_t n, const void* Z, const void* X, const void* Y, do
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
-  kern<<<nblk, kThreads, smem, st>>>(n, (const T*)Z, (const T*)X, (const T*)Y, part, stop);
-  OFSC_LAUNCH_CHECK();
+  launch_k(kern, dim3(nblk), dim3(kThreads), smem, st, pdl_take(), n, (const T*)Z,
+           (const T*)X, (const T*)Y, part, stop);
 }
 
 int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n) {

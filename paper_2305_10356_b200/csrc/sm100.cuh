@@ -13,6 +13,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// ---- programmatic dependent launch (PDL) ----------------------------------------
+// A kernel launched with programmatic stream serialization may be scheduled while
+// its predecessor drains; pdl_wait() (griddepcontrol.wait) blocks until the
+// predecessor grid has completed and its memory is visible, so every kernel of the
+// PDL chain calls it before touching anything a predecessor wrote.  Without the
+// launch attribute both are no-ops.  pdl_trigger() lets the dependent be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- mbarrier --------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
