@@ -958,6 +958,15 @@ static bool overlap_exchange() {   // OFSC_NO_OVERLAP=1: exchange, then one SpMM
 
 // One iteration of Algorithm 2 (l.8-12), the R-mode schedule of DESIGN.md:
 // C3 -> beta -> C4 -> [all-gather V] -> C2 -> Gram reduce -> [all-reduce] -> line search.
+static bool pdl_ls() {   // OFSC_PDL_LS=0: the line-search kernel waits for C2b in full
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("OFSC_PDL_LS");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1;
+}
+
 static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool refresh,
                           cudaStream_t s, Prof& pr) {
   Workspace& w = g->ws;
@@ -1026,6 +1035,8 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
   if (fork_reduce) {
     // p == 1: C2b's partials reduced and the line search run by one kernel (its last CTA)
     OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_f1, 0));
+    // PDL edge from C2b (the joined Q/P reduction stays a full dependency)
+    pdl_next(pdl && pdl_ls());
     pr.ph(OFSC_PH_LINE_SEARCH, 1, [&] { launch_reduce_linesearch(p, w.part_g2, w.nb2, s); });
     return;
   }

@@ -539,8 +539,8 @@ __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const d
 
 void launch_reduce_linesearch(const IterParams& p, const double* part, int nblk, cudaStream_t st) {
   const int per_blk = 2 * p.KP * p.KP;
-  k_reduce_linesearch<<<(per_blk + 31) / 32, 256, 0, st>>>(p, part, nblk);
-  OFSC_LAUNCH_CHECK();
+  launch_k(k_reduce_linesearch, dim3((per_blk + 31) / 32), dim3(256), 0, st, pdl_take(), p, part,
+           nblk);
 }
 
 __global__ void __launch_bounds__(256) k_linesearch_hook(int method, int k, int KP,
