@@ -210,8 +210,39 @@ def nvlink_stats(info, kern, K, kp, es, world, max_over_ranks):
             "comm_ms_per_iter_profiled": round(comm_ms, 4),
             "achieved_gbs": round(gbs, 1) if gbs else None,
             "frac_of_900": round(gbs / 900.0, 4) if gbs else None,
+            "allgather_probe": allgather_probe(info["n"], kp, es, world, max_over_ranks),
             "note": "profiled pass runs exchange and SpMM back to back; the timed pass overlaps "
                     "the exchange with the own-column part of the SpMM"}
+
+
+def allgather_probe(n, kp, es, world, max_over_ranks, reps=5):
+    """The achievable NVLink rate at the c4 message size: torch's
+    all_gather_into_tensor of an (n / p) x KP block per rank, CUDA events, max over
+    ranks; bus bandwidth = (p - 1) / p x total bytes / time, per GPU."""
+    import torch
+    import torch.distributed as dist
+    rows = -(-n // world)
+    elems = rows * kp
+    dt = torch.float64 if es == 8 else torch.float32
+    src = torch.ones(elems, dtype=dt, device="cuda")
+    dst = torch.empty(elems * world, dtype=dt, device="cuda")
+    dist.all_gather_into_tensor(dst, src)          # warm-up / connect
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    a.record()
+    for _ in range(reps):
+        dist.all_gather_into_tensor(dst, src)
+    b.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / reps)
+    total = elems * world * es
+    busbw = (world - 1) / world * total / (ms / 1e3) / 1e9
+    del src, dst
+    torch.cuda.empty_cache()
+    return {"bytes_per_rank_in": int(elems * (world - 1) * es), "ms": round(ms, 4),
+            "bus_gbs": round(busbw, 1), "frac_of_900": round(busbw / 900.0, 4),
+            "frac_of_measured_770": round(busbw / 770.0, 4)}
 
 
 def load_gather_peak():
