@@ -38,7 +38,7 @@ def test_bench_line_contract():
         assert key in d, key
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
     assert d["unit"] == "it/s" and d["higher_is_better"] is True
-    assert abs(d["value"] - d["steps"] / (d["ms_per_step"] * d["steps"] / 1e3)) <= 1e-3 * d["value"]
+    assert abs(d["value"] - 1e3 / d["ms_per_step"]) <= 5e-3 * d["value"]   # rounding of ms_per_step
     r = d["roofline"]
     for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert key in r, key
