@@ -216,3 +216,15 @@ def test_c5_full_size_streaming_protocol():
         assert rel(Xg, o.X) <= 1e-12
         X = Xg                                            # warm start
     g.close()
+
+
+@pytest.mark.parametrize("method", ["ofm_f1", "triofm_f2"])
+def test_p2_c3_fp32(method):
+    """fp32 storage at c3 (N = 200k, k = 64): 10 iterations vs the precision-matched
+    oracle (P2 fp32 tolerance 1e-4)."""
+    cfg, op, g, X0 = setup("c3", True)
+    X0r = X0.astype(np.float32).astype(np.float64)
+    o = run_ofm(op, method, X0r, 10, refresh=0, precision="f32")
+    X, r = gpu_run(g, method, X0r, 10, dtype="f32")
+    assert r.report["iters"] == 10
+    assert rel(X, o.X) <= 1e-4
