@@ -1474,6 +1474,22 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
         gat(P > 1 ? (size_t)P * std::max(K * W, 3) * 8 : 0, s),
         lbd(fused ? (size_t)std::max<int64_t>(n_local, 1) * 8 : 8, s), dlt((size_t)K * 8, s),
         sep((size_t)K * 8, s);
+    // light steps (bounds first, sums by label changes; kernels_kmeans.cu): once at
+    // most 1/8 of the rows failed the previous step's bound tests (the light step
+    // assigns those by the direct form, without tensor cores).  S = running sums.
+    const bool light_ok = fused && kmeans_light_supported(dim, K);
+    const int nbl = light_ok ? kmeans_light_blocks(std::max<int64_t>(n_local, 1)) : 0;
+    DBuf ubd(light_ok ? (size_t)std::max<int64_t>(n_local, 1) * 8 : 8, s),
+        Ssum((size_t)K * W * 8, s), partl(light_ok ? (size_t)nbl * K * W * 8 : 8, s);
+    unsigned long long n_total = (unsigned long long)std::max<int64_t>(n_local, 0);
+    if (light_ok && comm_active(comm)) {
+      DBuf nt(8, s);
+      OFSC_CUDA(cudaMemcpyAsync(nt.p, &n_total, 8, cudaMemcpyHostToDevice, s));
+      comm_sum_u64(comm, nt.as<unsigned long long>(), 1, gat.as<unsigned long long>(), s);
+      OFSC_CUDA(cudaMemcpyAsync(&n_total, nt.p, 8, cudaMemcpyDeviceToHost, s));
+      OFSC_CUDA(cudaStreamSynchronize(s));
+    }
+    unsigned long long prev_fail = ~0ull;
     OFSC_CUDA(cudaMemsetAsync(d_labels, 0xff, std::max<int64_t>(n_local, 0) * sizeof(int32_t), s));
     // pinned counter readback, allocated once per host thread (cudaFreeHost would
     // synchronise the whole device, e.g. the feature download of spectral_cluster)
@@ -1501,11 +1517,17 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
         OFSC_CUDA(cudaEventCreate(&eb));
         OFSC_CUDA(cudaEventRecord(ea, s));
       }
-      if (n_local > 0 && fused)
+      const bool light = light_ok && it > 1 && !noskip && elkan && prev_fail * 8 <= n_total;
+      if (n_local > 0 && light)
+        launch_kmeans_light(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels, ubd.as<double>(),
+                            lbd.as<double>(), dlt.as<double>(), sep.as<double>(),
+                            chg.as<unsigned long long>(), partl.as<double>(), nbl, s);
+      else if (n_local > 0 && fused)
         launch_kmeans_step(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
                            chg.as<unsigned long long>(), pin.as<double>(), part.as<double>(),
                            lbd.as<double>(), it > 1 && !noskip ? dlt.as<double>() : nullptr,
-                           elkan ? sep.as<double>() : nullptr, nb, s);
+                           elkan ? sep.as<double>() : nullptr,
+                           light_ok ? ubd.as<double>() : nullptr, nb, s);
       else if (n_local > 0)
         launch_kmeans_assign(dt, n_local, dim, d_Y, ldy, K, d_centroids, d_labels,
                              chg.as<unsigned long long>(), pin.as<double>(), nb, s);
@@ -1523,26 +1545,50 @@ ofsc_status ofsc_kmeans(ofsc_comm comm, ofsc_dtype dt, int64_t n_local, int32_t 
         OFSC_CUDA(cudaEventElapsedTime(&ms, ea, eb));
         cudaEventDestroy(ea);
         cudaEventDestroy(eb);
-        fprintf(stderr, "[ofsc kmeans] step %d changes %llu skipped %llu product_blocks %llu ms %.3f\n",
-                it, h_chg[0], h_chg[1], h_chg[2], ms);
+        fprintf(stderr, "[ofsc kmeans] step %d changes %llu skipped %llu product_blocks %llu ms %.3f light %d\n",
+                it, h_chg[0], h_chg[1], h_chg[2], ms, light ? 1 : 0);
       }
       {
         double v;
         memcpy(&v, (const void*)&((volatile unsigned long long*)h_chg)[3], 8);
         inertia = v;
       }
-      if (it > 1 && ((volatile unsigned long long*)h_chg)[0] == 0) break;
-      if (n_local > 0 && !fused)
-        launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nbp, s);
-      else if (n_local == 0)
-        OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nbp * K * W * 8, s));
-      launch_reduce_partials(part.as<double>(), nbp, K * W, red.as<double>(), s);
-      if (comm_active(comm)) comm_sum_f64(comm, red.as<double>(), (size_t)K * W, gat.as<double>(), s);
+      const unsigned long long nchanged = ((volatile unsigned long long*)h_chg)[0];
+      const bool last = (it > 1 && nchanged == 0) || it == max_iters;
+      if (light && last) {
+        // the light step does not visit every row: the inertia of this (final)
+        // assignment comes from one pass with the centroids it used
+        if (n_local > 0)
+          launch_kmeans_inertia(dt, n_local, dim, d_Y, ldy, d_centroids, d_labels, pin.as<double>(),
+                                nb, s);
+        launch_reduce_partials(pin.as<double>(), nb, 1, tot.as<double>(), s);
+        if (comm_active(comm)) comm_sum_f64(comm, tot.as<double>(), 1, gat.as<double>(), s);
+        OFSC_CUDA(cudaMemcpyAsync(&inertia, tot.p, 8, cudaMemcpyDeviceToHost, s));
+        OFSC_CUDA(cudaStreamSynchronize(s));
+      }
+      {
+        const unsigned long long nsk = ((volatile unsigned long long*)h_chg)[1];
+        prev_fail = n_total > nsk ? n_total - nsk : 0;
+      }
+      if (it > 1 && nchanged == 0) break;
+      if (light) {
+        if (n_local == 0) OFSC_CUDA(cudaMemsetAsync(partl.p, 0, (size_t)nbl * K * W * 8, s));
+        launch_reduce_partials(partl.as<double>(), nbl, K * W, red.as<double>(), s);
+        if (comm_active(comm)) comm_sum_f64(comm, red.as<double>(), (size_t)K * W, gat.as<double>(), s);
+        launch_kmeans_accum(K * W, Ssum.as<double>(), red.as<double>(), s);
+      } else {
+        if (n_local > 0 && !fused)
+          launch_kmeans_partial(dt, n_local, dim, d_Y, ldy, K, d_labels, part.as<double>(), nbp, s);
+        else if (n_local == 0)
+          OFSC_CUDA(cudaMemsetAsync(part.p, 0, (size_t)nbp * K * W * 8, s));
+        launch_reduce_partials(part.as<double>(), nbp, K * W, Ssum.as<double>(), s);
+        if (comm_active(comm)) comm_sum_f64(comm, Ssum.as<double>(), (size_t)K * W, gat.as<double>(), s);
+      }
       if (fused) {
-        launch_kmeans_finish_delta(K, dim, red.as<double>(), d_centroids, dlt.as<double>(), s);
+        launch_kmeans_finish_delta(K, dim, Ssum.as<double>(), d_centroids, dlt.as<double>(), s);
         launch_kmeans_halfsep(K, dim, d_centroids, sep.as<double>(), s);
       }
-      else launch_kmeans_finish(K, dim, red.as<double>(), d_centroids, s);
+      else launch_kmeans_finish(K, dim, Ssum.as<double>(), d_centroids, s);
     }
     OFSC_CUDA(cudaStreamSynchronize(s));
     if (iters_out) *iters_out = std::min(it, max_iters);

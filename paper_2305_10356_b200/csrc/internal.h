@@ -233,7 +233,19 @@ int kmeans_step_blocks(int64_t n);
 void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                         const double* C, int* labels, unsigned long long* changes,
                         double* part_inertia, double* part, double* lbound, const double* delta,
-                        const double* sep, int nblk, cudaStream_t st);
+                        const double* sep, double* ubound, int nblk, cudaStream_t st);
+// light step (bounds first; Y read only by the rows that fail; sums by label changes):
+// part[b] = per-CTA (dS, dcnt); ubound/lbound carried from the previous step
+bool kmeans_light_supported(int dim, int K);
+int kmeans_light_blocks(int64_t n);
+void launch_kmeans_light(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                         const double* C, int* labels, double* ubound, double* lbound,
+                         const double* delta, const double* sep, unsigned long long* changes,
+                         double* part, int nblk, cudaStream_t st);
+void launch_kmeans_accum(int n, double* S, const double* dS, cudaStream_t st);
+void launch_kmeans_inertia(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy,
+                           const double* C, const int* labels, double* part, int nblk,
+                           cudaStream_t st);
 // sep[c] = half the distance of centroid c to its nearest other centroid (deflated)
 void launch_kmeans_halfsep(int K, int dim, const double* C, double* sep, cudaStream_t st);
 // fused path: C = means (empty keeps), delta[c] = ||C_new - C_old|| (dim <= 64)

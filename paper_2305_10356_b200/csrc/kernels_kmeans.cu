@@ -465,7 +465,7 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
               const double* __restrict__ C, int* __restrict__ labels,
               unsigned long long* changes, double* part_inertia, double* part,
               double* __restrict__ lbound, const double* __restrict__ delta,
-              const double* __restrict__ sep) {
+              const double* __restrict__ sep, double* __restrict__ ubound) {
   // DP: dim rounded up to a multiple of 16 (padding columns are zero)
   constexpr int TR = kKsRows;
   constexpr int PRE = TR * DP / kKmThreads;       // tile elements per thread
@@ -680,6 +680,7 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
       const int r = rrow, w = rw;
       int lab = old_lab;
       double dist = Da;
+      double uslack = 0.0;                         // absolute error of a score-based distance
       if (fmask) {
         const bool blk = (fmask >> r) & 1u;
         const int sl = __popc(fmask & ((1u << r) - 1u));   // compact slot of row r
@@ -707,6 +708,7 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
           const double tau = 1e-12 * (1.0 + yn + tau_c);
           lab = xc;
           dist = yn + x1;
+          uslack = 2.0 * tau;
           lnew = sqrt(fmax(yn + x2 - 2.0 * tau, 0.0));
           if (!(x2 - x1 > tau)) {                  // direct form, exactly as the oracle
             double best = CUDART_INF;              // centroids c = w, w + 8, ... then merged
@@ -734,6 +736,7 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
             }
             lab = bc;
             dist = best;
+            uslack = 0.0;
             lnew = 0.0;                            // near tie: recompute next step
           }
         }
@@ -744,6 +747,10 @@ k_kmeans_step(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
           if (old_lab != lab) ++nchg;
           labels[r0 + r] = lab;
           lbound[r0 + r] = lnew;
+          // upper bound on the distance to the assigned centroid (the light steps'
+          // Hamerly test): Da and the direct form carry <= 64 u relative error
+          // (non-negative terms), a score-based distance <= 2 tau absolute
+          if (ubound) ubound[r0 + r] = sqrt(fmax(dist, 0.0) + uslack) * (1.0 + kKmRel);
           inertia += dist;
           atomicAdd(&cnt[lab], 1);                 // integer: exact
         }
@@ -836,7 +843,7 @@ int kmeans_step_blocks(int64_t n) {
 void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
                         const double* C, int* labels, unsigned long long* changes,
                         double* part_inertia, double* part, double* lbound, const double* delta,
-                        const double* sep, int nblk, cudaStream_t st) {
+                        const double* sep, double* ubound, int nblk, cudaStream_t st) {
   const size_t smem = kmeans_step_smem(dim, K);
 #define OFSC_KS3(TT, NB, DPC)                                                                    \
   {                                                                                              \
@@ -844,7 +851,7 @@ void launch_kmeans_step(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
     k_kmeans_step<TT, NB, DPC><<<nblk, kKmThreads, smem, st>>>(                                  \
         n, dim, (const TT*)Y, ldy, K, C, labels, changes, part_inertia, part, lbound, delta,    \
-        sep);                                                                                    \
+        sep, ubound);                                                                                  \
   }
 #define OFSC_KS(TT, NB)                                                                          \
   switch ((dim + 15) / 16) {                                                                     \
@@ -986,4 +993,341 @@ void launch_kmeans_finish(int K, int dim, const double* red, double* C, cudaStre
   OFSC_LAUNCH_CHECK();
 }
 
+
+// ---------------------------------------------------------------------------
+// Light Lloyd step (late steps, R28): bounds first, Y only for the rows that fail.
+//   test:   u' = (u + delta[a]) (1 + rel) bounds the distance to the row's own
+//           centroid from above, l' = l - max_{c != a} delta[c] - rel (l + dm) the
+//           distance to every other centroid from below (Hamerly); sep[a] (half the
+//           distance from c_a to its nearest other centroid, deflated) is Elkan's
+//           test.  If u' < l' or u' < sep[a], every other centroid is strictly
+//           farther, so Lloyd's argmin is a: the row is not read, (u', l') carried.
+//   retest: a failing row is read and its exact distance Da to c_a tightens u
+//           (the terms are non-negative: relative error <= (dim + 5) u << rel);
+//           if now u < l' or u < sep[a] the row still keeps its label.
+//   assign: otherwise the oracle's direct form (sum over d in order of
+//           (y_d - C_cd)^2; this translation unit is compiled without FMA
+//           contraction; ties -> lowest index) over all K centroids: one warp per
+//           row, lane l owns centroids l, l + 32, ... (centroids transposed in smem:
+//           conflict-free); the exact best / runner-up give the row's new (u, l).
+//   sums:   only the rows whose label changed: dS[new] += y, dS[old] -= y (warp
+//           owning the centroid, lane: columns 2 lane, 2 lane + 1, changed rows in
+//           row order: fixed order, no atomics), dcnt by integer smem atomics;
+//           part[b] = (dS, dcnt) per CTA feeds the fixed-order reduction, then
+//           S += dS (k_kmeans_accum) and C = S / cnt.
+// ---------------------------------------------------------------------------
+constexpr int kKlRows = kKmThreads;   // rows per tile: one per thread in the test
+
+template <int KPW>
+__device__ __forceinline__ void kl_add(double (&sacc)[KPW][2], int j, double y0, double y1) {
+#pragma unroll
+  for (int q = 0; q < KPW; ++q)
+    if (q == j) {
+      sacc[q][0] += y0;
+      sacc[q][1] += y1;
+    }
+}
+
+template <typename T, int NBW>
+__global__ void __launch_bounds__(kKmThreads, 2)
+k_kmeans_light(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
+               const double* __restrict__ C, int* __restrict__ labels,
+               double* __restrict__ ubound, double* __restrict__ lbound,
+               const double* __restrict__ delta, const double* __restrict__ sep,
+               unsigned long long* changes, double* part) {
+  constexpr int KPW = 8 * NBW;                    // centroids owned per warp (sums)
+  extern __shared__ double sm[];
+  const int W = dim + 1;
+  double* Ct = sm;                                // [dim][K] (transposed)
+  double* yb = Ct + (size_t)K * dim;              // [8 warps][64] row buffer
+  int* fl = (int*)(yb + 8 * 64);                  // [kKlRows] failing tile rows (row order)
+  int* fo = fl + kKlRows;                         // [kKlRows] old label, -1: unchanged
+  int* fn = fo + kKlRows;                         // [kKlRows] new label
+  int* cnt = fn + kKlRows;                        // [K] count deltas
+  __shared__ int s_wf[kKmThreads / 32], s_nf;
+  __shared__ double s_m1, s_m2;
+  __shared__ int s_i1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < K * dim; e += kKmThreads) {
+    const int c = e / dim, d = e % dim;
+    Ct[d * K + c] = C[e];
+  }
+  for (int c = tid; c < K; c += kKmThreads) cnt[c] = 0;
+  if (tid == 0) {
+    double m1 = 0.0, m2 = 0.0;
+    int i1 = -1;
+    for (int c = 0; c < K; ++c) {
+      const double v = delta[c];
+      if (v > m1) {
+        m2 = m1;
+        m1 = v;
+        i1 = c;
+      } else if (v > m2) {
+        m2 = v;
+      }
+    }
+    s_m1 = m1;
+    s_m2 = m2;
+    s_i1 = i1;
+  }
+  __syncthreads();
+  double sacc[KPW][2];
+#pragma unroll
+  for (int j = 0; j < KPW; ++j) sacc[j][0] = sacc[j][1] = 0.0;
+  unsigned int nchg = 0, nskip = 0;
+  const int64_t ntiles = (n + kKlRows - 1) / kKlRows;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kKlRows;
+    const int64_t r = r0 + tid;
+    bool fail = false;
+    if (r < n) {
+      const int a = labels[r];
+      const double dm = a == s_i1 ? s_m2 : s_m1;
+      const double ub = ubound[r], lb = lbound[r];
+      const double u2 = (ub + delta[a]) * (1.0 + kKmRel);
+      const double l2 = lb - dm - kKmRel * (lb + dm);
+      const double sa = sep[a];
+      if ((l2 > 0.0 && u2 < l2) || (sa > 0.0 && u2 < sa)) {
+        ubound[r] = u2;
+        lbound[r] = l2;
+        ++nskip;
+      } else {
+        fail = true;
+      }
+    }
+    // failing rows compacted in row order (a tile without one costs one barrier)
+    const unsigned bm = __ballot_sync(0xffffffffu, fail);
+    if (lane == 0) s_wf[warp] = __popc(bm);
+    if (__syncthreads_count(fail) == 0) continue;
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < kKmThreads / 32; ++w) {
+        const int c = s_wf[w];
+        s_wf[w] = t;
+        t += c;
+      }
+      s_nf = t;
+    }
+    __syncthreads();
+    if (fail) fl[s_wf[warp] + __popc(bm & ((1u << lane) - 1u))] = tid;
+    __syncthreads();
+    const int nf = s_nf;
+    double* yr = yb + warp * 64;
+    for (int q = warp; q < nf; q += kKmThreads / 32) {
+      const int64_t row = r0 + fl[q];
+      const int a0 = labels[row];
+      double da = 0.0;                            // exact distance to the own centroid
+      for (int d = lane; d < dim; d += 32) {
+        const double y = ld1(Y + row * ldy + d);
+        yr[d] = y;
+        const double df = y - Ct[d * K + a0];
+        da = fma(df, df, da);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) da += __shfl_xor_sync(0xffffffffu, da, o);
+      {
+        const double dm = a0 == s_i1 ? s_m2 : s_m1;
+        const double lb = lbound[row];            // not yet carried: the test stored nothing
+        const double l2 = lb - dm - kKmRel * (lb + dm);
+        const double u2 = sqrt(da) * (1.0 + kKmRel);
+        const double sa = sep[a0];
+        if ((l2 > 0.0 && u2 < l2) || (sa > 0.0 && u2 < sa)) {
+          if (lane == 0) {
+            ubound[row] = u2;
+            lbound[row] = l2;
+            fo[q] = -1;
+            fn[q] = a0;
+            ++nskip;
+          }
+          __syncwarp();
+          continue;
+        }
+      }
+      __syncwarp();
+      double b1 = CUDART_INF, b2 = CUDART_INF;
+      int c1 = 0x7fffffff;
+      for (int c = lane; c < K; c += 32) {        // c increases: lowest index wins ties
+        double a = 0.0;
+        for (int d = 0; d < dim; ++d) {
+          const double diff = yr[d] - Ct[d * K + c];
+          a = a + diff * diff;
+        }
+        if (a < b1) {
+          b2 = b1;
+          b1 = a;
+          c1 = c;
+        } else if (a < b2) {
+          b2 = a;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {             // lexicographic (distance, index) minimum
+        const double ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
+        const double ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+        const int oc1 = __shfl_xor_sync(0xffffffffu, c1, o);
+        if (ob1 < b1 || (ob1 == b1 && oc1 < c1)) {
+          b2 = fmin(b1, ob2);
+          b1 = ob1;
+          c1 = oc1;
+        } else {
+          b2 = fmin(b2, ob1);
+        }
+      }
+      if (lane == 0) {
+        const int old = a0;
+        labels[row] = c1;
+        ubound[row] = sqrt(b1) * (1.0 + kKmRel);
+        lbound[row] = isinf(b2) ? CUDART_INF : sqrt(b2) * (1.0 - kKmRel);
+        fo[q] = old != c1 ? old : -1;
+        fn[q] = c1;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // label changes of this tile, in row order: counts (exact) and sums (owner warps)
+    for (int q = tid; q < nf; q += kKmThreads)
+      if (fo[q] >= 0) {
+        atomicAdd(&cnt[fn[q]], 1);
+        atomicAdd(&cnt[fo[q]], -1);
+        ++nchg;
+      }
+    for (int q = 0; q < nf; ++q) {
+      const int o = fo[q];
+      if (o < 0) continue;
+      const int nw = fn[q];
+      const bool mo = o / KPW == warp, mn = nw / KPW == warp;
+      if (!mo && !mn) continue;
+      double y0 = 0.0, y1 = 0.0;
+      if (2 * lane < dim) {
+        const T* yp = Y + (r0 + fl[q]) * ldy + 2 * lane;
+        y0 = ld1(yp);
+        y1 = 2 * lane + 1 < dim ? ld1(yp + 1) : 0.0;
+      }
+      if (mo) kl_add<KPW>(sacc, o % KPW, -y0, -y1);
+      if (mn) kl_add<KPW>(sacc, nw % KPW, y0, y1);
+    }
+    __syncthreads();                              // fl / fo / fn reused by the next tile
+  }
+  for (int o = 16; o; o >>= 1) {
+    nchg += __shfl_xor_sync(0xffffffffu, nchg, o);
+    nskip += __shfl_xor_sync(0xffffffffu, nskip, o);
+  }
+  if (lane == 0) {
+    if (nchg) atomicAdd(changes, (unsigned long long)nchg);        // integer: order-independent
+    if (nskip) atomicAdd(changes + 1, (unsigned long long)nskip);  // statistics: rows not read
+  }
+  __syncthreads();
+  double* pb = part + (int64_t)blockIdx.x * K * W;
+#pragma unroll
+  for (int j = 0; j < KPW; ++j) {
+    const int c = warp * KPW + j;
+    if (c < K)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int d = 2 * lane + h;
+        if (d < dim) pb[c * W + d] = sacc[j][h];
+      }
+  }
+  for (int c = tid; c < K; c += kKmThreads) pb[c * W + dim] = (double)cnt[c];
+}
+
+size_t kmeans_light_smem(int dim, int K) {
+  return ((size_t)K * dim + 8 * 64) * 8 + ((size_t)3 * kKlRows + K) * 4;
+}
+
+bool kmeans_light_supported(int dim, int K) {
+  const char* e = getenv("OFSC_KMEANS_LIGHT");
+  return !(e && e[0] == '0') && dim <= 64 && K <= 128 && kmeans_light_smem(dim, K) <= 100 * 1024;
+}
+
+int kmeans_light_blocks(int64_t n) {
+  const int64_t tiles = (n + kKlRows - 1) / kKlRows;
+  const int64_t cap = (int64_t)num_sms() * 2;
+  return (int)(tiles < 1 ? 1 : (tiles > cap ? cap : tiles));
+}
+
+void launch_kmeans_light(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy, int K,
+                         const double* C, int* labels, double* ubound, double* lbound,
+                         const double* delta, const double* sep, unsigned long long* changes,
+                         double* part, int nblk, cudaStream_t st) {
+  const size_t smem = kmeans_light_smem(dim, K);
+#define OFSC_KL(TT, NB)                                                                            \
+  {                                                                                                \
+    OFSC_CUDA(cudaFuncSetAttribute(k_kmeans_light<TT, NB>,                                         \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
+    k_kmeans_light<TT, NB><<<nblk, kKmThreads, smem, st>>>(n, dim, (const TT*)Y, ldy, K, C, labels, \
+                                                          ubound, lbound, delta, sep, changes,    \
+                                                          part);                                  \
+  }
+  if (dt == OFSC_F64) {
+    if (K > 64) OFSC_KL(double, 2) else OFSC_KL(double, 1)
+  } else {
+    if (K > 64) OFSC_KL(float, 2) else OFSC_KL(float, 1)
+  }
+#undef OFSC_KL
+  OFSC_LAUNCH_CHECK();
+}
+
+// S += dS (running cluster sums and counts of the light steps)
+__global__ void k_kmeans_accum(int n, double* __restrict__ S, const double* __restrict__ dS) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) S[e] += dS[e];
+}
+
+void launch_kmeans_accum(int n, double* S, const double* dS, cudaStream_t st) {
+  k_kmeans_accum<<<(n + 255) / 256, 256, 0, st>>>(n, S, dS);
+  OFSC_LAUNCH_CHECK();
+}
+
+// Inertia of an assignment: sum over rows of the direct-form distance to the
+// row's centroid (d order, no FMA contraction); 64-row tiles staged in smem,
+// one thread per row; per-CTA partial in row order -> fixed-order reduction.
+template <typename T>
+__global__ void __launch_bounds__(kKmThreads)
+k_kmeans_inertia(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy,
+                 const double* __restrict__ C, const int* __restrict__ labels, double* part) {
+  constexpr int TR = 64;
+  __shared__ double ys[TR * 65];
+  __shared__ double s_in[TR];
+  const int tid = threadIdx.x;
+  const int ld = dim + 1;
+  double acc = 0.0;
+  const int64_t ntiles = (n + TR - 1) / TR;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TR;
+    const int rows = (int)imin64(TR, n - r0);
+    for (int e = tid; e < rows * dim; e += kKmThreads) {
+      const int q = e / dim, d = e % dim;
+      ys[q * ld + d] = ld1(Y + (r0 + q) * ldy + d);
+    }
+    __syncthreads();
+    if (tid < rows) {
+      const double* cr = C + (int64_t)labels[r0 + tid] * dim;
+      double a = 0.0;
+      for (int d = 0; d < dim; ++d) {
+        const double diff = ys[tid * ld + d] - cr[d];
+        a = a + diff * diff;
+      }
+      acc += a;
+    }
+    __syncthreads();
+  }
+  if (tid < TR) s_in[tid] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0;
+    for (int q = 0; q < TR; ++q) a += s_in[q];
+    part[blockIdx.x] = a;
+  }
+}
+
+void launch_kmeans_inertia(ofsc_dtype dt, int64_t n, int dim, const void* Y, int64_t ldy,
+                           const double* C, const int* labels, double* part, int nblk,
+                           cudaStream_t st) {
+  if (dt == OFSC_F64)
+    k_kmeans_inertia<double><<<nblk, kKmThreads, 0, st>>>(n, dim, (const double*)Y, ldy, C, labels, part);
+  else
+    k_kmeans_inertia<float><<<nblk, kKmThreads, 0, st>>>(n, dim, (const float*)Y, ldy, C, labels, part);
+  OFSC_LAUNCH_CHECK();
+}
 }  // namespace ofsc

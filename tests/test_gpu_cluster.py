@@ -195,7 +195,51 @@ def test_kmeans_bound_pruning_exact(n, dim, K, capfd, monkeypatch):
     C2 = torch.from_numpy(C0.copy()).cuda()
     l2, it2, in2 = ofsc.kmeans(Yd, C2, max_iters=40)
     assert torch.equal(l2, lg) and it2 == itg
-    assert torch.equal(C2, C)                     # same labels -> bit-identical sums
+    # the light steps update the sums by the label changes (S += dS): the same
+    # labels give the same centroids up to the rounding of those updates
+    assert np.allclose(C2.cpu().numpy(), C.cpu().numpy(), atol=1e-13, rtol=0)
+    assert abs(in2 - ing) <= 1e-12 * ing
+    # without the light steps every step re-sums all rows: bit-identical sums
+    monkeypatch.delenv("OFSC_KMEANS_NOSKIP")
+    monkeypatch.setenv("OFSC_KMEANS_LIGHT", "0")
+    C3 = torch.from_numpy(C0.copy()).cuda()
+    l3, it3, in3 = ofsc.kmeans(Yd, C3, max_iters=40)
+    assert torch.equal(l3, lg) and it3 == itg
+    assert torch.equal(C3, C2)
+    assert abs(in3 - in2) <= 1e-12 * in2
+
+
+@pytest.mark.parametrize("n,dim,K,dt", [(200003, 64, 64, "f64"), (120001, 48, 100, "f64"),
+                                        (50001, 5, 7, "f64"), (80021, 64, 64, "f32")])
+def test_kmeans_light_steps(n, dim, K, dt, capfd, monkeypatch):
+    """Late Lloyd steps that read only the rows whose carried Hamerly / Elkan
+    bounds fail (R28) and update the sums by the label changes: labels and step
+    count equal the oracle's Lloyd run and the full-pass kernel's; centroids
+    within 1e-13; the statistics show light steps that left most rows unread."""
+    Y, _ = _blobs(n, dim, K, 3 * n + K, spread=0.2)
+    if dt == "f32":
+        Y = Y.astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(11)
+    C0 = Y[rng.choice(n, K, replace=False)].copy()
+    lo, Co, ito, ino = kmeans_lloyd(Y, C0, max_iters=60)
+    Yd = torch.from_numpy(Y).cuda()
+    if dt == "f32":
+        Yd = Yd.float()
+    monkeypatch.setenv("OFSC_KMEANS_STATS", "1")
+    C = torch.from_numpy(C0.copy()).cuda()
+    lg, itg, ing = ofsc.kmeans(Yd, C, max_iters=60)
+    err = capfd.readouterr().err
+    steps = [l for l in err.splitlines() if "[ofsc kmeans]" in l]
+    light = [int(l.split("skipped")[1].split()[0]) for l in steps if l.endswith("light 1")]
+    assert len(steps) == itg and len(light) >= 1 and max(light) > n // 2
+    assert np.array_equal(lg.cpu().numpy(), lo) and itg == ito
+    assert np.allclose(C.cpu().numpy(), Co, atol=1e-13, rtol=0)
+    assert abs(ing - ino) <= 1e-12 * ino
+    monkeypatch.setenv("OFSC_KMEANS_LIGHT", "0")
+    C2 = torch.from_numpy(C0.copy()).cuda()
+    l2, it2, in2 = ofsc.kmeans(Yd, C2, max_iters=60)
+    assert torch.equal(l2, lg) and it2 == itg
+    assert np.allclose(C2.cpu().numpy(), C.cpu().numpy(), atol=1e-13, rtol=0)
     assert abs(in2 - ing) <= 1e-12 * ing
 
 
