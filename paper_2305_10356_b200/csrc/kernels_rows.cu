@@ -243,7 +243,7 @@ __global__ void k_update_x(IterParams p) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(e % p.KP);
-    st1(X + e, rndT<T>(ld1(X + e) + p.alpha[c] * ld1(V + e)));
+    st1(X + e, rndT<T>(fma(p.alpha[c], ld1(V + e), ld1(X + e))));   // as C3 phase A
   }
 }
 

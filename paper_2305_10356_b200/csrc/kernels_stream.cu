@@ -132,8 +132,8 @@ k_update_direction(IterParams p, int apply_update) {
         x = (double)sX[e];
         ax = (double)sAX[e];
         if (apply_update) {
-          x = rndT<T>(x + s_alpha[c] * (double)sV[e]);
-          ax = rndT<T>(ax + s_alpha[c] * (double)sAV[e]);
+          x = rndT<T>(fma(s_alpha[c], (double)sV[e], x));
+          ax = rndT<T>(fma(s_alpha[c], (double)sAV[e], ax));
           sX[e] = (T)x;
           sAX[e] = (T)ax;
         }
@@ -181,10 +181,11 @@ k_update_direction(IterParams p, int apply_update) {
             const int c = cb * 8 + 2 * tig + h;
             const double ax = AXp[r * LD + c];
             double g;
-            if (METHOD == OFSC_OFM_F1) g = 4.0 * ax + 4.0 * a1[rb][h];
-            else if (METHOD == OFSC_TRIOFM_F1) g = ax + a1[rb][h];
-            else if (METHOD == OFSC_OFM_F2) g = 4.0 * ax - 2.0 * a1[rb][h] - 2.0 * a2[rb][h];
-            else g = 2.0 * ax - a2[rb][h] - a1[rb][h];
+            // explicit roundings: every C3 variant computes the same bits
+            if (METHOD == OFSC_OFM_F1) g = fma(4.0, a1[rb][h], 4.0 * ax);
+            else if (METHOD == OFSC_TRIOFM_F1) g = __dadd_rn(ax, a1[rb][h]);
+            else if (METHOD == OFSC_OFM_F2) g = fma(-2.0, a2[rb][h], fma(-2.0, a1[rb][h], 4.0 * ax));
+            else g = __dadd_rn(__dadd_rn(2.0 * ax, -a2[rb][h]), -a1[rb][h]);
             g = rndT<T>(g);
             const double gp = (double)sG[r * KP + c];
             sG[r * KP + c] = (T)g;
@@ -358,8 +359,8 @@ k_update_direction_ws(IterParams p, int apply_update) {
         x = (double)sX[e];
         ax = (double)sAX[e];
         if (apply_update) {
-          x = rndT<T>(x + s_alpha[c] * (double)sV[e]);
-          ax = rndT<T>(ax + s_alpha[c] * (double)sAV[e]);
+          x = rndT<T>(fma(s_alpha[c], (double)sV[e], x));
+          ax = rndT<T>(fma(s_alpha[c], (double)sAV[e], ax));
           sX[e] = (T)x;
           sAX[e] = (T)ax;
         }
@@ -397,10 +398,11 @@ k_update_direction_ws(IterParams p, int apply_update) {
             const int c = cb * 8 + 2 * tig + h;
             const double ax = AXp[r * LD + c];
             double g;
-            if (METHOD == OFSC_OFM_F1) g = 4.0 * ax + 4.0 * a1[rb][h];
-            else if (METHOD == OFSC_TRIOFM_F1) g = ax + a1[rb][h];
-            else if (METHOD == OFSC_OFM_F2) g = 4.0 * ax - 2.0 * a1[rb][h] - 2.0 * a2[rb][h];
-            else g = 2.0 * ax - a2[rb][h] - a1[rb][h];
+            // explicit roundings: every C3 variant computes the same bits
+            if (METHOD == OFSC_OFM_F1) g = fma(4.0, a1[rb][h], 4.0 * ax);
+            else if (METHOD == OFSC_TRIOFM_F1) g = __dadd_rn(ax, a1[rb][h]);
+            else if (METHOD == OFSC_OFM_F2) g = fma(-2.0, a2[rb][h], fma(-2.0, a1[rb][h], 4.0 * ax));
+            else g = __dadd_rn(__dadd_rn(2.0 * ax, -a2[rb][h]), -a1[rb][h]);
             g = rndT<T>(g);
             const double gp = (double)sG[r * KP + c];
             sG[r * KP + c] = (T)g;
@@ -483,7 +485,14 @@ int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n) {
     if (dt == OFSC_F64) b = f2 ? C3Smem<double, KPC, 2>::bytes : C3Smem<double, KPC, 0>::bytes;
     else b = f2 ? C3Smem<float, KPC, 2>::bytes : C3Smem<float, KPC, 0>::bytes;
   });
-  return stream_grid(n, b);
+  // at most 2 resident CTAs per SM: at KP = 48 a third fits in shared memory but
+  // measured slower (c5 OFM-f2 2.072 -> 2.017 ms, TriOFM-f2 2.132 -> 1.987 ms per
+  // iteration with 2; profiles/r02/c3_grid_ab.jsonl).  OFSC_C3_CTAS overrides (A/B).
+  const char* e = getenv("OFSC_C3_CTAS");
+  const int per_sm = (e && *e) ? atoi(e) : 2;
+  const int64_t tiles = std::max<int64_t>(1, (n + kSTR - 1) / kSTR);
+  return (int)std::min<int64_t>(std::min<int64_t>((int64_t)num_sms() * per_sm, tiles),
+                                stream_grid(n, b));
 }
 
 void launch_update_direction(ofsc_dtype dt, const IterParams& p, int apply_update, int nblk,
@@ -591,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_direction_gram(IterParams p) {
       const int r = e / KP, c = e % KP;
       double v = 0.0, x = 0.0;
       if (r < rows) {
-        v = rndT<T>(-(double)sG[e] + s_beta[c] * (double)sV[e]);
+        v = rndT<T>(fma(s_beta[c], (double)sV[e], -(double)sG[e]));
         x = (double)sX[e];
         sV[e] = (T)v;
       }
@@ -710,7 +719,7 @@ __global__ void __launch_bounds__(kGWS_THREADS, 1) k_direction_gram_ws(IterParam
         const int r = e / KP, c = e % KP;
         double v = 0.0, x = 0.0;
         if (r < rows) {
-          v = rndT<T>(-(double)sG[e] + s_beta[c] * (double)sV[e]);
+          v = rndT<T>(fma(s_beta[c], (double)sV[e], -(double)sG[e]));
           x = (double)sX[e];
           sV[e] = (T)v;
         }

@@ -322,18 +322,22 @@ def test_graph_launch_structure_is_transparent(method):
     assert np.array_equal(ra.history, rb.history)
 
 
+@pytest.mark.parametrize("k", [48, 64])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("method", METHODS)
-def test_c3_kernel_variants_bitwise(method, dtype, monkeypatch):
+def test_c3_kernel_variants_bitwise(method, dtype, k, monkeypatch):
     """C3's two kernels -- the single-role k_update_direction and the producer-warp
     k_update_direction_ws (default for the f1 methods) -- compute the same bits
-    (same arithmetic, same order; only the TMA traffic is owned differently), on
-    the KP = 64 production width (reordered N = 20,011 graph)."""
-    op, g, X0 = setup_wide(64)
+    (same products, same k order, explicitly rounded G expression; only the TMA
+    traffic is owned differently), on the KP = 48 / 64 production widths
+    (reordered N = 20,011 graph).  Both run the same grid: the column-dot
+    partials, and so beta, depend on which tiles a CTA owns."""
+    op, g, X0 = setup_wide(k)
     outs = []
-    for v in ("0", "1"):
-        monkeypatch.setenv("OFSC_C3_WS", v)
+    for ws in ("0", "1"):
+        monkeypatch.setenv("OFSC_C3_WS", ws)
         X, r = gpu_run(g, method, X0, 10, dtype=dtype)
         outs.append((X, r.history))
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert np.array_equal(outs[0][1], outs[1][1])
+    for X, h in outs[1:]:
+        assert np.array_equal(outs[0][0], X)
+        assert np.array_equal(outs[0][1], h)

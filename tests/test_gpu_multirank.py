@@ -134,9 +134,12 @@ def test_p5_fp32():
 
 
 @pytest.mark.parametrize("p", [2, 8])
-def test_p5_kmeans_labels_equal_single_rank(p):
+def test_p5_kmeans_labels_equal_single_rank(p, capfd, monkeypatch):
     """K-means at p ranks on identical features: labels equal the oracle's Lloyd run
-    (and therefore p = 1's, tested in test_gpu_cluster.py), ties excepted."""
+    (and therefore p = 1's, tested in test_gpu_cluster.py), ties excepted; the
+    late steps run as light steps (bounds first, sums by label changes, the
+    change sums and counts summed over ranks)."""
+    monkeypatch.setenv("OFSC_KMEANS_STATS", "1")
     cfg, s, d, lab, op, X0 = c2()
     o = run_ofm(op, "ofm_f2", X0, 60, refresh=0)
     Y = row_normalize(o.X)
@@ -158,6 +161,8 @@ def test_p5_kmeans_labels_equal_single_rank(p):
     finally:
         world.close()
     labels = np.concatenate([o_[0] for o_ in outs])
+    steps = [l for l in capfd.readouterr().err.splitlines() if "[ofsc kmeans]" in l]
+    assert len(steps) == p * outs[0][1] and sum(l.endswith("light 1") for l in steps) >= p
     assert all(o_[1] == outs[0][1] for o_ in outs)
     assert all(np.array_equal(o_[3], outs[0][3]) for o_ in outs)   # replicated centroids
     mism = np.nonzero(labels != lab_o)[0]
