@@ -240,15 +240,8 @@ struct C3WsSmem {
   static constexpr size_t bytes = base + 2 * kC3Stages * 8;          // + adone, cdone barriers
 };
 
-// WG = 1: three warpgroups (12 warps): warpgroups 0-1 compute, warpgroup 2 holds the
-// producer warp and gives its registers to the compute warps (setmaxnreg), so the
-// f2 methods' register-resident M and W fragments fit without spills at 2 CTAs/SM.
-constexpr int kC3WgThreads = 384;
-constexpr int kC3WgProducerRegs = 24;
-constexpr int kC3WgComputeRegs = 104;
-
-template <typename T, int KP, int METHOD, int WG = 0>
-__global__ void __launch_bounds__(WG ? kC3WgThreads : kC3WsThreads, 2)
+template <typename T, int KP, int METHOD>
+__global__ void __launch_bounds__(kC3WsThreads, 2)
 k_update_direction_ws(IterParams p, int apply_update) {
   using S = C3Smem<T, KP, METHOD>;
   constexpr int LD = S::LD;
@@ -302,10 +295,9 @@ k_update_direction_ws(IterParams p, int apply_update) {
   }
   if (tid < KP) s_alpha[tid] = apply_update ? p.alpha[tid] : 0.0;
   __syncthreads();
-  if (warp >= NCW) {
-    if constexpr (WG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kC3WgProducerRegs));
+  if (warp == NCW) {
     // ---- producer warp: loads, stores, stage recycling (lane 0)
-    if (warp == NCW && lane == 0) {
+    if (lane == 0) {
       for (int s = 0; s < NS; ++s) {
         const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
         if (tile < ntiles) issue(s, tile);
@@ -337,7 +329,6 @@ k_update_direction_ws(IterParams p, int apply_update) {
     return;
   }
   // ---- compute warps (k_update_direction's phases A, B, C)
-  if constexpr (WG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kC3WgComputeRegs));
   const bool mma_warp = warp < NB;
   const int cb = mma_warp ? warp : 0;
   double bm[KS], bw[F1 ? 1 : KS];
@@ -442,16 +433,16 @@ k_update_direction_ws(IterParams p, int apply_update) {
   }
 }
 
-template <typename T, int KP, int METHOD, int WG = 0>
+template <typename T, int KP, int METHOD>
 static void launch_c3_ws(const IterParams& p, int apply, int nblk, cudaStream_t s) {
   const size_t smem = C3WsSmem<T, KP, METHOD>::bytes;
-  auto kern = k_update_direction_ws<T, KP, METHOD, WG>;
+  auto kern = k_update_direction_ws<T, KP, METHOD>;
   static bool set = false;
   if (!set) {
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
-  launch_k(kern, dim3(nblk), dim3(WG ? kC3WgThreads : kC3WsThreads), smem, s, pdl_take(), p, apply);
+  launch_k(kern, dim3(nblk), dim3(kC3WsThreads), smem, s, pdl_take(), p, apply);
 }
 
 // Default: the warp-specialised C3 for the f1 methods (one DMMA product per tile:
@@ -507,21 +498,6 @@ int c3_grid(ofsc_dtype dt, int KP, int method, int64_t n) {
 void launch_update_direction(ofsc_dtype dt, const IterParams& p, int apply_update, int nblk,
                              cudaStream_t s) {
   OFSC_DISPATCH_KP(p.KP, {
-    if (c3_ws(p.method) == 2) {   // three-warpgroup form (setmaxnreg), f2 methods (A/B)
-      if (dt == OFSC_F64) {
-        switch (p.method) {
-          case 2: launch_c3_ws<double, KPC, 2, 1>(p, apply_update, nblk, s); return;
-          case 3: launch_c3_ws<double, KPC, 3, 1>(p, apply_update, nblk, s); return;
-          default: break;
-        }
-      } else {
-        switch (p.method) {
-          case 2: launch_c3_ws<float, KPC, 2, 1>(p, apply_update, nblk, s); return;
-          case 3: launch_c3_ws<float, KPC, 3, 1>(p, apply_update, nblk, s); return;
-          default: break;
-        }
-      }
-    }
     if (c3_ws(p.method)) {
       if (dt == OFSC_F64) {
         switch (p.method) {

@@ -326,16 +326,15 @@ def test_graph_launch_structure_is_transparent(method):
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("method", METHODS)
 def test_c3_kernel_variants_bitwise(method, dtype, k, monkeypatch):
-    """C3's kernels -- the single-role k_update_direction, the producer-warp
-    k_update_direction_ws (default for the f1 methods) and its three-warpgroup form
-    (the producer warpgroup's registers handed to the compute warps) -- compute the same bits
+    """C3's two kernels -- the single-role k_update_direction and the producer-warp
+    k_update_direction_ws (default for the f1 methods) -- compute the same bits
     (same products, same k order, explicitly rounded G expression; only the TMA
     traffic is owned differently), on the KP = 48 / 64 production widths
     (reordered N = 20,011 graph).  Both run the same grid: the column-dot
     partials, and so beta, depend on which tiles a CTA owns."""
     op, g, X0 = setup_wide(k)
     outs = []
-    for ws in ("0", "1", "2"):     # 2: the three-warpgroup (setmaxnreg) form, f2 methods
+    for ws in ("0", "1"):
         monkeypatch.setenv("OFSC_C3_WS", ws)
         X, r = gpu_run(g, method, X0, 10, dtype=dtype)
         outs.append((X, r.history))
