@@ -1016,7 +1016,8 @@ void launch_kmeans_finish(int K, int dim, const double* red, double* C, cudaStre
 //           part[b] = (dS, dcnt) per CTA feeds the fixed-order reduction, then
 //           S += dS (k_kmeans_accum) and C = S / cnt.
 // ---------------------------------------------------------------------------
-constexpr int kKlRows = kKmThreads;   // rows per tile: one per thread in the test
+constexpr int kKlPer = 4;                       // rows per thread in the bound test
+constexpr int kKlRows = kKmThreads * kKlPer;    // rows per tile
 
 template <int KPW>
 __device__ __forceinline__ void kl_add(double (&sacc)[KPW][2], int j, double y0, double y1) {
@@ -1044,7 +1045,7 @@ k_kmeans_light(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
   int* fo = fl + kKlRows;                         // [kKlRows] old label, -1: unchanged
   int* fn = fo + kKlRows;                         // [kKlRows] new label
   int* cnt = fn + kKlRows;                        // [K] count deltas
-  __shared__ int s_wf[kKmThreads / 32], s_nf;
+  __shared__ int s_wf[kKlPer * (kKmThreads / 32)], s_nf;
   __shared__ double s_m1, s_m2;
   __shared__ int s_i1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1078,30 +1079,41 @@ k_kmeans_light(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
   const int64_t ntiles = (n + kKlRows - 1) / kKlRows;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * kKlRows;
-    const int64_t r = r0 + tid;
-    bool fail = false;
-    if (r < n) {
-      const int a = labels[r];
-      const double dm = a == s_i1 ? s_m2 : s_m1;
-      const double ub = ubound[r], lb = lbound[r];
-      const double u2 = (ub + delta[a]) * (1.0 + kKmRel);
-      const double l2 = lb - dm - kKmRel * (lb + dm);
-      const double sa = sep[a];
-      if ((l2 > 0.0 && u2 < l2) || (sa > 0.0 && u2 < sa)) {
-        ubound[r] = u2;
-        lbound[r] = l2;
-        ++nskip;
-      } else {
-        fail = true;
+    // tile row j * 256 + tid for j < kKlPer: loads of all four rows issued together
+    bool fail[kKlPer];
+    int any = 0;
+#pragma unroll
+    for (int j = 0; j < kKlPer; ++j) {
+      const int64_t r = r0 + j * kKmThreads + tid;
+      fail[j] = false;
+      if (r < n) {
+        const int a = labels[r];
+        const double dm = a == s_i1 ? s_m2 : s_m1;
+        const double ub = ubound[r], lb = lbound[r];
+        const double u2 = (ub + delta[a]) * (1.0 + kKmRel);
+        const double l2 = lb - dm - kKmRel * (lb + dm);
+        const double sa = sep[a];
+        if ((l2 > 0.0 && u2 < l2) || (sa > 0.0 && u2 < sa)) {
+          ubound[r] = u2;
+          lbound[r] = l2;
+          ++nskip;
+        } else {
+          fail[j] = true;
+          any = 1;
+        }
       }
     }
-    // failing rows compacted in row order (a tile without one costs one barrier)
-    const unsigned bm = __ballot_sync(0xffffffffu, fail);
-    if (lane == 0) s_wf[warp] = __popc(bm);
-    if (__syncthreads_count(fail) == 0) continue;
+    // failing rows compacted in row order (j, warp, lane); a tile without one costs one barrier
+    unsigned bm[kKlPer];
+#pragma unroll
+    for (int j = 0; j < kKlPer; ++j) {
+      bm[j] = __ballot_sync(0xffffffffu, fail[j]);
+      if (lane == 0) s_wf[j * (kKmThreads / 32) + warp] = __popc(bm[j]);
+    }
+    if (__syncthreads_count(any) == 0) continue;
     if (tid == 0) {
       int t = 0;
-      for (int w = 0; w < kKmThreads / 32; ++w) {
+      for (int w = 0; w < kKlPer * (kKmThreads / 32); ++w) {
         const int c = s_wf[w];
         s_wf[w] = t;
         t += c;
@@ -1109,7 +1121,10 @@ k_kmeans_light(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
       s_nf = t;
     }
     __syncthreads();
-    if (fail) fl[s_wf[warp] + __popc(bm & ((1u << lane) - 1u))] = tid;
+#pragma unroll
+    for (int j = 0; j < kKlPer; ++j)
+      if (fail[j])
+        fl[s_wf[j * (kKmThreads / 32) + warp] + __popc(bm[j] & ((1u << lane) - 1u))] = j * kKmThreads + tid;
     __syncthreads();
     const int nf = s_nf;
     double* yr = yb + warp * 64;
