@@ -989,30 +989,6 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, p.colred, 2 * (size_t)p.KP, s); });
     pr.ph(OFSC_PH_BETA, 1, [&] { launch_beta(p, w.nb3, 1, s); });
   }
-  static int exp_conc = -1;   // TIMING EXPERIMENT ONLY (wrong numerics): C4 || SpMM(G)
-  if (exp_conc < 0) {
-    const char* e = getenv("OFSC_EXP_CONC");
-    exp_conc = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (exp_conc && g->p == 1 && w.fork_st && !pr.timing) {
-    OFSC_CUDA(cudaEventRecord(w.ev_f0, s));
-    OFSC_CUDA(cudaStreamWaitEvent(w.fork_st, w.ev_f0, 0));
-    pdl_next(false);
-    launch_direction_gram(dt, p, w.nb4, w.fork_st);
-    launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, w.fork_st);
-    OFSC_CUDA(cudaEventRecord(w.ev_f1, w.fork_st));
-    pdl_next(false);
-    launch_spmm(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot, g->s32_slot,
-                w.G, w.AV, &p.ctl->stop, s, g->cid, g->cstart, w.ctr, 0, &g->heavy, &g->svs,
-                g->nnz_local);
-    OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_f1, 0));
-    pdl_next(false);
-    launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
-    pdl_next(false);
-    launch_reduce_linesearch(p, w.part_g2, w.nb2, s);
-    pr.launches[OFSC_PH_SPMM_GRAM] += 5;
-    return;
-  }
   pdl_next(pdl);
   pr.ph(OFSC_PH_DIRECTION_GRAM, 1, [&] { launch_direction_gram(dt, p, w.nb4, s); });
   // p == 1: C4's partial Grams (Q, P) are reduced on a forked stream while the SpMM
