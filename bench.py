@@ -189,6 +189,48 @@ def load_traffic():
     return None
 
 
+def dmma_peak():
+    """Measured fp64 tensor (DMMA.8x8x4) peak, TFLOP/s (profiles/r01/fp64_probe.txt)."""
+    p = os.path.join(ROOT, "profiles", "r01", "fp64_probe.txt")
+    try:
+        for line in open(p):
+            if line.startswith("DMMA tpb=256:"):
+                return float(line.split(":")[1].split()[0]), "measured: tools/fp64_probe.cu (profiles/r01/fp64_probe.txt)"
+    except OSError:
+        pass
+    return 40.0, "nominal B200 fp64 tensor (no measured file)"
+
+
+def kernel_rooflines(kern, algo, n, k, method, hbm_peak):
+    """Per big kernel: average launch time, HBM fraction on its algorithmic bytes and
+    fp64-tensor fraction on the algorithmic flops of its DMMA products (triu and the
+    symmetric Grams count their upper triangle only); `binding` = the larger."""
+    tri = method.startswith("tri")
+    f1 = method.endswith("f1")
+    half = n * k * (k + 1)                     # one triangular / symmetric product
+    full = 2 * n * k * k                       # one full N x k . k x k product
+    flops = {
+        "update_direction": (half if tri else full) * (1 if f1 else 2),
+        "direction_gram": half + full,         # Q = V^T V (symmetric) + P = V^T X
+        "gram_stream": half + full,            # T = V^T A V (symmetric) + R' = X^T A V
+        "spmm": 0,
+    }
+    tpk, tsrc = dmma_peak()
+    out = {"fp64_tensor_peak_tflops": tpk, "fp64_tensor_peak_source": tsrc, "hbm_peak_gbs": hbm_peak}
+    for name in ("spmm", "update_direction", "direction_gram", "gram_stream"):
+        if name not in kern or not kern[name]["launches"]:
+            continue
+        ms = kern[name]["ms_total"] / kern[name]["launches"]
+        gbs = algo[name] / (ms / 1e3) / 1e9
+        tf = flops[name] / (ms / 1e3) / 1e12
+        fh, ft = gbs / hbm_peak, tf / tpk
+        out[name] = {"avg_launch_ms": round(ms, 4), "hbm_gbs": round(gbs, 1), "hbm_frac": round(fh, 4),
+                     "fp64_tensor_tflops": round(tf, 2), "fp64_tensor_frac": round(ft, 4),
+                     "binding": "hbm" if fh >= ft else "fp64_tensor",
+                     "algorithmic_bytes": algo[name], "algorithmic_flops": flops[name]}
+    return out
+
+
 def kp_of(k):
     return 16 if k <= 16 else 32 if k <= 32 else 48 if k <= 48 else 64
 
@@ -362,6 +404,9 @@ def run_ours(args):
                        "frac": round(ach / gpk["l2_gather_gbs"], 4),
                        "bytes_per_launch": gather_bytes, "avg_launch_ms": round(sp_ms, 4),
                        "peak_source": gpk["source"]}
+    # every big kernel against both of its ceilings: HBM (algorithmic bytes, above)
+    # and the fp64 tensor pipe (DMMA.8x8x4; algorithmic flops of its products)
+    kr = kernel_rooflines(kern, algo, nl, k, args.method, hbm_peak)
     it_dram = None
     if traffic and traffic.get("config") == cfg.name and world == 1 and args.dtype == "f64" \
             and traffic.get("dram_bytes_per_iteration"):
@@ -388,6 +433,7 @@ def run_ours(args):
                    if info["reordered"] else "none (random node ids)"},
         "roofline": roofline,
         "roofline_l2_gather": roofline_l2,
+        "kernel_rooflines": kr,
         "iteration_dram_ncu": it_dram,
         "iteration_hbm": {"algorithmic_bytes_per_iter_per_gpu": it_bytes,
                           "definition": "11 B + 4 nnz + 8 (N + 1) + 8 N (SURVEY 8(d).3), B = N k w",

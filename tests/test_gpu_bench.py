@@ -49,6 +49,10 @@ def test_bench_line_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
+    kr = d["kernel_rooflines"]
+    for name in ("spmm", "update_direction", "direction_gram", "gram_stream"):
+        assert 0 < kr[name]["hbm_frac"] < 1.5 and 0 <= kr[name]["fp64_tensor_frac"] < 1.5
+        assert kr[name]["binding"] in ("hbm", "fp64_tensor")
     assert d["clustering"]["seeds"] == 10 and -1 <= d["clustering"]["ari_mean"] <= 1
 
 
