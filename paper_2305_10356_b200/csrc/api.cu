@@ -939,9 +939,11 @@ static void refresh_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, cudaSt
     Zg = w.Xg;
   }
   pr.ph(OFSC_PH_REFRESH, 3, [&] {
+    // p == 1: the iteration SpMM's in-order row hand-out and neighbour-scale stream
     launch_spmm_then_gram(dt, p.KP, g->n_local, g->own_off, g->row_ptr, g->col, g->s_slot,
                      g->s32_slot, Zg, nullptr, w.AX, w.part_g2, 1, &p.ctl->stop, w.nb2, s,
-                     &g->heavy);
+                     &g->heavy, g->p == 1 ? w.ctr : nullptr, g->p == 1 ? &g->svs : nullptr,
+                     g->nnz_local);
     launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, p.M, s);  // M, W contiguous
   });
   pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, p.M, 2 * (size_t)p.KP * p.KP, s); });

@@ -124,11 +124,15 @@ void launch_direction_gram(ofsc_dtype dt, const IterParams& p, int nblk, cudaStr
 struct HeavyRows;
 // C2: Y = A Z (Z gathered; C2a), then the partial Grams over the own rows (C2b, a
 // separate TMA-streamed DMMA kernel). mode 0: (Zown^T Y, Xown^T Y); mode 1: (Zown^T Zown, Zown^T Y)
+struct SvalStream;
 void launch_spmm_then_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off,
                       const int64_t* row_ptr, const int32_t* col, const double* s,
                       const float* s32, const void* Zg, const void* Xown, void* Y,
                       double* part, int mode, const int* stop, int nblk, cudaStream_t st,
-                      const HeavyRows* heavy = nullptr);
+                      const HeavyRows* heavy = nullptr,
+                      unsigned long long* ctr = nullptr,   // in-order row hand-out (L2 window)
+                      const SvalStream* svs = nullptr,     // neighbour-scale stream (p == 1)
+                      int64_t nnz = -1);
 // C2a: Y = A Z only (KP-padded rows)
 // cid/cstart (may be NULL): community of each row -> L2 evict_last for in-community
 // neighbour rows, evict_first for the rest (p == 1 only)

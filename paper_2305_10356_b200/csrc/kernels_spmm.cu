@@ -738,9 +738,10 @@ void launch_spmm_then_gram(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_o
                       const int64_t* row_ptr, const int32_t* col, const double* s,
                       const float* s32, const void* Zg, const void* Xown, void* Y, double* part,
                       int mode, const int* stop, int nblk, cudaStream_t st,
-                      const HeavyRows* heavy) {
+                      const HeavyRows* heavy, unsigned long long* ctr, const SvalStream* svs,
+                      int64_t nnz) {
   launch_spmm(dt, KP, n_local, own_off, row_ptr, col, s, s32, Zg, Y, stop, st, nullptr, nullptr,
-              nullptr, 0, heavy);
+              ctr, 0, heavy, svs, nnz);
   if (part) {
     const size_t es = dt == OFSC_F64 ? 8 : 4;
     const void* Zown = (const char*)Zg + (size_t)own_off * KP * es;
