@@ -209,14 +209,14 @@ def test_kmeans_bound_pruning_exact(n, dim, K, capfd, monkeypatch):
     assert abs(in3 - in2) <= 1e-12 * in2
 
 
-@pytest.mark.parametrize("n,dim,K,dt", [(200003, 64, 64, "f64"), (120001, 48, 100, "f64"),
-                                        (50001, 5, 7, "f64"), (80021, 64, 64, "f32")])
-def test_kmeans_light_steps(n, dim, K, dt, capfd, monkeypatch):
+@pytest.mark.parametrize("n,dim,K,dt,spread", [(40003, 64, 64, "f64", 0.2), (30001, 48, 100, "f64", 0.1),
+                                               (30011, 5, 7, "f64", 0.2), (20021, 64, 64, "f32", 0.2)])
+def test_kmeans_light_steps(n, dim, K, dt, spread, capfd, monkeypatch):
     """Late Lloyd steps that read only the rows whose carried Hamerly / Elkan
     bounds fail (R28) and update the sums by the label changes: labels and step
     count equal the oracle's Lloyd run and the full-pass kernel's; centroids
     within 1e-13; the statistics show light steps that left most rows unread."""
-    Y, _ = _blobs(n, dim, K, 3 * n + K, spread=0.2)
+    Y, _ = _blobs(n, dim, K, 3 * n + K, spread=spread)
     if dt == "f32":
         Y = Y.astype(np.float32).astype(np.float64)
     rng = np.random.default_rng(11)
