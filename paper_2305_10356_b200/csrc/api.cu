@@ -75,10 +75,11 @@ struct Workspace {
   cudaStream_t fork_st = nullptr;            // p == 1: C4's Gram reduction beside the SpMM
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;
   double *part_cols = nullptr, *part_g4 = nullptr, *part_g2 = nullptr, *grams = nullptr;
-  double* state = nullptr;  // M, W [KP*KP each], alpha, beta, gg_prev [KP], colred [2KP]
+  double* part_gd = nullptr;  // f1 methods: column dots diag T, diag R' per block
+  double* state = nullptr;  // M, W [KP*KP each], alpha, beta, gg_prev [KP], colred, diagred [2KP]
   DevCtl* ctl = nullptr;
   unsigned long long* ctr = nullptr;  // SpMM work counter
-  int nb3 = 0, nb4 = 0, nb2 = 0;
+  int nb3 = 0, nb4 = 0, nb2 = 0, nbd = 0;
   cudaGraph_t g_iter = nullptr, g_refresh = nullptr, g_loop = nullptr;
   cudaGraphExec_t e_iter = nullptr, e_refresh = nullptr, e_loop = nullptr;
   cudaStream_t cap = nullptr;  // private stream used only for graph capture
@@ -105,11 +106,11 @@ struct Workspace {
     e_iter = e_refresh = e_loop = nullptr;
     g_iter = g_refresh = g_loop = nullptr;
     for (void* q : {X, AX, G, AV, Vg, Xg, sendbuf, (void*)part_cols, (void*)part_g4, (void*)part_g2,
-                    (void*)grams, (void*)state, (void*)ctl, (void*)ctr})
+                    (void*)part_gd, (void*)grams, (void*)state, (void*)ctl, (void*)ctr})
       dfree(q);
     ctr = nullptr;
     X = AX = G = AV = Vg = Xg = sendbuf = nullptr;
-    part_cols = part_g4 = part_g2 = grams = state = nullptr;
+    part_cols = part_g4 = part_g2 = part_gd = grams = state = nullptr;
     ctl = nullptr;
     have = false;
   }
@@ -826,8 +827,10 @@ static void ensure_workspace(ofsc_graph g, ofsc_dtype dt, int KP, cudaStream_t s
   dev_alloc((void**)&w.part_cols, (size_t)nbmax * 2 * KP * 8, s);
   dev_alloc((void**)&w.part_g4, (size_t)nbmax * 2 * KP * KP * 8, s);
   dev_alloc((void**)&w.part_g2, (size_t)w.nb2 * 2 * KP * KP * 8, s);
+  w.nbd = gram_diag_grid(nl);
+  dev_alloc((void**)&w.part_gd, (size_t)w.nbd * 2 * KP * 8, s);
   dev_alloc((void**)&w.grams, (size_t)4 * KP * KP * 8, s);
-  dev_alloc((void**)&w.state, (size_t)(2 * KP * KP + 5 * KP) * 8, s);
+  dev_alloc((void**)&w.state, (size_t)(2 * KP * KP + 7 * KP) * 8, s);
   dev_alloc((void**)&w.ctl, sizeof(DevCtl), s);
   dev_alloc((void**)&w.ctr, 4 * sizeof(unsigned long long), s);  // one per SpMM column pass
   w.dt = dt;
@@ -870,10 +873,12 @@ static IterParams make_params(ofsc_graph g, int method, const ofsc_opts& o, int 
   p.beta = p.alpha + KP;
   p.gg_prev = p.beta + KP;
   p.colred = p.gg_prev + KP;
+  p.diagred = p.colred + 2 * KP;
   p.grams = w.grams;
   p.part_cols = w.part_cols;
   p.part_g4 = w.part_g4;
   p.part_g2 = w.part_g2;
+  p.part_gd = w.part_gd;
   p.ctl = w.ctl;
   p.spmm_ctr = w.ctr;
   return p;
@@ -969,6 +974,19 @@ static bool pdl_ls() {   // OFSC_PDL_LS=0: the line-search kernel waits for C2b 
   return env == 1;
 }
 
+// OFM-f1 / TriOFM-f1: C2b forms only diag T and diag R' (their cubics, eq:f1-derivative
+// P:298-305 and eq:alphai-f1 P:315-322, read T and R' through T_ii and R'_ii, and
+// neither direction reads W = X^T A X, whose off-diagonal is then left as the last
+// refresh formed it).  OFSC_F1_DIAG=0: the full Gram pair for every method (A/B).
+static bool f1_diag(int method) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("OFSC_F1_DIAG");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1 && (method == OFSC_OFM_F1 || method == OFSC_TRIOFM_F1);
+}
+
 static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool refresh,
                           cudaStream_t s, Prof& pr) {
   Workspace& w = g->ws;
@@ -1031,20 +1049,33 @@ static void iteration_ops(ofsc_graph g, ofsc_dtype dt, const IterParams& p, bool
     });
   }
   pdl_next(pdl);
+  // the f1 methods need only diag T, diag R' (k_gram_diag: 3B streamed, no k x k products)
+  const bool diag = f1_diag(p.method);
   pr.ph(OFSC_PH_GRAM_STREAM, 1, [&] {
-    launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
+    if (diag)
+      launch_gram_diag(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_gd, &p.ctl->stop, w.nbd, s);
+    else
+      launch_gram_stream(dt, p.KP, g->n_local, p.V, w.X, w.AV, w.part_g2, 0, &p.ctl->stop, w.nb2, s);
   });
   if (fork_reduce) {
     // p == 1: C2b's partials reduced and the line search run by one kernel (its last CTA)
     OFSC_CUDA(cudaStreamWaitEvent(s, w.ev_f1, 0));
     // PDL edge from C2b (the joined Q/P reduction stays a full dependency)
     pdl_next(pdl && pdl_ls());
-    pr.ph(OFSC_PH_LINE_SEARCH, 1, [&] { launch_reduce_linesearch(p, w.part_g2, w.nb2, s); });
+    pr.ph(OFSC_PH_LINE_SEARCH, 1, [&] {
+      if (diag) launch_reduce_linesearch(p, w.part_gd, w.nbd, 1, s);
+      else launch_reduce_linesearch(p, w.part_g2, w.nb2, 0, s);
+    });
     return;
   }
   pr.ph(OFSC_PH_GRAM_REDUCE, 2, [&] {
     launch_reduce_partials(w.part_g4, w.nb4, 2 * p.KP * p.KP, w.grams, s);
-    launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, w.grams + 2 * p.KP * p.KP, s);
+    if (diag) {
+      launch_reduce_partials(w.part_gd, w.nbd, 2 * p.KP, p.diagred, s);
+      launch_expand_diag(p, s);
+    } else {
+      launch_reduce_partials(w.part_g2, w.nb2, 2 * p.KP * p.KP, w.grams + 2 * p.KP * p.KP, s);
+    }
   });
   pr.ph(OFSC_PH_COMM, 0, [&] { allreduce_d(g, w.grams, 4 * (size_t)p.KP * p.KP, s); });
   pr.ph(OFSC_PH_LINE_SEARCH, 1, [&] { launch_linesearch(p, s); });
@@ -1167,7 +1198,7 @@ ofsc_status ofsc_run_ex(ofsc_graph g, ofsc_method method, ofsc_dtype dt, const o
     OFSC_CUDA(cudaMemsetAsync(w.G, 0, blk, s));
     OFSC_CUDA(cudaMemsetAsync(w.AV, 0, blk, s));
     OFSC_CUDA(cudaMemsetAsync(w.Vg, 0, vg, s));
-    OFSC_CUDA(cudaMemsetAsync(w.state, 0, (size_t)(2 * KP * KP + 5 * KP) * 8, s));
+    OFSC_CUDA(cudaMemsetAsync(w.state, 0, (size_t)(2 * KP * KP + 7 * KP) * 8, s));
     OFSC_CUDA(cudaMemsetAsync(w.ctl, 0, sizeof(DevCtl), s));
     // init: AX = A X0, M = X0^T X0, W = X0^T A X0
     {

@@ -85,6 +85,8 @@ struct IterParams {
   double* part_cols;    // [nblk][2][KP]
   double* part_g4;      // [nblk][2][KP][KP] (Q, P)
   double* part_g2;      // [nblk][2][KP][KP] (T, R')
+  double* part_gd;      // [nblk][2][KP] column dots diag T, diag R' (f1 methods)
+  double* diagred;      // [2 KP] their reduction
   DevCtl* ctl;
   unsigned long long* spmm_ctr;  // [4] SpMM row counters, zeroed by k_beta (PDL chain: no memset)
   double* hist;         // [T][4]
@@ -181,6 +183,14 @@ int gram_stream_grid(ofsc_dtype dt, int KP, int64_t n);
 void launch_gram_stream(ofsc_dtype dt, int KP, int64_t n, const void* Zown, const void* Xown,
                         const void* Y, double* part, int mode, const int* stop, int nblk,
                         cudaStream_t st);
+// C2b for the f1 methods (OFM-f1, TriOFM-f1): only the column dots diag(Z^T Y),
+// diag(X^T Y) -> part[nblk][2][KP] (the f1 line search reads T, R' through their
+// diagonals alone; kernels_stream.cu k_gram_diag)
+int gram_diag_grid(int64_t n);
+void launch_gram_diag(ofsc_dtype dt, int KP, int64_t n, const void* Zown, const void* Xown,
+                      const void* Y, double* part, const int* stop, int nblk, cudaStream_t st);
+// T = diag(diagred[0..KP)), R' = diag(diagred[KP..2KP)) into grams[2..3] (1 CTA)
+void launch_expand_diag(const IterParams& p, cudaStream_t st);
 // plain SpMM (no Grams) into an arbitrary ld
 void launch_spmm_plain(ofsc_dtype dt, int k, int64_t n_local, int64_t own_off,
                        const int64_t* row_ptr, const int32_t* col, const double* s,
@@ -199,8 +209,10 @@ void launch_beta(const IterParams& p, int nblk, int reduced, cudaStream_t st);
 // exact line search + algebraic M, W update (1 CTA)
 void launch_linesearch(const IterParams& p, cudaStream_t st);
 // fixed-order reduction of nblk partial (T, R') arrays into grams[2..3] fused with the
-// line search: the last CTA to finish its slice runs it (p == 1)
-void launch_reduce_linesearch(const IterParams& p, const double* part, int nblk, cudaStream_t st);
+// line search: the last CTA to finish its slice runs it (p == 1).  diag: the partials
+// are k_gram_diag's column dots, expanded into diagonal T, R' before the line search
+void launch_reduce_linesearch(const IterParams& p, const double* part, int nblk, int diag,
+                              cudaStream_t st);
 // line-search hook: coefficients from given Grams (device), no ctl
 void launch_linesearch_hook(int method, int k, int KP, const double* grams, double* M, double* W,
                             double* alpha, int* codes, cudaStream_t st);

@@ -500,8 +500,28 @@ void launch_linesearch(const IterParams& p, cudaStream_t st) {
   OFSC_LAUNCH_CHECK();
 }
 
+// T = diag(d_T), R' = diag(d_R) as full KP x KP matrices (zero off the diagonal)
+// from the reduced column dots d = [d_T | d_R] of k_gram_diag (f1 methods).
+__device__ void expand_diag(const double* __restrict__ d, double* __restrict__ tr, int KP) {
+  for (int e = threadIdx.x; e < 2 * KP * KP; e += blockDim.x) {
+    const int q = e / (KP * KP), f = e % (KP * KP);
+    const int i = f / KP, j = f % KP;
+    tr[e] = i == j ? d[q * KP + i] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_expand_diag(IterParams p) {
+  if (p.ctl->stop) return;
+  expand_diag(p.diagred, p.grams + 2 * p.KP * p.KP, p.KP);
+}
+
+void launch_expand_diag(const IterParams& p, cudaStream_t st) {
+  k_expand_diag<<<1, 256, 0, st>>>(p);
+  OFSC_LAUNCH_CHECK();
+}
+
 __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const double* __restrict__ part,
-                                                           int nblk) {
+                                                           int nblk, int diag) {
   __shared__ double red[11 * 256];
   __shared__ LsOut out;
   __shared__ int s_last;
@@ -509,8 +529,9 @@ __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const d
   pdl_trigger();
   if (p.ctl->stop) return;
   const int KP = p.KP;
-  const int per_blk = 2 * KP * KP;
-  double* dst = p.grams + 2 * KP * KP;              // T, R'
+  // diag (f1 methods): the 2 KP column dots of k_gram_diag, else the full T, R'
+  const int per_blk = diag ? 2 * KP : 2 * KP * KP;
+  double* dst = diag ? p.diagred : p.grams + 2 * KP * KP;
   reduce_slice32(part, nblk, per_blk, dst, red);    // this CTA's 32 outputs (common.cuh)
   __threadfence();
   __syncthreads();
@@ -518,6 +539,10 @@ __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const d
   __syncthreads();
   if (!s_last) return;
   __threadfence();                                   // every slice of T, R' is visible
+  if (diag) {
+    expand_diag(p.diagred, p.grams + 2 * KP * KP, KP);
+    __syncthreads();
+  }
   const int t = p.ctl->iter;
   const double* g = p.grams;
   ls_core(p.method, p.k, KP, g, g + KP * KP, g + 2 * KP * KP, g + 3 * KP * KP, p.M, p.W,
@@ -537,10 +562,11 @@ __global__ void __launch_bounds__(256) k_reduce_linesearch(IterParams p, const d
   }
 }
 
-void launch_reduce_linesearch(const IterParams& p, const double* part, int nblk, cudaStream_t st) {
-  const int per_blk = 2 * p.KP * p.KP;
+void launch_reduce_linesearch(const IterParams& p, const double* part, int nblk, int diag,
+                              cudaStream_t st) {
+  const int per_blk = diag ? 2 * p.KP : 2 * p.KP * p.KP;
   launch_k(k_reduce_linesearch, dim3((per_blk + 31) / 32), dim3(256), 0, st, pdl_take(), p, part,
-           nblk);
+           nblk, diag);
 }
 
 __global__ void __launch_bounds__(256) k_linesearch_hook(int method, int k, int KP,

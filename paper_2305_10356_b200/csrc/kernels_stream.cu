@@ -9,6 +9,8 @@
 // completed on an mbarrier; results leave through TMA bulk stores from the same
 // stage buffers.  The N x k . k x k products and the Grams run on the fp64
 // tensor path (mma.sync m8n8k4 f64 = DMMA.8x8x4) from padded smem copies.
+#include <algorithm>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -1061,6 +1063,100 @@ void launch_gram_stream(ofsc_dtype dt, int KP, int64_t n, const void* Zown, cons
       else launch_gs<float, KPC, 1>(n, Zown, Xown, Y, part, stop, nblk, st);
     }
   });
+}
+
+// ---------------------------------------------------------------------------
+// C2b for the f1 methods: the diagonals of T = V^T AV and R' = X^T AV only.
+// OFM-f1 and TriOFM-f1 read T and R' through tr T, tr R' (eq:f1-derivative,
+// P:298-305) and T_ii, R'_ii (eq:alphai-f1) alone, and their directions
+// (eq:gradientf1, eq:gradientg1) never read W = X^T A X, so the k x k products of
+// the full Grams are not needed: this kernel streams V, X, AV once (3B, HBM-bound)
+// and forms the 2k column dots sum_r V_rc AV_rc, sum_r X_rc AV_rc in fp64.
+// A CTA owns a fixed contiguous row range; each thread owns two adjacent columns
+// of every RPI-th row of it; warps' sums meet in shared memory in a fixed order,
+// so the partials (part[blk][2][KP]) are deterministic for a given grid.
+// ---------------------------------------------------------------------------
+template <typename T, int KP>
+__global__ void __launch_bounds__(256) k_gram_diag(int64_t n, int64_t rows_per_blk,
+                                                   const T* __restrict__ Z,
+                                                   const T* __restrict__ X,
+                                                   const T* __restrict__ Y,
+                                                   double* __restrict__ part,
+                                                   const int* stop) {
+  constexpr int LPR = KP / 2;               // lanes per row (two columns each)
+  constexpr int RPI = 256 / LPR;            // rows per CTA step
+  using V2 = typename Vec2<T>::type;
+  __shared__ double red[RPI][2 * KP];
+  pdl_wait();      // PDL: the predecessor kernel has completed (sm100.cuh)
+  pdl_trigger();
+  if (stop && *stop) return;
+  const int sub = threadIdx.x / LPR, l = threadIdx.x % LPR;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk;
+  const int64_t r1 = min(n, r0 + rows_per_blk);
+  double t0 = 0, t1 = 0, q0 = 0, q1 = 0;
+  if (sub < RPI) {
+    int64_t r = r0 + sub;
+    constexpr int U = 4;                    // rows in flight per thread
+    for (; r + (U - 1) * RPI < r1; r += U * RPI) {
+      V2 z[U], x[U], y[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t o = (r + u * RPI) * KP + 2 * l;
+        z[u] = __ldcs(reinterpret_cast<const V2*>(Z + o));
+        x[u] = __ldcs(reinterpret_cast<const V2*>(X + o));
+        y[u] = __ldcs(reinterpret_cast<const V2*>(Y + o));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        t0 = fma((double)z[u].x, (double)y[u].x, t0);
+        t1 = fma((double)z[u].y, (double)y[u].y, t1);
+        q0 = fma((double)x[u].x, (double)y[u].x, q0);
+        q1 = fma((double)x[u].y, (double)y[u].y, q1);
+      }
+    }
+    for (; r < r1; r += RPI) {
+      const int64_t o = r * KP + 2 * l;
+      const V2 z = __ldcs(reinterpret_cast<const V2*>(Z + o));
+      const V2 x = __ldcs(reinterpret_cast<const V2*>(X + o));
+      const V2 y = __ldcs(reinterpret_cast<const V2*>(Y + o));
+      t0 = fma((double)z.x, (double)y.x, t0);
+      t1 = fma((double)z.y, (double)y.y, t1);
+      q0 = fma((double)x.x, (double)y.x, q0);
+      q1 = fma((double)x.y, (double)y.y, q1);
+    }
+    red[sub][2 * l] = t0;
+    red[sub][2 * l + 1] = t1;
+    red[sub][KP + 2 * l] = q0;
+    red[sub][KP + 2 * l + 1] = q1;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * KP; c += blockDim.x) {
+    double a = red[0][c];
+#pragma unroll 4
+    for (int s = 1; s < RPI; ++s) a += red[s][c];
+    part[(int64_t)blockIdx.x * 2 * KP + c] = a;
+  }
+}
+
+// two CTAs per SM (16 warps, 12 16-byte loads in flight per thread: enough to stream
+// at HBM rate) and at least 64 rows per CTA; few partials for the fixed-order reduction
+int gram_diag_grid(int64_t n) {
+  const int64_t g = std::min<int64_t>((int64_t)num_sms() * 2, (n + 63) / 64);
+  return (int)std::max<int64_t>(1, g);
+}
+
+void launch_gram_diag(ofsc_dtype dt, int KP, int64_t n, const void* Zown, const void* Xown,
+                      const void* Y, double* part, const int* stop, int nblk, cudaStream_t st) {
+  const int64_t per = (n + nblk - 1) / std::max(nblk, 1);
+  OFSC_DISPATCH_KP(KP, {
+    if (dt == OFSC_F64)
+      launch_k(k_gram_diag<double, KPC>, dim3(nblk), dim3(256), 0, st, pdl_take(), n, per,
+               (const double*)Zown, (const double*)Xown, (const double*)Y, part, stop);
+    else
+      launch_k(k_gram_diag<float, KPC>, dim3(nblk), dim3(256), 0, st, pdl_take(), n, per,
+               (const float*)Zown, (const float*)Xown, (const float*)Y, part, stop);
+  });
+  OFSC_LAUNCH_CHECK();
 }
 
 }  // namespace ofsc

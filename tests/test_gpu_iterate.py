@@ -281,12 +281,19 @@ def test_degenerate_graphs(case, method):
         # TriOFM's per-column cubics have mirror-image roots whose psi values tie
         # to rounding, so the two sides may take different (equally good) roots.
         # Then the first differing step must be such a three-root choice with
-        # equal psi, and the objective trajectories must agree.
+        # equal psi, and both trajectories must reach the unique minimum: for A = -I
+        # f1* = sum_{i>k} lambda_i^2 = n - k (Theorem 2's fixed points; pinned in
+        # test_oracle_methods) and f2* = sum_{i<=k} lambda_i = -k.  After a different
+        # root the two approach it at different rates (measured 1.4e-9 vs 1.8e-6
+        # from f1* = 46 after 10 iterations), so they are compared with the limit,
+        # not with each other.
         t = next(t for t in range(o.iters) if list(r.codes[t]) != list(o.codes[t])
                  or np.max(np.abs(r.alphas[t] - o.alphas[t])) > 1e-9 * np.max(np.abs(o.alphas[t])))
         assert method.startswith("tri") and case == "no_edges_A_is_minus_I", (case, method, t)
         assert any(8 <= c <= 10 for c in o.codes[t]), o.codes[t]
-        assert abs(r.history[-1, 0] - o.history[-1, 0]) <= 1e-8 * abs(o.history[-1, 0])
+        fstar = float(n - k) if method.endswith("f1") else -float(k)
+        for f in (o.history[-1, 0], r.history[-1, 0]):
+            assert abs(f - fstar) <= 1e-6 * abs(fstar), (f, fstar)
     g.close()
 
 
