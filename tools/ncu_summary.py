@@ -44,7 +44,8 @@ for r in rows:
     d[r[ix["Metric Name"]]] = v
 ids = sorted(launch)
 short = {"k_update_direction": "update_direction", "k_direction_gram": "direction_gram",
-         "k_spmm": "spmm", "k_gram_stream": "gram_stream", "k_beta": "beta",
+         "k_spmm": "spmm", "k_gram_stream": "gram_stream", "k_gram_diag": "gram_stream",
+         "k_beta": "beta",
          "k_linesearch": "line_search", "k_reduce_linesearch": "line_search",
          "k_reduce_partials": "gram_reduce"}
 # the last iteration: the last k_update_direction launch and what follows it
@@ -81,7 +82,8 @@ traffic = {"config": "c4", "kernel": "spmm", "dram_bytes_per_launch": per.get("s
            "dram_bytes_per_iteration": tot_bytes, "per_phase_dram_bytes": per,
            "ncu_iteration_ms": tot_ms,
            "source": f"{dst_dir}/ncu_iter_summary.json (ncu --clock-control none, c4 reordered, OFM-f2, last iteration of tools/run_iters.py)"}
-json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
+if "notraffic" not in sys.argv[3:]:      # the bench's traffic figure is the OFM-f2 run's
+    json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
 for e in summ:
     print(f"{e['kernel'][:40]:40s} {e.get('gpu__time_duration.sum', 0):8.3f} ms  "
           f"DRAM {(e.get('dram__bytes_read.sum', 0) + e.get('dram__bytes_write.sum', 0)) / 1e9:7.2f} GB  "
