@@ -252,7 +252,9 @@ enum {
   OFSC_PH_LINE_SEARCH = 5,      /* k x k: cubics, roots, alpha, M/W update */
   OFSC_PH_REFRESH = 6,          /* refresh iterations: X update, A X, X^T X, X^T A X */
   OFSC_PH_COMM = 7,             /* NCCL collectives (p > 1) */
-  OFSC_PH_GRAM_STREAM = 8,      /* C2b: T = V^T AV, R' = X^T AV (TMA-streamed, DMMA) */
+  OFSC_PH_GRAM_STREAM = 8,      /* C2b: T = V^T AV, R' = X^T AV (TMA-streamed, DMMA);
+                                   OFM-f1 / TriOFM-f1: diag T, diag R' only (their cubics,
+                                   P:298-305 and P:315-322, read no other entry) */
   OFSC_NUM_PHASES = 10
 };
 
