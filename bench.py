@@ -212,7 +212,9 @@ def kernel_rooflines(kern, algo, n, k, method, hbm_peak):
     flops = {
         "update_direction": (half if tri else full) * (1 if f1 else 2),
         "direction_gram": half + full,         # Q = V^T V (symmetric) + P = V^T X
-        "gram_stream": half + full,            # T = V^T A V (symmetric) + R' = X^T A V
+        # T = V^T A V (symmetric) + R' = X^T A V; the f1 methods form only their
+        # diagonals (k_gram_diag: 2 N k fp64 FMAs, no tensor products)
+        "gram_stream": 0 if f1 else half + full,
         "spmm": 0,
     }
     tpk, tsrc = dmma_peak()
@@ -525,6 +527,12 @@ def run_ours(args):
             r = timed_run(m)
             per[m] = round(K / (max_over_ranks(r["timed_ms"]) / 1e3), 3)
         out["per_method_it_s"] = per
+        # the f1 methods' C2b (k_gram_diag: diag T, diag R' only) against its ceiling
+        if args.method.endswith("f2"):
+            pf1 = timed_run("ofm_f1", profile=True)
+            kf1 = {PHASES[i]: {"ms_total": pf1["kernel_ms"][i], "launches": pf1["kernel_launches"][i]}
+                   for i in range(10) if pf1["kernel_launches"][i] or pf1["kernel_ms"][i]}
+            out["kernel_rooflines_ofm_f1"] = kernel_rooflines(kf1, algo, nl, k, "ofm_f1", hbm_peak)
 
     # --- e2e through the C ABI with pinned host buffers ---
     if not args.no_e2e:

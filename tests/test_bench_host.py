@@ -22,5 +22,9 @@ def test_kernel_rooflines_counts():
     assert kr["direction_gram"]["algorithmic_flops"] == n * k * (k + 1) + 2 * n * k * k
     tri = bench.kernel_rooflines(kern, algo, n, k, "triofm_f1", 1000.0)
     assert tri["update_direction"]["algorithmic_flops"] == n * k * (k + 1)
+    # the f1 methods' C2b forms only diag T, diag R' (no tensor products): HBM-bound 3B
+    assert tri["gram_stream"]["algorithmic_flops"] == 0 and tri["gram_stream"]["binding"] == "hbm"
+    assert abs(tri["gram_stream"]["hbm_gbs"] - 3 * B / 1e6) < 0.051
+    assert kr["gram_stream"]["algorithmic_flops"] == n * k * (k + 1) + 2 * n * k * k
     assert kr["spmm"]["binding"] == "hbm" and kr["spmm"]["fp64_tensor_frac"] == 0.0
     assert kr["fp64_tensor_peak_tflops"] > 30
