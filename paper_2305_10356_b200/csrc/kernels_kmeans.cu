@@ -1161,12 +1161,7 @@ k_kmeans_light(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
       __syncwarp();
       double b1 = CUDART_INF, b2 = CUDART_INF;
       int c1 = 0x7fffffff;
-      for (int c = lane; c < K; c += 32) {        // c increases: lowest index wins ties
-        double a = 0.0;
-        for (int d = 0; d < dim; ++d) {
-          const double diff = yr[d] - Ct[d * K + c];
-          a = a + diff * diff;
-        }
+      auto take = [&](double a, int c) {          // c increases: lowest index wins ties
         if (a < b1) {
           b2 = b1;
           b1 = a;
@@ -1174,6 +1169,30 @@ k_kmeans_light(int64_t n, int dim, const T* __restrict__ Y, int64_t ldy, int K,
         } else if (a < b2) {
           b2 = a;
         }
+      };
+      int c = lane;
+      // centroids c and c + 32 together: two independent d-ordered chains, loads
+      // unrolled ahead (each chain is the same sum, term by term, as one at a time)
+      for (; c + 32 < K; c += 64) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+        for (int d = 0; d < dim; ++d) {
+          const double y = yr[d];
+          const double e0 = y - Ct[d * K + c], e1 = y - Ct[d * K + c + 32];
+          a0 = a0 + e0 * e0;
+          a1 = a1 + e1 * e1;
+        }
+        take(a0, c);
+        take(a1, c + 32);
+      }
+      for (; c < K; c += 32) {
+        double a = 0.0;
+#pragma unroll 8
+        for (int d = 0; d < dim; ++d) {
+          const double diff = yr[d] - Ct[d * K + c];
+          a = a + diff * diff;
+        }
+        take(a, c);
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {             // lexicographic (distance, index) minimum
