@@ -673,6 +673,17 @@ void launch_spmm(ofsc_dtype dt, int KP, int64_t n_local, int64_t own_off, const 
   // a PDL launch (the iteration's SpMM right after C4) must not be preceded by a memset:
   // there k_beta has zeroed the counters (IterParams::spmm_ctr)
   const bool pdl_first = pdl_take();
+  // static interleaved row assignment (no global counter) when the gathered operand is
+  // below OFSC_SPMM_STATIC_KB kilobytes (default 16 MB): a graph that small stays in L2
+  // whatever the row order, and the counter costs an atomic round trip per chunk.
+  // Measured (profiles/r02/spmm_static_ab.jsonl, same sums): c1 32.6 -> 31.2 us, c2
+  // 70.0 -> 68.9 us per iteration; at c3 (102 MB, ~ the L2) the in-order window is
+  // needed (0.547 -> 0.605 ms static), so it keeps the counter.
+  {
+    const int64_t static_kb = env_int("OFSC_SPMM_STATIC_KB", 16384);
+    const int64_t op_kb = (n_local + own_off) * KP * (dt == OFSC_F64 ? 8 : 4) >> 10;
+    if (static_kb > 0 && op_kb < static_kb && phase == 0) ctr = nullptr;
+  }
   if (ctr && !pdl_first) OFSC_CUDA(cudaMemsetAsync(ctr, 0, passes * sizeof(unsigned long long), st));
   for (int ps = 0; ps < passes; ++ps) {
     const bool pdl = pdl_first && ps == 0;
