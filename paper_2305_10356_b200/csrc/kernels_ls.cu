@@ -503,11 +503,12 @@ void launch_linesearch(const IterParams& p, cudaStream_t st) {
 // T = diag(d_T), R' = diag(d_R) as full KP x KP matrices (zero off the diagonal)
 // from the reduced column dots d = [d_T | d_R] of k_gram_diag (f1 methods).
 __device__ void expand_diag(const double* __restrict__ d, double* __restrict__ tr, int KP) {
-  for (int e = threadIdx.x; e < 2 * KP * KP; e += blockDim.x) {
-    const int q = e / (KP * KP), f = e % (KP * KP);
-    const int i = f / KP, j = f % KP;
-    tr[e] = i == j ? d[q * KP + i] : 0.0;
-  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = w; i < KP; i += nw)                 // row i of T and of R' (no divisions)
+    for (int j = lane; j < KP; j += 32) {
+      tr[i * KP + j] = i == j ? d[i] : 0.0;
+      tr[KP * KP + i * KP + j] = i == j ? d[KP + i] : 0.0;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_expand_diag(IterParams p) {
