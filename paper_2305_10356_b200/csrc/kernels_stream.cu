@@ -41,21 +41,25 @@ struct StreamTile {
 // ring and the padded X', AX' tile (2 CTAs per SM).
 constexpr int kC3Stages = 2;
 
-template <typename T, int KP, int METHOD>
+// TR rows per tile, NS TMA stages (default 16 x 2; k_update_direction also has an
+// 8-row x 4-stage form, A/B knob OFSC_C3_TR8: the same bytes of ring in flight, each
+// stage released after half the work)
+template <typename T, int KP, int METHOD, int TR = kSTR, int NS = kC3Stages>
 struct C3Smem {
   static constexpr int LD = KP + 4;
-  static constexpr size_t xp = (size_t)kSTR * LD * 8;
-  static constexpr size_t arr = (size_t)kSTR * KP * sizeof(T);
+  static constexpr size_t xp = (size_t)TR * LD * 8;
+  static constexpr size_t arr = (size_t)TR * KP * sizeof(T);
   static constexpr size_t stage = 5 * arr;                          // X, AX, V, AV, G
-  static constexpr size_t bytes = 2 * xp + kC3Stages * stage + KP * 8 + kC3Stages * 8;
+  static constexpr size_t bytes = 2 * xp + NS * stage + KP * 8 + NS * 8;
 };
 
-template <typename T, int KP, int METHOD>
+template <typename T, int KP, int METHOD, int TR = kSTR, int NS = kC3Stages>
 __global__ void __launch_bounds__(kThreads, 2)
 k_update_direction(IterParams p, int apply_update) {
-  using S = C3Smem<T, KP, METHOD>;
+  using S = C3Smem<T, KP, METHOD, TR, NS>;
   constexpr int LD = S::LD;
-  constexpr int NS = kC3Stages;
+  constexpr int SUB = kSTR / TR;                 // TR-row tiles per 16-row tile
+  constexpr int RB = TR / 8;                     // 8-row DMMA blocks per tile
   constexpr bool TRI = (METHOD == OFSC_TRIOFM_F1 || METHOD == OFSC_TRIOFM_F2);
   constexpr bool F1 = (METHOD == OFSC_OFM_F1 || METHOD == OFSC_TRIOFM_F1);
   constexpr int NB = KP / 8;
@@ -65,22 +69,28 @@ k_update_direction(IterParams p, int apply_update) {
   if (p.ctl->stop) return;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* Xp = (double*)smraw;
-  double* AXp = Xp + kSTR * LD;
+  double* AXp = Xp + TR * LD;
   unsigned char* stg = smraw + 2 * S::xp;
   double* s_alpha = (double*)(stg + NS * S::stage);
   uint64_t* bar = (uint64_t*)(s_alpha + KP);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int64_t ntiles = (p.n_local + kSTR - 1) / kSTR;
+  // the CTA's it-th tile: part it % SUB of its (it / SUB)-th 16-row tile, so every
+  // thread visits the rows (and accumulates its column dots) in the same order for
+  // any TR: the results are bitwise those of the 16-row form
+  auto tile_row0 = [&](int64_t it) -> int64_t {
+    const int64_t t16 = blockIdx.x + (it / SUB) * (int64_t)gridDim.x;
+    return t16 < ntiles ? t16 * kSTR + (it % SUB) * TR : INT64_MAX;
+  };
   T* gX = (T*)p.X;
   T* gAX = (T*)p.AX;
   T* gG = (T*)p.G;
   const T* gV = (const T*)p.V;
   const T* gAV = (const T*)p.AV;
   auto arr = [&](int st, int a) { return (T*)(stg + st * S::stage + a * S::arr); };  // 0 X,1 AX,2 V,3 AV,4 G
-  auto issue = [&](int st, int64_t tile) {
-    const int64_t row0 = tile * kSTR;
-    const int rows = (int)imin64(kSTR, p.n_local - row0);
+  auto issue = [&](int st, int64_t row0) {
+    const int rows = (int)imin64(TR, p.n_local - row0);
     const uint32_t b = (uint32_t)rows * KP * sizeof(T);
     mbar_arrive_expect_tx(&bar[st], (apply_update ? 5u : 3u) * b);
     const int64_t off = row0 * KP;
@@ -100,8 +110,8 @@ k_update_direction(IterParams p, int apply_update) {
   __syncthreads();
   if (tid == 0)
     for (int s = 0; s < NS; ++s) {
-      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
-      if (tile < ntiles) issue(s, tile);
+      const int64_t r0 = tile_row0(s);
+      if (r0 < p.n_local) issue(s, r0);
     }
   // register-resident B fragments: B[k][n] = M[4 kk + tig][cb*8 + gid] (triu for TriOFM)
   const bool mma_warp = warp < NB;
@@ -115,11 +125,11 @@ k_update_direction(IterParams p, int apply_update) {
     if (!F1) bw[kk] = keep ? p.W[j * KP + c] : 0.0;
   }
   double gg[2] = {0.0, 0.0}, dg[2] = {0.0, 0.0};
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % NS;
-    const int64_t row0 = tile * kSTR;
-    const int rows = (int)imin64(kSTR, p.n_local - row0);
+  for (int64_t it = 0;; ++it) {
+    const int64_t row0 = tile_row0(it);
+    if (row0 >= p.n_local) break;
+    const int st = (int)(it % NS);
+    const int rows = (int)imin64(TR, p.n_local - row0);
     mbar_wait(&bar[st], (uint32_t)((it / NS) & 1));
     T* sX = arr(st, 0);
     T* sAX = arr(st, 1);
@@ -127,7 +137,7 @@ k_update_direction(IterParams p, int apply_update) {
     const T* sAV = arr(st, 3);
     T* sG = arr(st, 4);
     // phase A: X' = X + alpha V, AX' = AX + alpha AV (rounded to storage), padded copies
-    for (int e = tid; e < kSTR * KP; e += kThreads) {
+    for (int e = tid; e < TR * KP; e += kThreads) {
       const int r = e / KP, c = e % KP;
       double x = 0.0, ax = 0.0;
       if (r < rows) {
@@ -153,7 +163,9 @@ k_update_direction(IterParams p, int apply_update) {
     }
     if (mma_warp) {
       // phase B: G tile column block cb = f(X' M, X' W, AX' M) on DMMA (both row blocks)
-      double a1[2][2] = {{0, 0}, {0, 0}}, a2[2][2] = {{0, 0}, {0, 0}};
+      double a1[RB][2], a2[RB][2];
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) a1[rb][0] = a1[rb][1] = a2[rb][0] = a2[rb][1] = 0.0;
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         // TriOFM: triu(M), triu(W) vanish below the diagonal, so the k-steps whose rows
@@ -161,7 +173,7 @@ k_update_direction(IterParams p, int apply_update) {
         // zeros: skipped (warp-uniform), half of the products on average
         if (TRI && 4 * kk > 8 * cb + 7) continue;
 #pragma unroll
-        for (int rb = 0; rb < 2; ++rb) {
+        for (int rb = 0; rb < RB; ++rb) {
           const int o = (rb * 8 + gid) * LD + 4 * kk + tig;
           const double xa = Xp[o];
           if (F1) {
@@ -175,7 +187,7 @@ k_update_direction(IterParams p, int apply_update) {
       }
       // phase C: G, column dots, in-place store into the stage's G tile
 #pragma unroll
-      for (int rb = 0; rb < 2; ++rb) {
+      for (int rb = 0; rb < RB; ++rb) {
         const int r = rb * 8 + gid;
         if (r < rows) {
 #pragma unroll
@@ -202,8 +214,8 @@ k_update_direction(IterParams p, int apply_update) {
     if (tid == 0) {
       bulk_s2g(gG + row0 * KP, sG, (uint32_t)rows * KP * sizeof(T));
       bulk_commit();
-      const int64_t nxt = tile + (int64_t)NS * gridDim.x;
-      if (nxt < ntiles) {
+      const int64_t nxt = tile_row0(it + NS);
+      if (nxt < p.n_local) {
         bulk_wait_read_all();                     // stage st no longer read by the stores
         issue(st, nxt);
       }
@@ -458,16 +470,32 @@ static int c3_ws(int method) {
   return method == OFSC_OFM_F1 || method == OFSC_TRIOFM_F1;
 }
 
-template <typename T, int KP, int METHOD>
-static void launch_c3(const IterParams& p, int apply, int nblk, cudaStream_t s) {
-  const size_t smem = C3Smem<T, KP, METHOD>::bytes;
-  auto kern = k_update_direction<T, KP, METHOD>;
+// OFSC_C3_TR8=1: the 8-row x 4-stage form of the single-role C3 (same bits).  Measured
+// (profiles/r02/c3_tr8_ab.jsonl): the c4 OFM-f2 kernel 4.11-4.16 -> 3.84-3.93 ms in the
+// profiling pass, but graph-launched iterations within noise at c4 (14.25-14.30 vs
+// 14.39-14.44 ms OFM-f2, 14.22-14.26 vs 14.00-14.08 TriOFM-f2) and 4 % slower at c5
+// (KP = 48): not the default.
+static int c3_tr8() {
+  const char* e = getenv("OFSC_C3_TR8");
+  return (e && e[0] == '1') ? 1 : 0;
+}
+
+template <typename T, int KP, int METHOD, int TR, int NS>
+static void launch_c3_form(const IterParams& p, int apply, int nblk, cudaStream_t s) {
+  const size_t smem = C3Smem<T, KP, METHOD, TR, NS>::bytes;
+  auto kern = k_update_direction<T, KP, METHOD, TR, NS>;
   static bool set = false;
   if (!set) {
     OFSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = true;
   }
   launch_k(kern, dim3(nblk), dim3(kThreads), smem, s, pdl_take(), p, apply);
+}
+
+template <typename T, int KP, int METHOD>
+static void launch_c3(const IterParams& p, int apply, int nblk, cudaStream_t s) {
+  if (c3_tr8()) launch_c3_form<T, KP, METHOD, 8, 4>(p, apply, nblk, s);
+  else launch_c3_form<T, KP, METHOD, kSTR, kC3Stages>(p, apply, nblk, s);
 }
 
 static int stream_grid(int64_t n_rows, size_t smem_bytes) {

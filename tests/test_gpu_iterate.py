@@ -341,8 +341,9 @@ def test_c3_kernel_variants_bitwise(method, dtype, k, monkeypatch):
     partials, and so beta, depend on which tiles a CTA owns."""
     op, g, X0 = setup_wide(k)
     outs = []
-    for ws in ("0", "1"):
+    for ws, tr8 in (("0", "0"), ("1", "0"), ("0", "1")):   # + the 8-row x 4-stage form
         monkeypatch.setenv("OFSC_C3_WS", ws)
+        monkeypatch.setenv("OFSC_C3_TR8", tr8)
         X, r = gpu_run(g, method, X0, 10, dtype=dtype)
         outs.append((X, r.history))
     for X, h in outs[1:]:
