@@ -201,10 +201,13 @@ def dmma_peak():
     return 40.0, "nominal B200 fp64 tensor (no measured file)"
 
 
-def kernel_rooflines(kern, algo, n, k, method, hbm_peak):
+def kernel_rooflines(kern, algo, n, k, method, hbm_peak, sm_mhz=None):
     """Per big kernel: average launch time, HBM fraction on its algorithmic bytes and
     fp64-tensor fraction on the algorithmic flops of its DMMA products (triu and the
-    symmetric Grams count their upper triangle only); `binding` = the larger."""
+    symmetric Grams count their upper triangle only); `binding` = the larger.  The DMMA
+    peak was measured at the full 1965 MHz SM clock (64 FMA/clk/SM); with the run's
+    median SM clock under load (`sm_mhz`, power capped) the same pipe peaks lower, which
+    `fp64_tensor_frac_at_clock` reports beside the contract fraction."""
     tri = method.startswith("tri")
     f1 = method.endswith("f1")
     half = n * k * (k + 1)                     # one triangular / symmetric product
@@ -219,6 +222,10 @@ def kernel_rooflines(kern, algo, n, k, method, hbm_peak):
     }
     tpk, tsrc = dmma_peak()
     out = {"fp64_tensor_peak_tflops": tpk, "fp64_tensor_peak_source": tsrc, "hbm_peak_gbs": hbm_peak}
+    tpk_clk = tpk * sm_mhz / 1965.0 if sm_mhz else None
+    if tpk_clk:
+        out["fp64_tensor_peak_at_sm_clock_tflops"] = round(tpk_clk, 2)
+        out["sm_mhz"] = sm_mhz
     for name in ("spmm", "update_direction", "direction_gram", "gram_stream"):
         if name not in kern or not kern[name]["launches"]:
             continue
@@ -230,6 +237,8 @@ def kernel_rooflines(kern, algo, n, k, method, hbm_peak):
                      "fp64_tensor_tflops": round(tf, 2), "fp64_tensor_frac": round(ft, 4),
                      "binding": "hbm" if fh >= ft else "fp64_tensor",
                      "algorithmic_bytes": algo[name], "algorithmic_flops": flops[name]}
+        if tpk_clk:
+            out[name]["fp64_tensor_frac_at_clock"] = round(tf / tpk_clk, 4)
     return out
 
 
@@ -408,7 +417,7 @@ def run_ours(args):
                        "peak_source": gpk["source"]}
     # every big kernel against both of its ceilings: HBM (algorithmic bytes, above)
     # and the fp64 tensor pipe (DMMA.8x8x4; algorithmic flops of its products)
-    kr = kernel_rooflines(kern, algo, nl, k, args.method, hbm_peak)
+    kr = kernel_rooflines(kern, algo, nl, k, args.method, hbm_peak, (clocks or {}).get("sm_mhz"))
     it_dram = None
     if traffic and traffic.get("config") == cfg.name and world == 1 and args.dtype == "f64" \
             and traffic.get("dram_bytes_per_iteration"):
@@ -532,7 +541,8 @@ def run_ours(args):
             pf1 = timed_run("ofm_f1", profile=True)
             kf1 = {PHASES[i]: {"ms_total": pf1["kernel_ms"][i], "launches": pf1["kernel_launches"][i]}
                    for i in range(10) if pf1["kernel_launches"][i] or pf1["kernel_ms"][i]}
-            out["kernel_rooflines_ofm_f1"] = kernel_rooflines(kf1, algo, nl, k, "ofm_f1", hbm_peak)
+            out["kernel_rooflines_ofm_f1"] = kernel_rooflines(kf1, algo, nl, k, "ofm_f1", hbm_peak,
+                                                              (clocks or {}).get("sm_mhz"))
 
     # --- e2e through the C ABI with pinned host buffers ---
     if not args.no_e2e:

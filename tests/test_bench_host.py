@@ -28,3 +28,8 @@ def test_kernel_rooflines_counts():
     assert kr["gram_stream"]["algorithmic_flops"] == n * k * (k + 1) + 2 * n * k * k
     assert kr["spmm"]["binding"] == "hbm" and kr["spmm"]["fp64_tensor_frac"] == 0.0
     assert kr["fp64_tensor_peak_tflops"] > 30
+    # at a power-capped SM clock the DMMA pipe peaks proportionally lower
+    kc = bench.kernel_rooflines(kern, algo, n, k, "ofm_f2", 1000.0, 1965.0 / 2)
+    assert abs(kc["fp64_tensor_peak_at_sm_clock_tflops"] - kc["fp64_tensor_peak_tflops"] / 2) < 0.01
+    assert abs(kc["gram_stream"]["fp64_tensor_frac_at_clock"]
+               - 2 * kc["gram_stream"]["fp64_tensor_frac"]) < 1e-3
